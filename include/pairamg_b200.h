@@ -1,0 +1,216 @@
+/*
+ * pairamg_b200.h -- C-ABI drop-in boundary of the B200-native AMG-FCG hot path.
+ *
+ * The reference ("pairamg", /root/reference/proj) declares an exported C
+ * shared library `add_library(pairamg SHARED capi.cpp)` with public headers
+ * in proj/include (src/CMakeLists.txt:20-23) whose error categories are
+ * "mirrored by the C API" (types.hpp:12), but neither capi.cpp nor include/
+ * exists.  This header is therefore the C surface of the reference's C++
+ * hot-path API, one entry point per reference function it replaces:
+ *
+ *   pairamg_runtime_create     <- spawn_ranks / RankCtx        (runtime.hpp:71-136)
+ *   pairamg_setup              <- setup_hierarchy               (amg.hpp:84-85, amg.cpp:144-295)
+ *   pairamg_solve              <- pcg_solve (absent)
+ *   pairamg_vcycle             <- vcycle_apply                  (cycle.hpp:31-32, cycle.cpp:126-152)
+ *   pairamg_spmv               <- spmv_dist                     (dist.hpp:83-86, dist.cpp:241-312)
+ *   pairamg_hierarchy_info /
+ *   pairamg_level_info         <- Hierarchy::level_sizes/level_nnz/opc, hierarchy_summary
+ *                                                               (amg.hpp:49-58, amg.cpp:297-313)
+ *   pairamg_level_export       <- Level{A, w, m_l1}             (amg.hpp:27-38)
+ *   pairamg_prolongator_export <- Level::P_block                (amg.hpp:36)
+ *   pairamg_matching_export    <- SetupConfig::record / MatchingTrace (amg.hpp:13-23, amg.cpp:207-220)
+ *   pairamg_get_setup_stats    <- SetupStats                    (amg.hpp:40-47)
+ *   pairamg_status_name        <- error_code_name               (types.hpp:37-51)
+ *
+ * Conventions:
+ *  - One pairamg_runtime per rank; rank r drives GPU `device` from one host
+ *    thread.  With nranks > 1 the ranks are separate processes (or threads)
+ *    joined by an NCCL unique id obtained on one rank with
+ *    pairamg_comm_unique_id and broadcast by the caller.  Calls on a solver
+ *    are rank-collective, in the same order on every rank (runtime.hpp:84).
+ *  - Inputs use the reference's data layout: the rank's owned row block of a
+ *    row-block partition (Partition, runtime.hpp:15-28) in CSR with int64
+ *    row_ptr and GLOBAL int64 column ids, strictly ascending per row
+ *    (csr.hpp:10-11), f64 values.  Host arrays are caller-owned and copied
+ *    in; device state is library-owned.  *_device variants take pointers in
+ *    the runtime device's global memory instead.
+ *  - Every function returns a pairamg_status; on failure
+ *    pairamg_last_error() returns a thread-local message.  Status values are
+ *    0 = ok followed by the reference ErrorCode values in declaration order
+ *    (types.hpp:13-24).
+ *  - All calls are synchronous with respect to the host.
+ */
+#ifndef PAIRAMG_B200_H
+#define PAIRAMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAIRAMG_B200_ABI_VERSION 1
+
+/* ErrorCode (types.hpp:13-24), shifted by one; 0 = success. */
+typedef enum pairamg_status {
+    PAIRAMG_OK = 0,
+    PAIRAMG_INVALID_ARGUMENT = 1,
+    PAIRAMG_CONTRACT_VIOLATION = 2,
+    PAIRAMG_MISSING_ROW = 3,
+    PAIRAMG_SINGULAR_SMOOTHER = 4,
+    PAIRAMG_STAGNATION = 5,
+    PAIRAMG_BREAKDOWN = 6,
+    PAIRAMG_DEADLOCK = 7,
+    PAIRAMG_PARSE_ERROR = 8,
+    PAIRAMG_IO_ERROR = 9,
+    PAIRAMG_INTERNAL = 10
+} pairamg_status;
+
+/* SetupConfig (amg.hpp:17-23).  Matching ties are broken by the total order
+ * key(e) = (w(e), -min(e), -max(e)) (hard part 1). */
+typedef struct pairamg_setup_config {
+    int aggregation_exponent; /* s: pairwise steps composed per level (default 3) */
+    int64_t coarse_size_target; /* stop when global rows <= this (default 40) */
+    int max_levels;             /* default 40 */
+} pairamg_setup_config;
+
+/* CycleConfig (cycle.hpp:7-12). */
+typedef struct pairamg_cycle_config {
+    int pre_sweeps;      /* default 4 */
+    int post_sweeps;     /* default 4 */
+    int coarsest_sweeps; /* default 20 */
+    double relax_weight; /* default 1.0 */
+} pairamg_cycle_config;
+
+/* SolveConfig. */
+typedef struct pairamg_solve_config {
+    double rtol;   /* default 1e-6 */
+    int max_iters; /* default 1000 */
+    int precflag;  /* 1 = AMG V-cycle preconditioner, 0 = identity */
+} pairamg_solve_config;
+
+/* SolveStats.  history (optional, caller-owned, capacity
+ * history_cap) receives |r_k|/|r_0| for k = 0..iterations. */
+typedef struct pairamg_solve_stats {
+    int iterations;
+    int converged;
+    double final_relres;
+    double rnorm0;
+    double t_solve_s; /* device time of the solve (CUDA events) */
+    double* history;
+    int history_cap;
+} pairamg_solve_stats;
+
+/* SetupStats (amg.hpp:40-47) plus the hierarchy summary. */
+typedef struct pairamg_setup_stats {
+    double t_total, t_matching, t_spmm, t_spmm_comm; /* seconds */
+    int64_t matching_messages; /* transport activity during matching (contract: 0) */
+    int64_t rc_messages;       /* transport activity during R*C (contract: 0) */
+    int levels;
+    double opc;
+} pairamg_setup_stats;
+
+typedef struct pairamg_runtime pairamg_runtime;
+typedef struct pairamg_solver pairamg_solver;
+
+void pairamg_default_setup_config(pairamg_setup_config* cfg);
+void pairamg_default_cycle_config(pairamg_cycle_config* cfg);
+void pairamg_default_solve_config(pairamg_solve_config* cfg);
+
+const char* pairamg_status_name(pairamg_status s);
+const char* pairamg_last_error(void);
+int pairamg_abi_version(void);
+
+/* ---- runtime (spawn_ranks / RankCtx, runtime.hpp:71-136) ---- */
+/* 128-byte NCCL unique id, to be broadcast to every rank by the caller. */
+pairamg_status pairamg_comm_unique_id(uint8_t id[128]);
+/* nranks == 1: id may be NULL and no communicator is created. */
+pairamg_status pairamg_runtime_create(int device, int rank, int nranks, const uint8_t* id,
+                                      pairamg_runtime** out);
+pairamg_status pairamg_runtime_destroy(pairamg_runtime* rt);
+
+/* ---- solver ---- */
+pairamg_status pairamg_solver_create(pairamg_runtime* rt, pairamg_solver** out);
+pairamg_status pairamg_solver_destroy(pairamg_solver* s);
+
+/* setup_hierarchy(ctx, A, w0, cfg) (amg.hpp:84-85).  part_starts: nranks+1
+ * row starts of the fine partition (the rank owns [part_starts[rank],
+ * part_starts[rank+1])); n_local = that extent; row_ptr (n_local+1),
+ * col_idx/values (row_ptr[n_local]) in the reference CsrMatrix layout with
+ * global columns.  w0 may be NULL (all ones).  cfg may be NULL
+ * (defaults). */
+pairamg_status pairamg_setup(pairamg_solver* s, int64_t global_n, const int64_t* part_starts,
+                             int64_t n_local, const int64_t* row_ptr, const int64_t* col_idx,
+                             const double* values, const double* w0,
+                             const pairamg_setup_config* cfg);
+pairamg_status pairamg_setup_device(pairamg_solver* s, int64_t global_n, const int64_t* part_starts,
+                                    int64_t n_local, int64_t nnz_local, const int64_t* d_row_ptr,
+                                    const int64_t* d_col_idx, const double* d_values,
+                                    const double* d_w0, const pairamg_setup_config* cfg);
+
+/* Flexible PCG: u = A^{-1} b to rtol.  u holds u0 on entry
+ * (NULL-free: pass zeros for u0 = 0).  Owned block of b and u. */
+pairamg_status pairamg_solve(pairamg_solver* s, const double* b_local, double* u_local,
+                             const pairamg_cycle_config* ccfg, const pairamg_solve_config* scfg,
+                             pairamg_solve_stats* stats);
+pairamg_status pairamg_solve_device(pairamg_solver* s, const double* d_b_local, double* d_u_local,
+                                    const pairamg_cycle_config* ccfg,
+                                    const pairamg_solve_config* scfg, pairamg_solve_stats* stats);
+
+/* x = B r, one V-cycle from level 0 (vcycle_apply). is_device selects pointer space. */
+pairamg_status pairamg_vcycle(pairamg_solver* s, const double* r_local, double* x_local,
+                              const pairamg_cycle_config* ccfg, int is_device);
+/* y = A^k x on level k (spmv_dist with the level's halo plan). */
+pairamg_status pairamg_spmv(pairamg_solver* s, int level, const double* x_local, double* y_local,
+                            int is_device);
+
+/* ---- hierarchy introspection / parity export (all host arrays) ---- */
+pairamg_status pairamg_hierarchy_info(pairamg_solver* s, int* nlevels, double* opc);
+pairamg_status pairamg_level_info(pairamg_solver* s, int level, int64_t* global_rows,
+                                  int64_t* global_nnz, int64_t* row_begin, int64_t* local_rows,
+                                  int64_t* local_nnz);
+/* Owned rows of A^k: row_ptr (local_rows+1), col (local_nnz, GLOBAL ids,
+ * ascending), val; w^k and the l1 diagonal (local_rows).  Any pointer may be NULL. */
+pairamg_status pairamg_level_export(pairamg_solver* s, int level, int64_t* row_ptr, int64_t* col,
+                                    double* val, double* w, double* l1);
+/* Composed prolongator into level k >= 1: one entry per owned fine row of
+ * level k-1 (global coarse column, value). */
+pairamg_status pairamg_prolongator_export(pairamg_solver* s, int level, int64_t* col, double* val);
+/* Pairwise matching of setup step `step` on the owned block: *n receives the
+ * owned vertex count; mate (may be NULL) receives global mates, -1 = unmatched. */
+pairamg_status pairamg_num_matchings(pairamg_solver* s, int* steps);
+pairamg_status pairamg_matching_export(pairamg_solver* s, int step, int64_t* n, int64_t* mate);
+pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* out);
+
+/* ---- measurement hooks ---- */
+/* Per-kernel-class device time accumulated over the last solve (CUDA events
+ * around every launch of the class when timing was enabled):
+ * class 0 = level-0 smoother sweeps, 1 = level-0 residual, 2 = level-0 outer
+ * SpMV+dots, 3 = FCG vector updates. *launches and *ms may be NULL. */
+pairamg_status pairamg_set_kernel_timing(pairamg_solver* s, int enabled);
+pairamg_status pairamg_kernel_timing(pairamg_solver* s, int kclass, int64_t* launches, double* ms,
+                                     double* bytes_per_launch);
+/* Number of library kernel launches enqueued by the last solve. */
+pairamg_status pairamg_launch_count(pairamg_solver* s, int64_t* launches);
+/* cudaStream_t the solver launches on (for caller-side events). */
+void* pairamg_solver_stream(pairamg_solver* s);
+
+/* ---- problem generator ---- */
+/* Owned rows [row_begin, row_end) of the 7- or 27-point Poisson operator on an
+ * nx*ny*nz grid (lexicographic, x fastest; diagonal 6 or 26, off-diagonals -1).
+ * Host variant: caller allocates row_ptr (rows+1), col/val (nnz from
+ * pairamg_poisson_nnz).  Device variant: pointers in device memory. */
+int64_t pairamg_poisson_nnz(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t row_begin,
+                            int64_t row_end);
+pairamg_status pairamg_poisson_host(int stencil, int64_t nx, int64_t ny, int64_t nz,
+                                    int64_t row_begin, int64_t row_end, int64_t* row_ptr,
+                                    int64_t* col, double* val);
+pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny,
+                                      int64_t nz, int64_t row_begin, int64_t row_end,
+                                      int64_t* d_row_ptr, int64_t* d_col, double* d_val);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

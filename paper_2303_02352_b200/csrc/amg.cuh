@@ -1,0 +1,63 @@
+// amg.cuh -- the device-resident AMG hierarchy (Hierarchy / Level,
+// amg.hpp:27-58) and the entry points of setup.cu / solve.cu.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace pb {
+
+struct SetupConfig {  // SetupConfig (amg.hpp:17-23)
+    int aggregation_exponent = 3;
+    int64_t coarse_size_target = 40;
+    int max_levels = 40;
+};
+
+struct CycleConfig {  // CycleConfig (cycle.hpp:7-12)
+    int pre_sweeps = 4, post_sweeps = 4, coarsest_sweeps = 20;
+    double relax_weight = 1.0;
+};
+
+struct Level {
+    DevMatrix A;
+    DBuf<double> w;   // smooth vector
+    DBuf<double> l1;  // l1-Jacobi diagonal
+    // transfer from the finer level (k >= 1): block prolongator, local ids
+    DBuf<int32_t> pcol;  // per fine row of level k-1: local coarse row
+    DBuf<double> pval;
+    DBuf<int64_t> rrp;   // R = P^T: local coarse rows -> local fine rows ascending
+    DBuf<int32_t> rcol;
+    DBuf<double> rval;
+    // solve-time layout
+    Sell sell_all;           // all rows (no halo)
+    Sell sell_int, sell_bnd; // interior / boundary rows (halo present)
+    // V-cycle work vectors
+    DBuf<double> x, xt;      // n + n_halo (ping-pong iterates)
+    DBuf<double> rhs, res;   // n
+};
+
+struct SetupStats {  // SetupStats (amg.hpp:40-47)
+    double t_total = 0, t_matching = 0, t_spmm = 0, t_spmm_comm = 0;
+    int64_t matching_messages = 0, rc_messages = 0;
+};
+
+struct Hierarchy {
+    std::vector<std::unique_ptr<Level>> levels;
+    std::vector<int64_t> level_sizes, level_nnz;  // global
+    double opc = 1.0;
+    SetupStats stats;
+    std::vector<std::string> warnings;
+    std::vector<DBuf<int64_t>> matchings;  // owned-block global mates per pairwise step
+    int nl() const { return static_cast<int>(levels.size()); }
+};
+
+// setup_hierarchy (amg.cpp:144-295) on the device.  The input is the owned
+// row block in global-column CSR (device buffers, ownership taken).
+void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBuf<int64_t>&& rp,
+                     DBuf<int64_t>&& gcol, DBuf<double>&& val, int64_t nnz, const double* d_w0,
+                     const SetupConfig& cfg);
+
+}  // namespace pb

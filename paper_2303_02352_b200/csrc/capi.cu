@@ -1,0 +1,519 @@
+// capi.cu -- the extern "C" boundary (include/pairamg_b200.h).  Every entry
+// point converts pb::Error / CUDA / NCCL failures into a pairamg_status and a
+// thread-local message, mirroring the reference's exception-carrying
+// ErrorCode (types.hpp:13-35) and the absent capi.cpp (src/CMakeLists.txt:20).
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <string>
+
+#include "pairamg_b200.h"
+#include "solver.cuh"
+
+struct pairamg_runtime {
+    std::unique_ptr<pb::Runtime> rt;
+};
+
+struct pairamg_solver {
+    pairamg_runtime* rt = nullptr;
+    std::unique_ptr<pb::Solver> s;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+pairamg_status guarded(F&& f) {
+    try {
+        f();
+        return PAIRAMG_OK;
+    } catch (const pb::Error& e) {
+        g_err = e.what();
+        return e.code();
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("out of memory: ") + e.what();
+        return PAIRAMG_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PAIRAMG_INTERNAL;
+    }
+}
+
+pb::Solver& S(pairamg_solver* s) {
+    if (!s || !s->s) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null solver");
+    PB_CUDA(cudaSetDevice(s->rt->rt->device()));
+    return *s->s;
+}
+
+pb::SetupConfig setup_cfg(const pairamg_setup_config* c) {
+    pb::SetupConfig o;
+    if (c) {
+        o.aggregation_exponent = c->aggregation_exponent;
+        o.coarse_size_target = c->coarse_size_target;
+        o.max_levels = c->max_levels;
+    }
+    return o;
+}
+
+pb::CycleConfig cycle_cfg(const pairamg_cycle_config* c) {
+    pb::CycleConfig o;
+    if (c) {
+        o.pre_sweeps = c->pre_sweeps;
+        o.post_sweeps = c->post_sweeps;
+        o.coarsest_sweeps = c->coarsest_sweeps;
+        o.relax_weight = c->relax_weight;
+    }
+    return o;
+}
+
+// CsrMatrix::validate (csr.cpp:56-78) on the device: row_ptr[0] == 0,
+// non-decreasing, columns strictly increasing and in [0, ncols).
+__global__ void k_validate(const int64_t* __restrict__ rp, const int64_t* __restrict__ col, int64_t n,
+                           int64_t ncols, unsigned long long* __restrict__ bad_row) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t b = rp[i], e = rp[i + 1];
+    bool ok = (i > 0 || b == 0) && b <= e;
+    for (int64_t t = b; ok && t < e; ++t) {
+        const int64_t c = col[t];
+        if (c < 0 || c >= ncols || (t > b && col[t - 1] >= c)) ok = false;
+    }
+    if (!ok) atomicMin(bad_row, static_cast<unsigned long long>(i));
+}
+
+void check_partition(const pb::Runtime& rt, int64_t global_n, const int64_t* starts, int64_t n_local) {
+    if (!starts) pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: part_starts is null");
+    const int p = rt.nranks();
+    if (starts[0] != 0 || starts[p] != global_n)
+        pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup: partition does not span [0, global_n)");
+    for (int r = 0; r < p; ++r)
+        if (starts[r + 1] < starts[r]) pb::fail(PAIRAMG_INVALID_ARGUMENT, "partition: negative block size");
+    if (starts[rt.rank() + 1] - starts[rt.rank()] != n_local)
+        pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup: n_local does not match the partition extent");
+}
+
+void setup_impl(pairamg_solver* s, int64_t global_n, const int64_t* starts, int64_t n_local, int64_t nnz,
+                pb::DBuf<int64_t>&& rp, pb::DBuf<int64_t>&& col, pb::DBuf<double>&& val, const double* d_w0,
+                const pairamg_setup_config* cfg) {
+    pb::Solver& sv = S(s);
+    cudaStream_t st = sv.rt.stream();
+    check_partition(sv.rt, global_n, starts, n_local);
+    if (n_local > 0) {
+        pb::DBuf<unsigned long long> bad(1, st);
+        PB_CUDA(cudaMemsetAsync(bad.get(), 0xff, 8, st));
+        k_validate<<<pb::blocks_for(n_local, 256), 256, 0, st>>>(rp.get(), col.get(), n_local, global_n, bad.get());
+        PB_CHECK_LAUNCH();
+        unsigned long long h = 0;
+        int64_t last = 0;
+        PB_CUDA(cudaMemcpyAsync(&h, bad.get(), 8, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaMemcpyAsync(&last, rp.get() + n_local, 8, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+        if (h != ~0ULL)
+            pb::fail(PAIRAMG_CONTRACT_VIOLATION, "csr: invalid row " + std::to_string(h) +
+                                                     " (row_ptr order, or columns not strictly increasing / out of range)");
+        if (last != nnz) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "csr: row_ptr[nrows] != nnz");
+    }
+    std::vector<int64_t> part(starts, starts + sv.rt.nranks() + 1);
+    sv.setup(std::move(part), std::move(rp), std::move(col), std::move(val), nnz, d_w0, setup_cfg(cfg));
+}
+
+// ---- Poisson generator ----
+__host__ __device__ inline int row_len(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t row) {
+    const int64_t i = row % nx, j = (row / nx) % ny, k = row / (nx * ny);
+    const int ax = 1 + (i > 0) + (i < nx - 1), ay = 1 + (j > 0) + (j < ny - 1), az = 1 + (k > 0) + (k < nz - 1);
+    return stencil == 27 ? ax * ay * az : 1 + (ax - 1) + (ay - 1) + (az - 1);
+}
+
+__host__ __device__ inline void fill_row(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t row,
+                                         int64_t* col, double* val) {
+    const int64_t i = row % nx, j = (row / nx) % ny, k = row / (nx * ny);
+    int o = 0;
+    for (int dk = -1; dk <= 1; ++dk)
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int di = -1; di <= 1; ++di) {
+                const int man = (di != 0) + (dj != 0) + (dk != 0);
+                if (stencil == 7 && man > 1) continue;
+                const int64_t ii = i + di, jj = j + dj, kk = k + dk;
+                if (ii < 0 || ii >= nx || jj < 0 || jj >= ny || kk < 0 || kk >= nz) continue;
+                col[o] = ii + nx * (jj + ny * kk);
+                val[o] = man == 0 ? (stencil == 27 ? 26.0 : 6.0) : -1.0;
+                ++o;
+            }
+}
+
+__global__ void k_poisson_len(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t m,
+                              int64_t* __restrict__ rp) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < m) rp[r] = row_len(stencil, nx, ny, nz, b + r);
+    if (r == m) rp[m] = 0;
+}
+
+__global__ void k_poisson_fill(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t m,
+                               const int64_t* __restrict__ rp, int64_t* __restrict__ col, double* __restrict__ val) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < m) fill_row(stencil, nx, ny, nz, b + r, col + rp[r], val + rp[r]);
+}
+
+}  // namespace
+
+extern "C" {
+
+void pairamg_default_setup_config(pairamg_setup_config* c) {
+    c->aggregation_exponent = 3;
+    c->coarse_size_target = 40;
+    c->max_levels = 40;
+}
+
+void pairamg_default_cycle_config(pairamg_cycle_config* c) {
+    c->pre_sweeps = 4;
+    c->post_sweeps = 4;
+    c->coarsest_sweeps = 20;
+    c->relax_weight = 1.0;
+}
+
+void pairamg_default_solve_config(pairamg_solve_config* c) {
+    c->rtol = 1e-6;
+    c->max_iters = 1000;
+    c->precflag = 1;
+}
+
+const char* pairamg_status_name(pairamg_status s) {
+    switch (s) {  // error_code_name (types.hpp:37-51)
+        case PAIRAMG_OK: return "ok";
+        case PAIRAMG_INVALID_ARGUMENT: return "invalid_argument";
+        case PAIRAMG_CONTRACT_VIOLATION: return "contract_violation";
+        case PAIRAMG_MISSING_ROW: return "missing_row";
+        case PAIRAMG_SINGULAR_SMOOTHER: return "singular_smoother";
+        case PAIRAMG_STAGNATION: return "stagnation";
+        case PAIRAMG_BREAKDOWN: return "breakdown";
+        case PAIRAMG_DEADLOCK: return "deadlock";
+        case PAIRAMG_PARSE_ERROR: return "parse_error";
+        case PAIRAMG_IO_ERROR: return "io_error";
+        case PAIRAMG_INTERNAL: return "internal";
+    }
+    return "unknown";
+}
+
+const char* pairamg_last_error(void) { return g_err.c_str(); }
+int pairamg_abi_version(void) { return PAIRAMG_B200_ABI_VERSION; }
+
+pairamg_status pairamg_comm_unique_id(uint8_t id[128]) {
+    return guarded([&] {
+        ncclUniqueId uid;
+        PB_NCCL(ncclGetUniqueId(&uid));
+        std::memcpy(id, uid.internal, 128);
+    });
+}
+
+pairamg_status pairamg_runtime_create(int device, int rank, int nranks, const uint8_t* id, pairamg_runtime** out) {
+    return guarded([&] {
+        if (!out) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null out");
+        auto r = std::make_unique<pairamg_runtime>();
+        r->rt = std::make_unique<pb::Runtime>(device, rank, nranks, id);
+        *out = r.release();
+    });
+}
+
+pairamg_status pairamg_runtime_destroy(pairamg_runtime* rt) {
+    return guarded([&] { delete rt; });
+}
+
+pairamg_status pairamg_solver_create(pairamg_runtime* rt, pairamg_solver** out) {
+    return guarded([&] {
+        if (!rt || !out) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null runtime/out");
+        PB_CUDA(cudaSetDevice(rt->rt->device()));
+        auto s = std::make_unique<pairamg_solver>();
+        s->rt = rt;
+        s->s = std::make_unique<pb::Solver>(*rt->rt);
+        *out = s.release();
+    });
+}
+
+pairamg_status pairamg_solver_destroy(pairamg_solver* s) {
+    return guarded([&] {
+        if (s && s->rt) cudaSetDevice(s->rt->rt->device());
+        delete s;
+    });
+}
+
+pairamg_status pairamg_setup(pairamg_solver* s, int64_t global_n, const int64_t* part_starts, int64_t n_local,
+                             const int64_t* row_ptr, const int64_t* col_idx, const double* values, const double* w0,
+                             const pairamg_setup_config* cfg) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (n_local < 0 || !row_ptr) pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: bad CSR arguments");
+        cudaStream_t st = sv.rt.stream();
+        const int64_t nnz = row_ptr[n_local];
+        if (nnz < 0 || (nnz > 0 && (!col_idx || !values)))
+            pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: bad CSR arguments");
+        pb::DBuf<int64_t> rp(static_cast<size_t>(n_local + 1), st), col(static_cast<size_t>(nnz), st);
+        pb::DBuf<double> val(static_cast<size_t>(nnz), st), w(w0 ? static_cast<size_t>(n_local) : 0, st);
+        PB_CUDA(cudaMemcpyAsync(rp.get(), row_ptr, 8 * (n_local + 1), cudaMemcpyHostToDevice, st));
+        if (nnz) {
+            PB_CUDA(cudaMemcpyAsync(col.get(), col_idx, 8 * nnz, cudaMemcpyHostToDevice, st));
+            PB_CUDA(cudaMemcpyAsync(val.get(), values, 8 * nnz, cudaMemcpyHostToDevice, st));
+        }
+        if (w0 && n_local) PB_CUDA(cudaMemcpyAsync(w.get(), w0, 8 * n_local, cudaMemcpyHostToDevice, st));
+        setup_impl(s, global_n, part_starts, n_local, nnz, std::move(rp), std::move(col), std::move(val),
+                   w0 ? w.get() : nullptr, cfg);
+    });
+}
+
+pairamg_status pairamg_setup_device(pairamg_solver* s, int64_t global_n, const int64_t* part_starts, int64_t n_local,
+                                    int64_t nnz_local, const int64_t* d_row_ptr, const int64_t* d_col_idx,
+                                    const double* d_values, const double* d_w0, const pairamg_setup_config* cfg) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        cudaStream_t st = sv.rt.stream();
+        if (n_local < 0 || nnz_local < 0) pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: bad sizes");
+        pb::DBuf<int64_t> rp(static_cast<size_t>(n_local + 1), st), col(static_cast<size_t>(nnz_local), st);
+        pb::DBuf<double> val(static_cast<size_t>(nnz_local), st);
+        PB_CUDA(cudaMemcpyAsync(rp.get(), d_row_ptr, 8 * (n_local + 1), cudaMemcpyDeviceToDevice, st));
+        if (nnz_local) {
+            PB_CUDA(cudaMemcpyAsync(col.get(), d_col_idx, 8 * nnz_local, cudaMemcpyDeviceToDevice, st));
+            PB_CUDA(cudaMemcpyAsync(val.get(), d_values, 8 * nnz_local, cudaMemcpyDeviceToDevice, st));
+        }
+        setup_impl(s, global_n, part_starts, n_local, nnz_local, std::move(rp), std::move(col), std::move(val), d_w0,
+                   cfg);
+    });
+}
+
+pairamg_status pairamg_solve_device(pairamg_solver* s, const double* d_b, double* d_u, const pairamg_cycle_config* ccfg,
+                                    const pairamg_solve_config* scfg, pairamg_solve_stats* stats) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        pairamg_solve_config sc;
+        pairamg_default_solve_config(&sc);
+        if (scfg) sc = *scfg;
+        sv.solve(d_b, d_u, cycle_cfg(ccfg), sc.rtol, sc.max_iters, sc.precflag != 0, stats);
+    });
+}
+
+pairamg_status pairamg_solve(pairamg_solver* s, const double* b, double* u, const pairamg_cycle_config* ccfg,
+                             const pairamg_solve_config* scfg, pairamg_solve_stats* stats) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "solve: setup not run");
+        cudaStream_t st = sv.rt.stream();
+        const int64_t n = sv.h.levels[0]->A.n;
+        pb::DBuf<double> db(static_cast<size_t>(n), st), du(static_cast<size_t>(n), st);
+        if (n) {
+            PB_CUDA(cudaMemcpyAsync(db.get(), b, 8 * n, cudaMemcpyHostToDevice, st));
+            PB_CUDA(cudaMemcpyAsync(du.get(), u, 8 * n, cudaMemcpyHostToDevice, st));
+        }
+        pairamg_solve_config sc;
+        pairamg_default_solve_config(&sc);
+        if (scfg) sc = *scfg;
+        sv.solve(db.get(), du.get(), cycle_cfg(ccfg), sc.rtol, sc.max_iters, sc.precflag != 0, stats);
+        if (n) PB_CUDA(cudaMemcpyAsync(u, du.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+pairamg_status pairamg_vcycle(pairamg_solver* s, const double* r, double* x, const pairamg_cycle_config* ccfg,
+                              int is_device) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "vcycle: setup not run");
+        cudaStream_t st = sv.rt.stream();
+        const int64_t n = sv.h.levels[0]->A.n;
+        if (is_device) {
+            sv.vcycle(r, x, cycle_cfg(ccfg));
+            return;
+        }
+        pb::DBuf<double> dr(static_cast<size_t>(n), st), dx(static_cast<size_t>(n), st);
+        if (n) PB_CUDA(cudaMemcpyAsync(dr.get(), r, 8 * n, cudaMemcpyHostToDevice, st));
+        sv.vcycle(dr.get(), dx.get(), cycle_cfg(ccfg));
+        if (n) PB_CUDA(cudaMemcpyAsync(x, dx.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+pairamg_status pairamg_spmv(pairamg_solver* s, int level, const double* x, double* y, int is_device) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "spmv: setup not run");
+        if (level < 0 || level >= sv.h.nl()) pb::fail(PAIRAMG_INVALID_ARGUMENT, "spmv: level out of range");
+        cudaStream_t st = sv.rt.stream();
+        const int64_t n = sv.h.levels[level]->A.n;
+        if (is_device) {
+            sv.spmv(level, x, y);
+            return;
+        }
+        pb::DBuf<double> dx(static_cast<size_t>(n), st), dy(static_cast<size_t>(n), st);
+        if (n) PB_CUDA(cudaMemcpyAsync(dx.get(), x, 8 * n, cudaMemcpyHostToDevice, st));
+        sv.spmv(level, dx.get(), dy.get());
+        if (n) PB_CUDA(cudaMemcpyAsync(y, dy.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+pairamg_status pairamg_hierarchy_info(pairamg_solver* s, int* nlevels, double* opc) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        if (nlevels) *nlevels = sv.h.nl();
+        if (opc) *opc = sv.h.opc;
+    });
+}
+
+pairamg_status pairamg_level_info(pairamg_solver* s, int level, int64_t* global_rows, int64_t* global_nnz,
+                                  int64_t* row_begin, int64_t* local_rows, int64_t* local_nnz) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        if (level < 0 || level >= sv.h.nl()) pb::fail(PAIRAMG_INVALID_ARGUMENT, "level out of range");
+        const pb::DevMatrix& A = sv.h.levels[level]->A;
+        if (global_rows) *global_rows = sv.h.level_sizes[level];
+        if (global_nnz) *global_nnz = sv.h.level_nnz[level];
+        if (row_begin) *row_begin = A.row_begin;
+        if (local_rows) *local_rows = A.n;
+        if (local_nnz) *local_nnz = A.nnz;
+    });
+}
+
+pairamg_status pairamg_level_export(pairamg_solver* s, int level, int64_t* row_ptr, int64_t* col, double* val,
+                                    double* w, double* l1) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        if (level < 0 || level >= sv.h.nl()) pb::fail(PAIRAMG_INVALID_ARGUMENT, "level out of range");
+        const pb::Level& L = *sv.h.levels[level];
+        cudaStream_t st = sv.rt.stream();
+        const int64_t n = L.A.n, nnz = L.A.nnz;
+        if (row_ptr) PB_CUDA(cudaMemcpyAsync(row_ptr, L.A.rp.get(), 8 * (n + 1), cudaMemcpyDeviceToHost, st));
+        if (col && nnz) {
+            pb::DBuf<int64_t> g(static_cast<size_t>(nnz), st);
+            pb::global_columns(L.A, g.get(), st);
+            PB_CUDA(cudaMemcpyAsync(col, g.get(), 8 * nnz, cudaMemcpyDeviceToHost, st));
+            PB_CUDA(cudaStreamSynchronize(st));
+        }
+        if (val && nnz) PB_CUDA(cudaMemcpyAsync(val, L.A.val.get(), 8 * nnz, cudaMemcpyDeviceToHost, st));
+        if (w && n) PB_CUDA(cudaMemcpyAsync(w, L.w.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        if (l1 && n) PB_CUDA(cudaMemcpyAsync(l1, L.l1.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+pairamg_status pairamg_prolongator_export(pairamg_solver* s, int level, int64_t* col, double* val) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        if (level < 1 || level >= sv.h.nl()) pb::fail(PAIRAMG_INVALID_ARGUMENT, "prolongator level must be >= 1");
+        const pb::Level& C = *sv.h.levels[level];
+        const int64_t nf = sv.h.levels[level - 1]->A.n;
+        cudaStream_t st = sv.rt.stream();
+        if (col && nf) {
+            std::vector<int32_t> lc(static_cast<size_t>(nf));
+            PB_CUDA(cudaMemcpyAsync(lc.data(), C.pcol.get(), 4 * nf, cudaMemcpyDeviceToHost, st));
+            PB_CUDA(cudaStreamSynchronize(st));
+            for (int64_t i = 0; i < nf; ++i) col[i] = C.A.row_begin + lc[static_cast<size_t>(i)];
+        }
+        if (val && nf) PB_CUDA(cudaMemcpyAsync(val, C.pval.get(), 8 * nf, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+pairamg_status pairamg_num_matchings(pairamg_solver* s, int* steps) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        *steps = static_cast<int>(sv.h.matchings.size());
+    });
+}
+
+pairamg_status pairamg_matching_export(pairamg_solver* s, int step, int64_t* n, int64_t* mate) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (step < 0 || step >= static_cast<int>(sv.h.matchings.size()))
+            pb::fail(PAIRAMG_INVALID_ARGUMENT, "matching step out of range");
+        const auto& m = sv.h.matchings[static_cast<size_t>(step)];
+        if (n) *n = static_cast<int64_t>(m.size());
+        if (mate && m.size()) {
+            PB_CUDA(cudaMemcpyAsync(mate, m.get(), 8 * m.size(), cudaMemcpyDeviceToHost, sv.rt.stream()));
+            PB_CUDA(cudaStreamSynchronize(sv.rt.stream()));
+        }
+    });
+}
+
+pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* out) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        const auto& st = sv.h.stats;
+        out->t_total = st.t_total;
+        out->t_matching = st.t_matching;
+        out->t_spmm = st.t_spmm;
+        out->t_spmm_comm = st.t_spmm_comm;
+        out->matching_messages = st.matching_messages;
+        out->rc_messages = st.rc_messages;
+        out->levels = sv.h.nl();
+        out->opc = sv.h.opc;
+    });
+}
+
+pairamg_status pairamg_set_kernel_timing(pairamg_solver* s, int enabled) {
+    return guarded([&] { S(s).timing = enabled != 0; });
+}
+
+pairamg_status pairamg_kernel_timing(pairamg_solver* s, int kclass, int64_t* launches, double* ms,
+                                     double* bytes_per_launch) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (kclass < 0 || kclass >= 4) pb::fail(PAIRAMG_INVALID_ARGUMENT, "kernel class out of range");
+        if (launches) *launches = sv.ktime[kclass].launches;
+        if (ms) *ms = sv.ktime[kclass].ms;
+        if (bytes_per_launch) *bytes_per_launch = sv.ktime[kclass].bytes_per_launch;
+    });
+}
+
+pairamg_status pairamg_launch_count(pairamg_solver* s, int64_t* launches) {
+    return guarded([&] { *launches = S(s).last_launches; });
+}
+
+void* pairamg_solver_stream(pairamg_solver* s) {
+    if (!s || !s->s) return nullptr;
+    return reinterpret_cast<void*>(s->s->rt.stream());
+}
+
+int64_t pairamg_poisson_nnz(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t e) {
+    int64_t z = 0;
+    for (int64_t r = b; r < e; ++r) z += row_len(stencil, nx, ny, nz, r);
+    return z;
+}
+
+pairamg_status pairamg_poisson_host(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t e,
+                                    int64_t* row_ptr, int64_t* col, double* val) {
+    return guarded([&] {
+        if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
+        if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
+        row_ptr[0] = 0;
+        for (int64_t r = b; r < e; ++r) {
+            fill_row(stencil, nx, ny, nz, r, col + row_ptr[r - b], val + row_ptr[r - b]);
+            row_ptr[r - b + 1] = row_ptr[r - b] + row_len(stencil, nx, ny, nz, r);
+        }
+    });
+}
+
+pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b,
+                                      int64_t e, int64_t* d_rp, int64_t* d_col, double* d_val) {
+    return guarded([&] {
+        if (!rt) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null runtime");
+        if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
+        if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
+        PB_CUDA(cudaSetDevice(rt->rt->device()));
+        cudaStream_t st = rt->rt->stream();
+        const int64_t m = e - b;
+        k_poisson_len<<<pb::blocks_for(m + 1, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp);
+        PB_CHECK_LAUNCH();
+        size_t bytes = 0;
+        PB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, d_rp, d_rp, m + 1, st));
+        pb::DBuf<uint8_t> tmp(bytes ? bytes : 1, st);
+        PB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, d_rp, d_rp, m + 1, st));
+        if (m) k_poisson_fill<<<pb::blocks_for(m, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp, d_col, d_val);
+        PB_CHECK_LAUNCH();
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// common.cuh -- shared infrastructure of the B200 AMG-FCG library: error
+// model (the reference ErrorCode taxonomy, types.hpp:13-35), stream-ordered
+// device buffers, launch helpers and exact-rounding FP64 primitives.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "pairamg_b200.h"
+
+namespace pb {
+
+// pairamg::Error (types.hpp:26-35) with the C status attached.
+class Error : public std::runtime_error {
+public:
+    Error(pairamg_status code, const std::string& what) : std::runtime_error(what), code_(code) {}
+    pairamg_status code() const noexcept { return code_; }
+
+private:
+    pairamg_status code_;
+};
+
+[[noreturn]] inline void fail(pairamg_status code, const std::string& msg) { throw Error(code, msg); }
+
+#define PB_CUDA(call)                                                                          \
+    do {                                                                                       \
+        cudaError_t e__ = (call);                                                              \
+        if (e__ != cudaSuccess)                                                                \
+            ::pb::fail(PAIRAMG_INTERNAL, std::string("CUDA error ") + cudaGetErrorString(e__) + \
+                                             " at " __FILE__ ":" + std::to_string(__LINE__));  \
+    } while (0)
+
+#define PB_CHECK_LAUNCH() PB_CUDA(cudaGetLastError())
+
+constexpr int kSmCount = 148;  // B200: 148 SMs on two dies
+
+inline int blocks_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 0x7fffffffLL) fail(PAIRAMG_INTERNAL, "grid too large");
+    return static_cast<int>(b);
+}
+
+// Stream-ordered device buffer (cudaMallocAsync on the solver stream; the
+// device's default memory pool keeps freed blocks cached, so the many setup
+// temporaries do not hit the driver allocator).
+template <typename T>
+class DBuf {
+public:
+    DBuf() = default;
+    DBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+    ~DBuf() { reset(); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(size_t n, cudaStream_t s) {
+        reset();
+        s_ = s;
+        n_ = n;
+        if (n) PB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    }
+    void reset() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    void zero(cudaStream_t s) {
+        if (n_) PB_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+    operator T*() const { return p_; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Exactly rounded FP64 (no contraction), matching the reference objects,
+// which contain no FMA.  The library is also
+// compiled with --fmad=false; these make the intent explicit at call sites.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+}  // namespace pb

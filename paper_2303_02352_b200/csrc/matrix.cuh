@@ -1,0 +1,97 @@
+// matrix.cuh -- device data layout of one rank's share of a hierarchy level.
+//
+// HBM layout (per level, per rank):
+//   DevMatrix  : owned rows in CSR, int64 row_ptr, int32 LOCAL column ids
+//                ([0,n) owned, [n, n+n_halo) halo slots), f64 values.  Each
+//                row keeps the reference's column order (ascending GLOBAL id,
+//                csr.hpp:10-11), so every per-row sum runs in the reference
+//                order (dist.cpp:277-300).
+//   HaloPlan   : HaloPlan (dist.hpp:50-65): sorted global ids of the halo
+//                slots (recv_ids), per-peer receive ranges, per-peer send
+//                lists of owned local ids, a packed send buffer.
+//   Sell       : the solve-time copy of a row set in SELL-32 (slices of 32
+//                consecutive rows stored column-major, padded per slice to
+//                the slice's longest row, pad column = -1).  One warp owns a
+//                slice, one lane a row: every val/col load of a warp is one
+//                contiguous 256 B / 128 B transaction and the lane's sum runs
+//                over its row in CSR order, bitwise equal to spmv_local.
+//                Interior and boundary rows get separate Sells so halo
+//                exchange overlaps interior rows (dist.cpp:303-311).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "runtime.cuh"
+
+namespace pb {
+
+struct HaloPlan {
+    int64_t n_halo = 0;
+    DBuf<int64_t> recv_gid;                  // sorted global ids of the halo slots
+    std::vector<int> recv_peers;             // source ranks, ascending
+    std::vector<int64_t> recv_off;           // npeers+1 offsets into the halo region
+    std::vector<int> send_peers;             // destination ranks, ascending
+    std::vector<int64_t> send_off;           // npeers+1 offsets into send_idx
+    DBuf<int32_t> send_idx;                  // owned local ids to pack, per peer
+    DBuf<double> send_buf;                   // packed values
+    DBuf<int64_t> send_buf_i64;              // packed ids (setup-time P exchange)
+    bool has_traffic() const { return n_halo > 0 || !send_peers.empty(); }
+};
+
+struct DevMatrix {
+    int64_t n = 0;          // owned rows
+    int64_t nnz = 0;
+    int64_t row_begin = 0;  // global id of owned row 0 (= owned column range begin)
+    int64_t n_global = 0;
+    std::vector<int64_t> starts;  // row partition (nranks+1)
+    DBuf<int64_t> rp;
+    DBuf<int32_t> col;
+    DBuf<double> val;
+    HaloPlan halo;
+    DBuf<int32_t> boundary_rows;  // rows with at least one halo column (ascending)
+    DBuf<int32_t> interior_rows;  // the others (ascending); empty when no halo
+    int64_t n_boundary = 0;
+};
+
+struct Sell {
+    int64_t nrows = 0, nslices = 0, padded_nnz = 0;
+    DBuf<int64_t> slice_off;  // nslices+1, in elements (multiples of 32)
+    DBuf<int32_t> col;        // padded local column ids, -1 = pad
+    DBuf<double> val;
+    DBuf<int32_t> rows;       // row id of each SELL row; empty = identity
+};
+
+// ---- sparse.cu ----
+// Global-column CSR (int64 row_ptr / col, device) of the owned rows ->
+// DevMatrix with local columns and a halo plan (build_rows_to_receive +
+// exchange_requests + build_spmv_plan, dist.cpp:158-233).  Takes ownership
+// of the buffers.
+void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gcol,
+              DBuf<double>&& val, int64_t nnz);
+// Global ids of M's columns (export).
+void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s);
+// SELL-32 copy of the rows listed in `rows` (nullptr = all rows).
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s);
+// l1_diagonal_dist (cycle.cpp:55-75); throws singular_smoother.
+void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s);
+// x_halo[h] <- owner's x for every halo slot (pack, NCCL send/recv). On `s`.
+void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_halo, cudaStream_t s);
+// Same for an (int64, f64) pair of per-row arrays (setup-time P exchange).
+void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_t* a_halo,
+                        const double* b_owned, double* b_halo, cudaStream_t s);
+
+// Apply kernels on a Sell (all sums in CSR order, exactly rounded):
+//   SPMV   : y[row] = A x
+//   JACOBI : y[row] = x[row] + (omega*(r[row] - (A x)))/d[row]
+//   RESID  : y[row] = r[row] - (A x)
+enum SellOp { kSpmv = 0, kJacobi = 1, kResid = 2 };
+void sell_apply(const Sell& S, int op, const double* x, double* y, const double* r, const double* d,
+                double omega, cudaStream_t s);
+// v = A w plus per-block partials of (w.r, w.v, w.q) (FCG lines 10-13).
+// Returns the number of partial triples written.
+int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
+                   double* partials, int max_blocks, cudaStream_t s);
+int sell_dots_grid(const Sell& S);
+
+}  // namespace pb

@@ -1,0 +1,547 @@
+// solve.cu -- the solve path: the symmetric V-cycle (vcycle_apply,
+// cycle.cpp:126-152) with l1-Jacobi sweeps (cycle.cpp:77-102), local
+// restriction / prolongation (cycle.cpp:104-124), and Notay's flexible CG
+// (Alg. 1) with one fused dot-triple reduction and one
+// fused four-vector update per iteration.  One whole FCG iteration (all
+// levels, halos, reductions) is captured once into a CUDA graph and
+// replayed; the host reads 80 bytes of device scalars per iteration for the
+// stopping test.
+#include <cmath>
+#include <cstring>
+
+#include "solver.cuh"
+
+namespace pb {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+
+// x = (omega*r)/d : the zero-start sweep (cycle.cpp:89-93)
+__global__ void k_zero_start(const double* __restrict__ r, const double* __restrict__ d,
+                             double* __restrict__ x, int64_t n, double omega) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = ddiv(dmul(omega, r[i]), d[i]);
+}
+
+// restrict_to_coarse (cycle.cpp:104-115): rc_c = 0.0 + sum R_ci res_i, fine ascending
+__global__ void k_restrict(const int64_t* __restrict__ rrp, const int32_t* __restrict__ rcol,
+                           const double* __restrict__ rval, const double* __restrict__ res,
+                           double* __restrict__ rc, int64_t nc) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double s = 0.0;
+    for (int64_t t = rrp[c]; t < rrp[c + 1]; ++t) s = dadd(s, dmul(rval[t], res[rcol[t]]));
+    rc[c] = s;
+}
+
+// prolongate_add (cycle.cpp:117-124): x_i = x_i + p_i * e_agg(i)
+__global__ void k_prolong(const int32_t* __restrict__ pcol, const double* __restrict__ pval,
+                          const double* __restrict__ e, double* __restrict__ x, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = dadd(x[i], dmul(pval[i], e[pcol[i]]));
+}
+
+// Block partials of (w.r, w.v, w.q) for the halo path (grid-stride, fixed grid).
+__global__ void __launch_bounds__(kRedThreads)
+    k_dots3(const double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ r,
+            const double* __restrict__ q, int64_t n, double* __restrict__ partials) {
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double wi = w[i];
+        sa = dadd(sa, dmul(wi, r[i]));
+        sb = dadd(sb, dmul(wi, v[i]));
+        sg = dadd(sg, dmul(wi, q[i]));
+    }
+    __shared__ double red[3][kRedThreads / 32];
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int k = 0; k < kRedThreads / 32; ++k) acc = dadd(acc, red[threadIdx.x][k]);
+        partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}
+
+// FCG vector updates (Alg. 1 lines 16-19), op order shared with the oracle:
+//   d = w - c d ; q = v - c q ; u = u + a d ; r = r - a q ;  plus |r|^2 partials.
+__global__ void __launch_bounds__(kRedThreads)
+    k_update(const double* __restrict__ w, double* __restrict__ d, double* __restrict__ u,
+             const double* __restrict__ v, double* __restrict__ q, double* __restrict__ r, int64_t n,
+             const FcgState* __restrict__ st, double* __restrict__ partials) {
+    const double c = st->c, a = st->a;
+    double rr = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double dn = dsub(w[i], dmul(c, d[i]));
+        const double qn = dsub(v[i], dmul(c, q[i]));
+        d[i] = dn;
+        q[i] = qn;
+        u[i] = dadd(u[i], dmul(a, dn));
+        const double rn = dsub(r[i], dmul(a, qn));
+        r[i] = rn;
+        rr = dadd(rr, dmul(rn, rn));
+    }
+    for (int o = 16; o; o >>= 1) rr = dadd(rr, __shfl_down_sync(0xffffffffu, rr, o));
+    __shared__ double red[kRedThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = rr;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int k = 0; k < kRedThreads / 32; ++k) acc = dadd(acc, red[k]);
+        partials[blockIdx.x] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    k_norm_partials(const double* __restrict__ r, int64_t n, double* __restrict__ partials) {
+    double rr = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        rr = dadd(rr, dmul(r[i], r[i]));
+    for (int o = 16; o; o >>= 1) rr = dadd(rr, __shfl_down_sync(0xffffffffu, rr, o));
+    __shared__ double red[kRedThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = rr;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int k = 0; k < kRedThreads / 32; ++k) acc = dadd(acc, red[k]);
+        partials[blockIdx.x] = acc;
+    }
+}
+
+// Fixed-order reduction of G partial K-tuples into out[K] (one block).
+__global__ void __launch_bounds__(kRedThreads)
+    k_reduce(const double* __restrict__ partials, int G, int K, double* __restrict__ out) {
+    __shared__ double red[kRedThreads];
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int g = threadIdx.x; g < G; g += kRedThreads) s = dadd(s, partials[g * K + k]);
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] = dadd(red[threadIdx.x], red[threadIdx.x + w]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[k] = red[0];
+        __syncthreads();
+    }
+}
+
+// Cross-rank sums in rank order (runtime.cpp:388-396), then the FCG scalar
+// recurrences (Alg. 1 lines 4-5, 14; breakdown check SPEC.md:478).
+__global__ void k_fcg_scalars(const double* __restrict__ g, int p, FcgState* __restrict__ st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double al = 0.0, be = 0.0, ga = 0.0;
+    for (int r = 0; r < p; ++r) {
+        al = dadd(al, g[3 * r + 0]);
+        be = dadd(be, g[3 * r + 1]);
+        ga = dadd(ga, g[3 * r + 2]);
+    }
+    st->alpha = al;
+    st->beta = be;
+    st->gamma = ga;
+    double rho_new, c;
+    if (st->it == 0) {
+        rho_new = be;  // rho_0 = w_0^T v_0
+        c = 0.0;       // d_0 = w_0, q_0 = v_0 (d, q start at zero)
+    } else {
+        rho_new = dsub(be, ddiv(dmul(ga, ga), st->rho));
+        c = ddiv(ga, st->rho);
+    }
+    if (rho_new == 0.0 || !isfinite(rho_new)) st->status = 1;
+    st->c = c;
+    st->a = ddiv(al, rho_new);
+    st->rho = rho_new;
+}
+
+__global__ void k_norm_final(const double* __restrict__ g, int p, FcgState* __restrict__ st, int init) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double rr = 0.0;
+    for (int r = 0; r < p; ++r) rr = dadd(rr, g[r]);
+    st->rr = rr;
+    if (init) {
+        st->rr0 = rr;
+        st->it = 0;
+        st->status = 0;
+        st->rho = 0.0;
+    } else {
+        st->it += 1;
+    }
+}
+
+int red_grid(int64_t n) {
+    const int64_t want = (n + kRedThreads - 1) / kRedThreads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
+}
+
+}  // namespace
+
+Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
+    PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
+}
+
+Solver::~Solver() {
+    cudaSetDevice(rt.device());
+    cudaStreamSynchronize(s_);
+    destroy_graph();
+    for (auto& v : tev_)
+        for (auto& pr : v) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (h_state_) cudaFreeHost(h_state_);
+}
+
+void Solver::destroy_graph() {
+    if (graph_) cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+}
+
+void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t>&& col, DBuf<double>&& val,
+                   int64_t nnz, const double* d_w0, const SetupConfig& cfg) {
+    destroy_graph();
+    ready = false;
+    setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
+    ensure_vectors();
+    ready = true;
+}
+
+void Solver::ensure_vectors() {
+    Level& L0 = *h.levels[0];
+    n_ = L0.A.n;
+    next_ = L0.A.n + L0.A.halo.n_halo;
+    u_.alloc(static_cast<size_t>(next_), s_);
+    r_.alloc(static_cast<size_t>(n_), s_);
+    w_.alloc(static_cast<size_t>(next_), s_);
+    v_.alloc(static_cast<size_t>(n_), s_);
+    d_.alloc(static_cast<size_t>(n_), s_);
+    q_.alloc(static_cast<size_t>(n_), s_);
+    max_blocks_ = kSmCount * 8;
+    partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
+    local_.alloc(8, s_);
+    gathered_.alloc(static_cast<size_t>(4 * rt.nranks()), s_);
+    state_.alloc(1, s_);
+    u_.zero(s_);
+    w_.zero(s_);
+}
+
+void Solver::ensure_events(int kc, int idx) {
+    while (static_cast<int>(tev_[kc].size()) <= idx) {
+        cudaEvent_t a, b;
+        PB_CUDA(cudaEventCreate(&a));
+        PB_CUDA(cudaEventCreate(&b));
+        tev_[kc].push_back({a, b});
+    }
+}
+
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st;
+    PB_CUDA(cudaStreamIsCapturing(s, &st));
+    return st == cudaStreamCaptureStatusActive;
+}
+
+void Solver::begin_time(int kc) {
+    if (!timing || kc < 0) return;
+    const int idx = tcount_[kc];
+    ensure_events(kc, idx);
+    topen_[kc] = idx;
+    if (capturing(s_))
+        PB_CUDA(cudaEventRecordWithFlags(tev_[kc][idx].first, s_, cudaEventRecordExternal));
+    else
+        PB_CUDA(cudaEventRecord(tev_[kc][idx].first, s_));
+}
+
+void Solver::end_time(int kc) {
+    if (!timing || kc < 0) return;
+    const int idx = topen_[kc];
+    if (capturing(s_))
+        PB_CUDA(cudaEventRecordWithFlags(tev_[kc][idx].second, s_, cudaEventRecordExternal));
+    else
+        PB_CUDA(cudaEventRecord(tev_[kc][idx].second, s_));
+    tcount_[kc] = idx + 1;
+}
+
+void Solver::collect_times() {
+    if (!timing) return;
+    for (int kc = 0; kc < 4; ++kc)
+        for (int i = 0; i < tcount_[kc]; ++i) {
+            float ms = 0.f;
+            PB_CUDA(cudaEventElapsedTime(&ms, tev_[kc][i].first, tev_[kc][i].second));
+            ktime[kc].ms += ms;
+            ktime[kc].launches += 1;
+        }
+}
+
+void Solver::apply(int k, int op, const double* x, double* y, const double* r, const double* d, double omega,
+                   int kc) {
+    Level& L = *h.levels[k];
+    begin_time(kc);
+    if (L.A.halo.has_traffic()) {
+        PB_CUDA(cudaEventRecord(ev_fork_, s_));
+        PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
+        halo_exchange(rt, L.A.halo, x, const_cast<double*>(x) + L.A.n, rt.comm_stream());
+        PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
+        launches_ += L.A.halo.send_off.back() ? 1 : 0;
+    }
+    if (L.A.halo.n_halo > 0) {
+        sell_apply(L.sell_int, op, x, y, r, d, omega, s_);
+        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        sell_apply(L.sell_bnd, op, x, y, r, d, omega, s_);
+        launches_ += 2;
+    } else {
+        if (L.A.halo.has_traffic()) PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        sell_apply(L.sell_all, op, x, y, r, d, omega, s_);
+        launches_ += 1;
+    }
+    end_time(kc);
+}
+
+void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
+                    bool l0) {
+    Level& L = *h.levels[k];
+    const int64_t n = L.A.n;
+    if (nu == 0) {
+        if (zero_start && n) PB_CUDA(cudaMemsetAsync(xc, 0, 8 * n, s_));
+        return;
+    }
+    int sweep = 0;
+    if (zero_start) {
+        begin_time(l0 ? 0 : -1);
+        if (n) k_zero_start<<<blocks_for(n, 256), 256, 0, s_>>>(rhs, L.l1.get(), xc, n, omega);
+        PB_CHECK_LAUNCH();
+        end_time(l0 ? 0 : -1);
+        launches_ += 1;
+        ++sweep;
+    }
+    for (; sweep < nu; ++sweep) {
+        apply(k, kJacobi, xc, xo, rhs, L.l1.get(), omega, l0 ? 0 : -1);
+        std::swap(xc, xo);
+    }
+}
+
+void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc) {
+    Level& L = *h.levels[k];
+    double* xc = L.x.get();
+    double* xo = L.xt.get();
+    const bool l0 = k == 0;
+    if (k == h.nl() - 1) {
+        smooth(k, true, cc.coarsest_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+        out = xc;
+        return;
+    }
+    smooth(k, true, cc.pre_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+    apply(k, kResid, xc, L.res.get(), rhs, nullptr, 0.0, l0 ? 1 : -1);
+    Level& C = *h.levels[k + 1];
+    if (C.A.n) k_restrict<<<blocks_for(C.A.n, 256), 256, 0, s_>>>(C.rrp.get(), C.rcol.get(), C.rval.get(),
+                                                                    L.res.get(), C.rhs.get(), C.A.n);
+    PB_CHECK_LAUNCH();
+    launches_ += 1;
+    double* e = nullptr;
+    vcycle_enqueue(k + 1, C.rhs.get(), e, cc);
+    if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(C.pcol.get(), C.pval.get(), e, xc, L.A.n);
+    PB_CHECK_LAUNCH();
+    launches_ += 1;
+    smooth(k, false, cc.post_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+    out = xc;
+}
+
+void Solver::reduce_dots_enqueue() {
+    const int p = rt.nranks();
+    // partial count G is encoded by the producer; it is fixed for the level
+    Level& L0 = *h.levels[0];
+    const int G = L0.A.halo.has_traffic() ? red_grid(n_) : sell_dots_grid(L0.sell_all);
+    k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), G, 3, local_.get());
+    PB_CHECK_LAUNCH();
+    const double* g = local_.get();
+    if (p > 1) {
+        rt.allgather_f64(local_.get(), gathered_.get(), 3, s_);
+        g = gathered_.get();
+    }
+    k_fcg_scalars<<<1, 32, 0, s_>>>(g, p, state_.get());
+    PB_CHECK_LAUNCH();
+    launches_ += 2;
+}
+
+void Solver::reduce_norm_enqueue(bool init) {
+    const int p = rt.nranks();
+    k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), red_grid(n_), 1, local_.get() + 3);
+    PB_CHECK_LAUNCH();
+    const double* g = local_.get() + 3;
+    if (p > 1) {
+        rt.allgather_f64(local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
+        g = gathered_.get() + 3 * p;
+    }
+    k_norm_final<<<1, 32, 0, s_>>>(g, p, state_.get(), init ? 1 : 0);
+    PB_CHECK_LAUNCH();
+    launches_ += 2;
+}
+
+void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
+    Level& L0 = *h.levels[0];
+    double* w = nullptr;
+    if (precflag) {
+        vcycle_enqueue(0, r_.get(), w, cc);
+    } else {
+        if (n_) PB_CUDA(cudaMemcpyAsync(w_.get(), r_.get(), 8 * n_, cudaMemcpyDeviceToDevice, s_));
+        w = w_.get();
+    }
+    w_out_ = w;
+    // v = A w and the dot triple (Alg. 1 lines 10-13)
+    if (!L0.A.halo.has_traffic()) {
+        begin_time(2);
+        sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
+        end_time(2);
+        launches_ += 1;
+    } else {
+        apply(0, kSpmv, w, v_.get(), nullptr, nullptr, 0.0, 2);
+        k_dots3<<<red_grid(n_), kRedThreads, 0, s_>>>(w, v_.get(), r_.get(), q_.get(), n_, partials_.get());
+        PB_CHECK_LAUNCH();
+        launches_ += 1;
+    }
+    reduce_dots_enqueue();
+    begin_time(3);
+    k_update<<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(), n_,
+                                                    state_.get(), partials_.get());
+    PB_CHECK_LAUNCH();
+    end_time(3);
+    launches_ += 1;
+    reduce_norm_enqueue(false);
+}
+
+void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double rtol, int max_iters,
+                   bool precflag, pairamg_solve_stats* st) {
+    if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "solve: setup not run");
+    if (rtol <= 0.0 || max_iters < 1) fail(PAIRAMG_INVALID_ARGUMENT, "solve: need rtol > 0 and max_iters >= 1");
+    if (cc.pre_sweeps < 0 || cc.post_sweeps < 0 || cc.coarsest_sweeps < 0)
+        fail(PAIRAMG_INVALID_ARGUMENT, "cycle config: sweep counts must be >= 0");
+    Level& L0 = *h.levels[0];
+    for (auto& kt : ktime) kt = KernelClassTiming{};
+    const double nnz0 = static_cast<double>(L0.A.nnz), n0 = static_cast<double>(n_);
+    ktime[0].bytes_per_launch = 12.0 * nnz0 + 36.0 * n0;  // Jacobi sweep
+    ktime[1].bytes_per_launch = 12.0 * nnz0 + 28.0 * n0;  // residual
+    ktime[2].bytes_per_launch = 12.0 * nnz0 + 36.0 * n0;  // SpMV + dot triple (reads r, q)
+    ktime[3].bytes_per_launch = 80.0 * n0;                // 6 vectors read, 4 written
+
+    cudaEvent_t e0, e1;
+    PB_CUDA(cudaEventCreate(&e0));
+    PB_CUDA(cudaEventCreate(&e1));
+    PB_CUDA(cudaEventRecord(e0, s_));
+    launches_ = 0;
+    // u0, d = q = 0, r0 = b - A u0, |r0|^2
+    if (n_) {
+        PB_CUDA(cudaMemcpyAsync(u_.get(), d_u, 8 * n_, cudaMemcpyDeviceToDevice, s_));
+        PB_CUDA(cudaMemsetAsync(d_.get(), 0, 8 * n_, s_));
+        PB_CUDA(cudaMemsetAsync(q_.get(), 0, 8 * n_, s_));
+    }
+    const bool timing_save = timing;
+    timing = false;
+    apply(0, kResid, u_.get(), r_.get(), d_b, nullptr, 0.0, -1);
+    k_norm_partials<<<red_grid(n_), kRedThreads, 0, s_>>>(r_.get(), n_, partials_.get());
+    PB_CHECK_LAUNCH();
+    launches_ += 1;
+    reduce_norm_enqueue(true);
+    timing = timing_save;
+    PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
+    PB_CUDA(cudaStreamSynchronize(s_));
+    const double rr0 = h_state_->rr0;
+    const double rnorm0 = std::sqrt(rr0);
+    int it = 0;
+    double rel = 1.0;
+    std::vector<double> hist{1.0};
+    if (rnorm0 != 0.0) {
+        // (re)capture the iteration graph
+        if (!graph_ || graph_cc_.pre_sweeps != cc.pre_sweeps || graph_cc_.post_sweeps != cc.post_sweeps ||
+            graph_cc_.coarsest_sweeps != cc.coarsest_sweeps || graph_cc_.relax_weight != cc.relax_weight ||
+            graph_prec_ != precflag || graph_timing_ != timing) {
+            destroy_graph();
+            tcount_.fill(0);
+            cudaGraph_t g;
+            const int64_t l0 = launches_;
+            PB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+            iteration_enqueue(cc, precflag);
+            PB_CUDA(cudaStreamEndCapture(s_, &g));
+            per_iter_launches_ = launches_ - l0;
+            launches_ = l0;
+            PB_CUDA(cudaGraphInstantiate(&graph_, g, 0));
+            PB_CUDA(cudaGraphDestroy(g));
+            graph_cc_ = cc;
+            graph_prec_ = precflag;
+            graph_timing_ = timing;
+        }
+        while (true) {
+            PB_CUDA(cudaGraphLaunch(graph_, s_));
+            launches_ += per_iter_launches_;
+            PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
+            PB_CUDA(cudaStreamSynchronize(s_));
+            collect_times();
+            if (h_state_->status)
+                fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(h_state_->it));
+            it = h_state_->it;
+            rel = std::sqrt(h_state_->rr) / rnorm0;
+            hist.push_back(rel);
+            if (rel < rtol || it >= max_iters) break;
+        }
+    }
+    if (n_) PB_CUDA(cudaMemcpyAsync(d_u, u_.get(), 8 * n_, cudaMemcpyDeviceToDevice, s_));
+    PB_CUDA(cudaEventRecord(e1, s_));
+    PB_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    last_launches = launches_;
+    if (st) {
+        st->iterations = it;
+        st->converged = rel < rtol ? 1 : 0;
+        st->final_relres = rel;
+        st->rnorm0 = rnorm0;
+        st->t_solve_s = ms * 1e-3;
+        if (st->history)
+            for (int i = 0; i < st->history_cap && i < static_cast<int>(hist.size()); ++i) st->history[i] = hist[i];
+    }
+}
+
+void Solver::vcycle(const double* d_r, double* d_x, const CycleConfig& cc) {
+    if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "vcycle: setup not run");
+    if (n_) PB_CUDA(cudaMemcpyAsync(r_.get(), d_r, 8 * n_, cudaMemcpyDeviceToDevice, s_));
+    double* out = nullptr;
+    const bool t = timing;
+    timing = false;
+    vcycle_enqueue(0, r_.get(), out, cc);
+    timing = t;
+    if (n_) PB_CUDA(cudaMemcpyAsync(d_x, out, 8 * n_, cudaMemcpyDeviceToDevice, s_));
+    PB_CUDA(cudaStreamSynchronize(s_));
+}
+
+void Solver::spmv(int level, const double* d_x, double* d_y) {
+    if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "spmv: setup not run");
+    if (level < 0 || level >= h.nl()) fail(PAIRAMG_INVALID_ARGUMENT, "spmv: level out of range");
+    Level& L = *h.levels[level];
+    if (L.A.n) PB_CUDA(cudaMemcpyAsync(L.xt.get(), d_x, 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
+    const bool t = timing;
+    timing = false;
+    apply(level, kSpmv, L.xt.get(), L.res.get(), nullptr, nullptr, 0.0, -1);
+    timing = t;
+    if (L.A.n) PB_CUDA(cudaMemcpyAsync(d_y, L.res.get(), 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
+    PB_CUDA(cudaStreamSynchronize(s_));
+}
+
+}  // namespace pb

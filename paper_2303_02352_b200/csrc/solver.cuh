@@ -1,0 +1,87 @@
+// solver.cuh -- per-rank solver object behind the C ABI: the device
+// hierarchy, the flexible-CG state and the captured iteration graph.
+#pragma once
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "amg.cuh"
+
+namespace pb {
+
+// Device-resident FCG scalars (Alg. 1 lines 11-15), read once per iteration.
+struct FcgState {
+    double alpha, beta, gamma, rho;  // current dots / rho_i
+    double c, a;                     // gamma_i/rho_{i-1}, alpha_i/rho_i
+    double rr, rr0;                  // |r_{i+1}|^2, |r_0|^2
+    int it;                          // iterations completed
+    int status;                      // 0 ok, 1 breakdown
+};
+
+struct KernelClassTiming {
+    int64_t launches = 0;
+    double ms = 0.0;
+    double bytes_per_launch = 0.0;
+};
+
+class Solver {
+public:
+    explicit Solver(Runtime& rt);
+    ~Solver();
+
+    void setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t>&& col, DBuf<double>&& val,
+               int64_t nnz, const double* d_w0, const SetupConfig& cfg);
+    // Flexible PCG on device vectors (owned block).  Returns iterations.
+    void solve(const double* d_b, double* d_u, const CycleConfig& cc, double rtol, int max_iters,
+               bool precflag, pairamg_solve_stats* st);
+    void vcycle(const double* d_r, double* d_x, const CycleConfig& cc);
+    void spmv(int level, const double* d_x, double* d_y);
+
+    Runtime& rt;
+    Hierarchy h;
+    bool ready = false;
+    bool timing = false;
+    std::array<KernelClassTiming, 4> ktime{};
+    int64_t last_launches = 0;
+
+private:
+    // enqueue helpers (host-side pointer bookkeeping; graph-capturable)
+    void smooth(int k, bool zero_start, int nu, const double* rhs, double*& xcur, double*& xoth, double omega,
+                bool time_l0);
+    void apply(int k, int op, const double* x, double* y, const double* r, const double* d, double omega,
+               int kclass);
+    void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
+    void iteration_enqueue(const CycleConfig& cc, bool precflag);
+    void reduce_dots_enqueue();
+    void reduce_norm_enqueue(bool init_rr0);
+    void ensure_vectors();
+    void ensure_events(int kclass, int idx);
+    void begin_time(int kclass);
+    void end_time(int kclass);
+    void collect_times();
+    void destroy_graph();
+
+    cudaStream_t s_;
+    int64_t n_ = 0, next_ = 0;
+    DBuf<double> u_, r_, w_, v_, d_, q_;
+    DBuf<double> partials_, local_, gathered_;
+    DBuf<FcgState> state_;
+    FcgState* h_state_ = nullptr;  // pinned
+    int max_blocks_ = 0;
+    double* w_out_ = nullptr;      // buffer holding w_i after the captured V-cycle
+    cudaGraphExec_t graph_ = nullptr;
+    CycleConfig graph_cc_{};
+    bool graph_prec_ = true;
+    bool graph_timing_ = false;
+    int64_t per_iter_launches_ = 0;
+    std::vector<cudaEvent_t> ev_pool_;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    // per-class event pairs recorded in the captured iteration
+    std::array<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>, 4> tev_{};
+    std::array<int, 4> tcount_{};
+    std::array<int, 4> topen_{};
+    int64_t launches_ = 0;
+};
+
+}  // namespace pb

@@ -1,0 +1,523 @@
+// sparse.cu -- distributed sparse primitives on one rank's device data:
+// localization + halo plans (dist.cpp:158-233), halo exchange (the sends /
+// receives of spmv_dist, dist.cpp:255-275), SELL-32 construction, the
+// SELL apply kernels (spmv_dist row loop dist.cpp:277-300, the l1-Jacobi
+// update cycle.cpp:96-100, the V-cycle residual cycle.cpp:141-143) and the
+// l1 diagonal (cycle.cpp:55-75).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+
+#include "matrix.cuh"
+
+namespace pb {
+
+namespace {
+
+struct OffRange {
+    int64_t b, e;
+    __host__ __device__ bool operator()(int64_t g) const { return g < b || g >= e; }
+};
+
+__global__ void k_map_cols(const int64_t* __restrict__ gcol, int32_t* __restrict__ lcol, int64_t nnz,
+                           int64_t b, int64_t e, const int64_t* __restrict__ recv, int64_t nrecv,
+                           int64_t n, int* __restrict__ bad) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nnz) return;
+    const int64_t g = gcol[t];
+    if (g >= b && g < e) {
+        lcol[t] = static_cast<int32_t>(g - b);
+        return;
+    }
+    int64_t lo = 0, hi = nrecv;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (recv[mid] < g)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    if (lo >= nrecv || recv[lo] != g) {
+        atomicExch(bad, 1);
+        lcol[t] = 0;
+        return;
+    }
+    lcol[t] = static_cast<int32_t>(n + lo);
+}
+
+__global__ void k_boundary_flags(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 int64_t n, uint8_t* __restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t f = 0;
+    for (int64_t t = rp[i]; t < rp[i + 1]; ++t)
+        if (col[t] >= n) {
+            f = 1;
+            break;
+        }
+    flag[i] = f;
+}
+
+__global__ void k_invert(const uint8_t* __restrict__ a, uint8_t* __restrict__ b, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i] ? 0 : 1;
+}
+
+__global__ void k_global_cols(const int32_t* __restrict__ col, int64_t nnz, int64_t n, int64_t b,
+                              const int64_t* __restrict__ recv, int64_t* __restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nnz) return;
+    const int32_t c = col[t];
+    out[t] = c < n ? b + c : recv[c - n];
+}
+
+__global__ void k_pack(const int32_t* __restrict__ idx, int64_t m, const double* __restrict__ x,
+                       double* __restrict__ buf) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < m) buf[t] = x[idx[t]];
+}
+
+__global__ void k_pack_pair(const int32_t* __restrict__ idx, int64_t m, const int64_t* __restrict__ a,
+                            const double* __restrict__ b, int64_t* __restrict__ abuf,
+                            double* __restrict__ bbuf) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < m) {
+        abuf[t] = a[idx[t]];
+        bbuf[t] = b[idx[t]];
+    }
+}
+
+// l1_diagonal_dist (cycle.cpp:55-75): d_i = a_ii + sum_{j != i} |a_ij| in CSR order.
+__global__ void k_l1(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                     const double* __restrict__ val, int64_t n, double* __restrict__ d,
+                     unsigned long long* __restrict__ zero_row) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+        const double a = val[t];
+        acc = dadd(acc, col[t] == i ? a : fabs(a));
+    }
+    if (acc == 0.0) atomicMin(zero_row, static_cast<unsigned long long>(i));
+    d[i] = acc;
+}
+
+// SELL widths: one warp per slice, width = longest row of the slice.
+__global__ void k_sell_width(const int64_t* __restrict__ rp, const int32_t* __restrict__ rows,
+                             int64_t nrows, int64_t nslices, int64_t* __restrict__ w32) {
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= nslices) return;
+    const int64_t sr = s * 32 + lane;
+    int len = 0;
+    if (sr < nrows) {
+        const int64_t row = rows ? rows[sr] : sr;
+        len = static_cast<int>(rp[row + 1] - rp[row]);
+    }
+    for (int o = 16; o; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+    if (lane == 0) w32[s] = 32LL * len;
+}
+
+__global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, const int32_t* __restrict__ rows,
+                            int64_t nrows, const int64_t* __restrict__ soff, int32_t* __restrict__ scol,
+                            double* __restrict__ sval) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : sr;
+    const int64_t s = sr >> 5;
+    const int lane = static_cast<int>(sr & 31);
+    const int64_t base = soff[s] + lane;
+    const int64_t b = rp[row], e = rp[row + 1];
+    for (int64_t t = b; t < e; ++t) {
+        scol[base + (t - b) * 32] = col[t];
+        sval[base + (t - b) * 32] = val[t];
+    }
+}
+
+constexpr int kSellThreads = 256;
+constexpr int kSellWarps = kSellThreads / 32;
+constexpr int kChunk = 8;
+
+// Row sum of one SELL lane in CSR order: sum = 0.0; sum += a*x (exact).
+__device__ __forceinline__ double sell_row_sum(const int32_t* __restrict__ cp,
+                                               const double* __restrict__ vp, int width,
+                                               const double* __restrict__ x) {
+    double sum = 0.0;
+    for (int k = 0; k < width; k += kChunk) {
+        int c[kChunk];
+        double a[kChunk], xv[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+            const bool in = k + j < width;
+            c[j] = in ? __ldg(cp + (k + j) * 32) : -1;
+            a[j] = in ? __ldg(vp + (k + j) * 32) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j)
+            if (c[j] >= 0) sum = dadd(sum, dmul(a[j], xv[j]));
+    }
+    return sum;
+}
+
+template <int OP, bool ROWS>
+__global__ void __launch_bounds__(kSellThreads)
+    k_sell(const int64_t* __restrict__ soff, const int32_t* __restrict__ col,
+           const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nslices,
+           int64_t nrows, const double* __restrict__ x, double* __restrict__ y,
+           const double* __restrict__ r, const double* __restrict__ d, double omega) {
+    const int lane = threadIdx.x & 31;
+    const int64_t slice = static_cast<int64_t>(blockIdx.x) * kSellWarps + (threadIdx.x >> 5);
+    if (slice >= nslices) return;
+    const int64_t beg = soff[slice];
+    const int width = static_cast<int>((soff[slice + 1] - beg) >> 5);
+    const double sum = sell_row_sum(col + beg + lane, val + beg + lane, width, x);
+    const int64_t sr = slice * 32 + lane;
+    if (sr >= nrows) return;
+    const int64_t row = ROWS ? rows[sr] : sr;
+    if (OP == kSpmv) {
+        y[row] = sum;
+    } else if (OP == kJacobi) {
+        y[row] = dadd(x[row], ddiv(dmul(omega, dsub(r[row], sum)), d[row]));
+    } else {
+        y[row] = dsub(r[row], sum);
+    }
+}
+
+// v = A w and block partials of (w.r, w.v, w.q): grid-stride over slices so
+// the number of partials is bounded by the grid (deterministic fixed order).
+__global__ void __launch_bounds__(kSellThreads)
+    k_sell_spmv_dots(const int64_t* __restrict__ soff, const int32_t* __restrict__ col,
+                     const double* __restrict__ val, int64_t nslices, int64_t nrows,
+                     const double* __restrict__ w, double* __restrict__ v,
+                     const double* __restrict__ r, const double* __restrict__ q,
+                     double* __restrict__ partials) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    for (int64_t slice = static_cast<int64_t>(blockIdx.x) * kSellWarps + warp; slice < nslices;
+         slice += static_cast<int64_t>(gridDim.x) * kSellWarps) {
+        const int64_t beg = soff[slice];
+        const int width = static_cast<int>((soff[slice + 1] - beg) >> 5);
+        const double sum = sell_row_sum(col + beg + lane, val + beg + lane, width, w);
+        const int64_t row = slice * 32 + lane;
+        if (row < nrows) {
+            v[row] = sum;
+            const double wi = w[row];
+            sa = dadd(sa, dmul(wi, r[row]));
+            sb = dadd(sb, dmul(wi, sum));
+            sg = dadd(sg, dmul(wi, q[row]));
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    __shared__ double red[3][kSellWarps];
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int i = 0; i < kSellWarps; ++i) acc = dadd(acc, red[threadIdx.x][i]);
+        partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}
+
+template <typename F>
+void cub_call(F&& f, cudaStream_t s) {
+    size_t bytes = 0;
+    PB_CUDA(f(nullptr, bytes));
+    DBuf<uint8_t> tmp(bytes ? bytes : 1, s);
+    PB_CUDA(f(tmp.get(), bytes));
+}
+
+int64_t read_i64(const int64_t* d, cudaStream_t s) {
+    int64_t h = 0;
+    PB_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+// Row ids where flag[i] != 0, ascending.
+int64_t select_rows(const uint8_t* flag, int64_t n, DBuf<int32_t>& out, cudaStream_t s) {
+    DBuf<int32_t> tmp(static_cast<size_t>(n), s);
+    DBuf<int64_t> cnt(1, s);
+    thrust::counting_iterator<int32_t> it(0);
+    cub_call([&](void* t, size_t& b) {
+        return cub::DeviceSelect::Flagged(t, b, it, flag, tmp.get(), cnt.get(), n, s);
+    }, s);
+    const int64_t m = read_i64(cnt.get(), s);
+    out.alloc(static_cast<size_t>(m), s);
+    if (m) PB_CUDA(cudaMemcpyAsync(out.get(), tmp.get(), 4 * m, cudaMemcpyDeviceToDevice, s));
+    return m;
+}
+
+}  // namespace
+
+void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gcol,
+              DBuf<double>&& val, int64_t nnz) {
+    cudaStream_t s = rt.stream();
+    const int p = rt.nranks();
+    const int r = rt.rank();
+    M.row_begin = M.starts[r];
+    M.n = M.starts[r + 1] - M.starts[r];
+    M.n_global = M.starts[p];
+    M.nnz = nnz;
+    if (nnz >= (int64_t(1) << 31) - 1)
+        fail(PAIRAMG_INVALID_ARGUMENT, "local nnz exceeds int32 column-slot range; use more ranks");
+    const int64_t b = M.row_begin, e = M.starts[r + 1];
+
+    // build_rows_to_receive (dist.cpp:158-168): sorted unique off-range ids.
+    HaloPlan& H = M.halo;
+    {
+        DBuf<int64_t> off(static_cast<size_t>(std::max<int64_t>(nnz, 1)), s);
+        DBuf<int64_t> cnt(1, s);
+        OffRange pred{b, e};
+        cub_call([&](void* t, size_t& bytes) {
+            return cub::DeviceSelect::If(t, bytes, gcol.get(), off.get(), cnt.get(), nnz, pred, s);
+        }, s);
+        const int64_t m = read_i64(cnt.get(), s);
+        if (m > 0) {
+            DBuf<int64_t> sorted(static_cast<size_t>(m), s);
+            cub_call([&](void* t, size_t& bytes) {
+                return cub::DeviceRadixSort::SortKeys(t, bytes, off.get(), sorted.get(), m, 0, 64, s);
+            }, s);
+            cub_call([&](void* t, size_t& bytes) {
+                return cub::DeviceSelect::Unique(t, bytes, sorted.get(), off.get(), cnt.get(), m, s);
+            }, s);
+            H.n_halo = read_i64(cnt.get(), s);
+            H.recv_gid.alloc(static_cast<size_t>(H.n_halo), s);
+            PB_CUDA(cudaMemcpyAsync(H.recv_gid.get(), off.get(), 8 * H.n_halo, cudaMemcpyDeviceToDevice, s));
+        } else {
+            H.n_halo = 0;
+        }
+    }
+    if (H.n_halo > 0 && p == 1)
+        fail(PAIRAMG_CONTRACT_VIOLATION, "localize: column index outside [0, n) on a single rank");
+    if (M.n + H.n_halo >= (int64_t(1) << 31) - 1)
+        fail(PAIRAMG_INVALID_ARGUMENT, "local rows + halo exceed int32 range");
+
+    // local column ids
+    M.col.alloc(static_cast<size_t>(nnz), s);
+    {
+        DBuf<int> bad(1, s);
+        bad.zero(s);
+        if (nnz)
+            k_map_cols<<<blocks_for(nnz, 256), 256, 0, s>>>(gcol.get(), M.col.get(), nnz, b, e,
+                                                            H.recv_gid.get(), H.n_halo, M.n, bad.get());
+        PB_CHECK_LAUNCH();
+        int hb = 0;
+        PB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaStreamSynchronize(s));
+        if (hb) fail(PAIRAMG_INTERNAL, "localize: halo id lookup failed");
+    }
+    M.rp = std::move(rp);
+    M.val = std::move(val);
+    gcol.reset();
+
+    // exchange_requests (dist.cpp:180-204): tell owners what we need.
+    H.recv_peers.clear();
+    H.recv_off.assign(1, 0);
+    H.send_peers.clear();
+    H.send_off.assign(1, 0);
+    if (p > 1) {
+        std::vector<int64_t> ids(static_cast<size_t>(H.n_halo));
+        if (H.n_halo)
+            PB_CUDA(cudaMemcpyAsync(ids.data(), H.recv_gid.get(), 8 * H.n_halo, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaStreamSynchronize(s));
+        std::vector<std::vector<int64_t>> req(static_cast<size_t>(p));
+        for (int64_t g : ids) {
+            const int owner = static_cast<int>(std::upper_bound(M.starts.begin(), M.starts.end(), g) -
+                                               M.starts.begin()) - 1;
+            if (owner == r || owner < 0 || owner >= p)
+                fail(PAIRAMG_INTERNAL, "halo plan: owned id in receive set");
+            req[owner].push_back(g);
+        }
+        for (int q = 0; q < p; ++q)
+            if (!req[q].empty()) {
+                H.recv_peers.push_back(q);
+                H.recv_off.push_back(H.recv_off.back() + static_cast<int64_t>(req[q].size()));
+            }
+        auto incoming = rt.alltoallv_i64(req);
+        std::vector<int32_t> sidx;
+        for (int q = 0; q < p; ++q) {
+            if (q == r || incoming[q].empty()) continue;
+            for (int64_t g : incoming[q]) {
+                if (g < b || g >= e) fail(PAIRAMG_INTERNAL, "halo plan: asked for a row we do not own");
+                sidx.push_back(static_cast<int32_t>(g - b));
+            }
+            H.send_peers.push_back(q);
+            H.send_off.push_back(static_cast<int64_t>(sidx.size()));
+        }
+        H.send_idx.alloc(sidx.size(), s);
+        H.send_buf.alloc(sidx.size(), s);
+        if (!sidx.empty())
+            PB_CUDA(cudaMemcpyAsync(H.send_idx.get(), sidx.data(), 4 * sidx.size(), cudaMemcpyHostToDevice, s));
+    }
+
+    // boundary / interior rows (build_spmv_plan, dist.cpp:222-231)
+    M.n_boundary = 0;
+    M.boundary_rows.reset();
+    M.interior_rows.reset();
+    if (H.n_halo > 0) {
+        DBuf<uint8_t> flag(static_cast<size_t>(M.n), s), inv(static_cast<size_t>(M.n), s);
+        k_boundary_flags<<<blocks_for(M.n, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.n, flag.get());
+        PB_CHECK_LAUNCH();
+        k_invert<<<blocks_for(M.n, 256), 256, 0, s>>>(flag.get(), inv.get(), M.n);
+        PB_CHECK_LAUNCH();
+        M.n_boundary = select_rows(flag.get(), M.n, M.boundary_rows, s);
+        select_rows(inv.get(), M.n, M.interior_rows, s);
+    }
+    PB_CUDA(cudaStreamSynchronize(s));
+}
+
+void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s) {
+    if (!M.nnz) return;
+    k_global_cols<<<blocks_for(M.nnz, 256), 256, 0, s>>>(M.col.get(), M.nnz, M.n, M.row_begin,
+                                                        M.halo.recv_gid.get(), d_out);
+    PB_CHECK_LAUNCH();
+}
+
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s) {
+    S.nrows = nrows;
+    S.nslices = (nrows + 31) / 32;
+    S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
+    PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
+    if (S.nslices) {
+        k_sell_width<<<blocks_for(S.nslices * 32, 256), 256, 0, s>>>(M.rp.get(), rows, nrows, S.nslices,
+                                                                     S.slice_off.get());
+        PB_CHECK_LAUNCH();
+        cub_call([&](void* t, size_t& bytes) {
+            return cub::DeviceScan::ExclusiveSum(t, bytes, S.slice_off.get(), S.slice_off.get(),
+                                                 S.nslices + 1, s);
+        }, s);
+    }
+    S.padded_nnz = read_i64(S.slice_off.get() + S.nslices, s);
+    S.col.alloc(static_cast<size_t>(S.padded_nnz), s);
+    S.val.alloc(static_cast<size_t>(S.padded_nnz), s);
+    if (S.padded_nnz) {
+        PB_CUDA(cudaMemsetAsync(S.col.get(), 0xff, 4 * S.padded_nnz, s));
+        PB_CUDA(cudaMemsetAsync(S.val.get(), 0, 8 * S.padded_nnz, s));
+    }
+    if (rows) {
+        S.rows.alloc(static_cast<size_t>(nrows), s);
+        if (nrows) PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
+    } else {
+        S.rows.reset();
+    }
+    if (nrows) {
+        k_sell_fill<<<blocks_for(nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, nrows,
+                                                           S.slice_off.get(), S.col.get(), S.val.get());
+        PB_CHECK_LAUNCH();
+    }
+}
+
+void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s) {
+    if (!M.n) return;
+    DBuf<unsigned long long> zr(1, s);
+    PB_CUDA(cudaMemsetAsync(zr.get(), 0xff, 8, s));
+    k_l1<<<blocks_for(M.n, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), M.n, d_out, zr.get());
+    PB_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    PB_CUDA(cudaMemcpyAsync(&h, zr.get(), 8, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (h != ~0ULL)
+        fail(PAIRAMG_SINGULAR_SMOOTHER, "l1_diagonal_dist: zero diagonal weight at global row " +
+                                            std::to_string(M.row_begin + static_cast<int64_t>(h)));
+}
+
+void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_halo, cudaStream_t s) {
+    if (!H.has_traffic()) return;
+    const int64_t nsend = H.send_off.back();
+    if (nsend) {
+        k_pack<<<blocks_for(nsend, 256), 256, 0, s>>>(H.send_idx.get(), nsend, x_owned, H.send_buf.get());
+        PB_CHECK_LAUNCH();
+    }
+    PB_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < H.send_peers.size(); ++i) {
+        const int64_t c = H.send_off[i + 1] - H.send_off[i];
+        PB_NCCL(ncclSend(H.send_buf.get() + H.send_off[i], static_cast<size_t>(c), ncclDouble, H.send_peers[i],
+                         rt.nccl(), s));
+        rt.stats().p2p_messages += 1;
+        rt.stats().p2p_bytes += 8 * c;
+    }
+    for (size_t i = 0; i < H.recv_peers.size(); ++i)
+        PB_NCCL(ncclRecv(x_halo + H.recv_off[i], static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]),
+                         ncclDouble, H.recv_peers[i], rt.nccl(), s));
+    PB_NCCL(ncclGroupEnd());
+}
+
+void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_t* a_halo,
+                        const double* b_owned, double* b_halo, cudaStream_t s) {
+    if (!H.has_traffic()) return;
+    const int64_t nsend = H.send_off.back();
+    if (H.send_buf_i64.size() < static_cast<size_t>(nsend)) H.send_buf_i64.alloc(static_cast<size_t>(nsend), s);
+    if (nsend) {
+        k_pack_pair<<<blocks_for(nsend, 256), 256, 0, s>>>(H.send_idx.get(), nsend, a_owned, b_owned,
+                                                           H.send_buf_i64.get(), H.send_buf.get());
+        PB_CHECK_LAUNCH();
+    }
+    PB_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < H.send_peers.size(); ++i) {
+        const size_t c = static_cast<size_t>(H.send_off[i + 1] - H.send_off[i]);
+        PB_NCCL(ncclSend(H.send_buf_i64.get() + H.send_off[i], c, ncclInt64, H.send_peers[i], rt.nccl(), s));
+        PB_NCCL(ncclSend(H.send_buf.get() + H.send_off[i], c, ncclDouble, H.send_peers[i], rt.nccl(), s));
+        rt.stats().p2p_messages += 1;
+        rt.stats().p2p_bytes += 16 * static_cast<int64_t>(c);
+    }
+    for (size_t i = 0; i < H.recv_peers.size(); ++i) {
+        const size_t c = static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]);
+        PB_NCCL(ncclRecv(a_halo + H.recv_off[i], c, ncclInt64, H.recv_peers[i], rt.nccl(), s));
+        PB_NCCL(ncclRecv(b_halo + H.recv_off[i], c, ncclDouble, H.recv_peers[i], rt.nccl(), s));
+    }
+    PB_NCCL(ncclGroupEnd());
+}
+
+void sell_apply(const Sell& S, int op, const double* x, double* y, const double* r, const double* d,
+                double omega, cudaStream_t s) {
+    if (!S.nslices) return;
+    const int grid = blocks_for(S.nslices, kSellWarps);
+    const bool rows = !S.rows.empty();
+#define PB_SELL(OP)                                                                                  \
+    if (rows)                                                                                        \
+        k_sell<OP, true><<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), \
+                                                       S.rows.get(), S.nslices, S.nrows, x, y, r, d,  \
+                                                       omega);                                        \
+    else                                                                                             \
+        k_sell<OP, false><<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), \
+                                                        nullptr, S.nslices, S.nrows, x, y, r, d, omega);
+    switch (op) {
+        case kSpmv: PB_SELL(kSpmv) break;
+        case kJacobi: PB_SELL(kJacobi) break;
+        case kResid: PB_SELL(kResid) break;
+        default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
+    }
+#undef PB_SELL
+    PB_CHECK_LAUNCH();
+}
+
+int sell_dots_grid(const Sell& S) {
+    const int64_t want = (S.nslices + kSellWarps - 1) / kSellWarps;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
+}
+
+int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
+                   double* partials, int max_blocks, cudaStream_t s) {
+    if (!S.rows.empty()) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: row-list SELL not supported");
+    const int grid = sell_dots_grid(S);
+    if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
+    k_sell_spmv_dots<<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), S.nslices,
+                                                    S.nrows, w, v, r, q, partials);
+    PB_CHECK_LAUNCH();
+    return grid;
+}
+
+}  // namespace pb
