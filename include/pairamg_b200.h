@@ -183,6 +183,14 @@ pairamg_status pairamg_num_matchings(pairamg_solver* s, int* steps);
 pairamg_status pairamg_matching_export(pairamg_solver* s, int step, int64_t* n, int64_t* mate);
 pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* out);
 
+/* ---- matching KAT hook ---- */
+/* suitor_match (matching.cpp:62-100) under the total-order tie rule, run by
+ * the setup's parallel Suitor kernels on a caller graph: host CSR (n+1 row
+ * pointers, local column ids, symmetric, weights aligned with columns;
+ * self loops ignored).  mate (n) receives partners, -1 = unmatched. */
+pairamg_status pairamg_match_graph(pairamg_runtime* rt, int64_t n, const int64_t* row_ptr, const int64_t* col,
+                                   const double* weight, int64_t* mate);
+
 /* ---- measurement hooks ---- */
 /* Per-kernel-class device time accumulated over the last solve (CUDA events
  * around every launch of the class when timing was enabled):

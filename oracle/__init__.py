@@ -102,12 +102,42 @@ def _lib(kind: str) -> C.CDLL:
     L.orc_spmv.argtypes = [vp, C.c_int, vp, vp]
     L.orc_vcycle.argtypes = [vp, vp, vp]
     L.orc_solve.argtypes = [vp, vp, vp, vp, C.c_int, C.POINTER(C.c_int), dp, dp]
+    L.orc_set_solve.argtypes = [vp, C.c_double, C.c_int]
+    L.orc_build_weights.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp]
+    L.orc_build_weights.restype = i64
+    L.orc_match_graph.argtypes = [i64, vp, vp, vp, C.c_int, vp]
     _loaded[kind] = L
     return L
 
 
 def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def build_weights(kind, rp, col, val, w):
+    """build_weights (matching.cpp:28-60) of a square block -> (grp, gcol, gw)."""
+    L = _lib(kind)
+    rp, col = np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(col, np.int64)
+    val, w = np.ascontiguousarray(val, np.float64), np.ascontiguousarray(w, np.float64)
+    n = len(rp) - 1
+    grp = np.empty(n + 1, np.int64)
+    gcol = np.empty(max(len(col), 1), np.int64)
+    gw = np.empty(max(len(col), 1), np.float64)
+    m = L.orc_build_weights(n, _p(rp), _p(col), _p(val), _p(w), _p(grp), _p(gcol), _p(gw))
+    if m < 0:
+        raise OracleError(L.orc_last_status(), L.orc_last_error().decode())
+    return grp, gcol[:m], gw[:m]
+
+
+def match_graph(kind, rp, col, w, mode=0):
+    """suitor_match (matching.cpp:62-100) on a weighted graph CSR -> mate."""
+    L = _lib(kind)
+    rp, col = np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(col, np.int64)
+    w = np.ascontiguousarray(w, np.float64)
+    mate = np.empty(len(rp) - 1, np.int64)
+    if L.orc_match_graph(len(rp) - 1, _p(rp), _p(col), _p(w), mode, _p(mate)) != 0:
+        raise OracleError(L.orc_last_status(), L.orc_last_error().decode())
+    return mate
 
 
 class Oracle:
@@ -246,6 +276,12 @@ class Oracle:
         x = np.empty_like(r)
         self._check(self.L.orc_vcycle(self.h, _p(r), _p(x)))
         return x
+
+    def set_solve(self, rtol=None, max_iters=None):
+        rtol = self.cfg.rtol if rtol is None else rtol
+        max_iters = self.cfg.max_iters if max_iters is None else max_iters
+        self.cfg.rtol, self.cfg.max_iters = rtol, max_iters
+        self._check(self.L.orc_set_solve(self.h, rtol, max_iters))
 
     def solve(self, b=None, want_u=False, hist_cap=1024):
         if b is not None:

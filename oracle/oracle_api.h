@@ -91,6 +91,17 @@ int orc_num_matchings(void* h);
 int64_t orc_matching_size(void* h, int step);
 int orc_export_matching(void* h, int step, int64_t* mate);
 
+/* Matching kernels on a caller graph (KAT hooks):
+ * orc_build_weights: build_weights (matching.cpp:28-60) of a square block
+ *   with smooth vector w -> graph CSR (diagonal removed) in grp/gcol/gw
+ *   (capacity nnz), returns the edge count (or -1).
+ * orc_match_graph: suitor_match (matching.cpp:62-100) on a weighted graph CSR
+ *   (symmetric, no self loops); mode as orc_config.matching_mode. */
+int64_t orc_build_weights(int64_t n, const int64_t* rp, const int64_t* col, const double* val,
+                          const double* w, int64_t* grp, int64_t* gcol, double* gw);
+int orc_match_graph(int64_t n, const int64_t* rp, const int64_t* col, const double* w, int mode,
+                    int64_t* mate);
+
 /* y = A^k x (global vectors). */
 int orc_spmv(void* h, int level, const double* x, double* y);
 /* x = B r, one V-cycle from level 0 (global vectors). */
@@ -98,6 +109,8 @@ int orc_vcycle(void* h, const double* r, double* x);
 /* Flexible PCG on the input system, b = ones unless b != NULL.
  * u (global, may be NULL) receives the solution; hist (cap entries) the
  * relative residual history |r_k|/|r_0| for k = 0..iters. */
+/* Change the solve parameters of an existing session (SolveConfig). */
+int orc_set_solve(void* h, double rtol, int max_iters);
 int orc_solve(void* h, const double* b, double* u, double* hist, int hist_cap, int* iters,
               double* relres, double* t_solve);
 

@@ -234,52 +234,14 @@ static void hierarchy_free(session_t* s) {
 
 /* ---------------------------------------------------------- matching --- */
 
-/* Decoupled matching of one rank's diagonal block [b, e) of A (global rows):
- * extract_diagonal_block (matching.cpp:8-26), build_weights
- * (matching.cpp:28-60), suitor_match (matching.cpp:62-100).  mate is local
- * (0..e-b-1, -1 unmatched).  matching_mode 1 replaces only the acceptor test
- * of matching.cpp:82 by the total order key(e) = (w, -min, -max). */
-static void match_block(const csr_t* A, int64_t b, int64_t e, const double* w, int mode,
-                        int64_t* mate) {
-    const int64_t n = e - b;
-    /* block graph: local columns in [0, n), diagonal removed */
-    int64_t* grp = xmalloc(sizeof(int64_t) * (size_t)(n + 1));
-    int64_t m = 0;
-    double* diag = xmalloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-    for (int64_t i = 0; i < n; ++i) {
-        diag[i] = 0.0;
-        for (int64_t t = A->rp[b + i]; t < A->rp[b + i + 1]; ++t) {
-            const int64_t j = A->ci[t];
-            if (j >= b && j < e) {
-                if (j - b == i)
-                    diag[i] = A->va[t];
-                else
-                    ++m;
-            }
-        }
-    }
-    int64_t* gci = xmalloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
-    double* gw = xmalloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
-    int64_t pos = 0;
-    grp[0] = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        const double* wl = w + b;
-        for (int64_t t = A->rp[b + i]; t < A->rp[b + i + 1]; ++t) {
-            const int64_t jg = A->ci[t];
-            if (jg < b || jg >= e) continue;
-            const int64_t j = jg - b;
-            if (j == i) continue; /* no self-loops */
-            const double num = 2.0 * A->va[t] * wl[i] * wl[j];
-            const double den = diag[i] * wl[i] * wl[i] + diag[j] * wl[j] * wl[j];
-            double weight = 1.0 - num / den;
-            if (!isfinite(weight)) weight = -1e300; /* kClampedWeight, matching.hpp:29 */
-            gci[pos] = j;
-            gw[pos] = weight;
-            ++pos;
-        }
-        grp[i + 1] = pos;
-    }
-
+/* suitor_match (matching.cpp:62-100) on a graph CSR (local ids, no self
+ * loops).  Ascending proposers; each bids on its heaviest neighbour that
+ * would accept, smallest index on ties (strict '>' scan); the displaced
+ * suitor re-bids; mate = mutual suitors.  mode 0: the reference acceptor
+ * `wv > suitor_weight[v]` (matching.cpp:82); mode 1: the acceptor compares
+ * the total order key(e) = (w, -min(e), -max(e)) (SURVEY.md 7 hard part 1). */
+static void suitor_run(int64_t n, const int64_t* grp, const int64_t* gci, const double* gw, int mode,
+                       int64_t* mate) {
     int64_t* suitor = xmalloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
     double* sw = xmalloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     for (int64_t v = 0; v < n; ++v) {
@@ -326,12 +288,96 @@ static void match_block(const csr_t* A, int64_t b, int64_t e, const double* w, i
         const int64_t s = suitor[v];
         if (s != -1 && suitor[s] == v) mate[v] = s;
     }
+    free(suitor);
+    free(sw);
+}
+
+int orc_match_graph(int64_t n, const int64_t* rp, const int64_t* col, const double* w, int mode,
+                    int64_t* mate) {
+    suitor_run(n, rp, col, w, mode, mate);
+    return 0;
+}
+
+/* build_weights (matching.cpp:28-60) on a square block (local columns). */
+int64_t orc_build_weights(int64_t n, const int64_t* rp, const int64_t* col, const double* val,
+                          const double* w, int64_t* grp, int64_t* gcol, double* gw) {
+    double* diag = xmalloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        diag[i] = 0.0;
+        for (int64_t t = rp[i]; t < rp[i + 1]; ++t)
+            if (col[t] == i) diag[i] = val[t];
+    }
+    int64_t pos = 0;
+    grp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+            const int64_t j = col[t];
+            if (j == i) continue;
+            const double num = 2.0 * val[t] * w[i] * w[j];
+            const double den = diag[i] * w[i] * w[i] + diag[j] * w[j] * w[j];
+            double weight = 1.0 - num / den;
+            if (!isfinite(weight)) weight = -1e300;
+            gcol[pos] = j;
+            gw[pos] = weight;
+            ++pos;
+        }
+        grp[i + 1] = pos;
+    }
+    free(diag);
+    return pos;
+}
+
+/* Decoupled matching of one rank's diagonal block [b, e) of A (global rows):
+ * extract_diagonal_block (matching.cpp:8-26), build_weights
+ * (matching.cpp:28-60), suitor_match (matching.cpp:62-100).  mate is local
+ * (0..e-b-1, -1 unmatched).  matching_mode 1 replaces only the acceptor test
+ * of matching.cpp:82 by the total order key(e) = (w, -min, -max). */
+static void match_block(const csr_t* A, int64_t b, int64_t e, const double* w, int mode,
+                        int64_t* mate) {
+    const int64_t n = e - b;
+    /* block graph: local columns in [0, n), diagonal removed */
+    int64_t* grp = xmalloc(sizeof(int64_t) * (size_t)(n + 1));
+    int64_t m = 0;
+    double* diag = xmalloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        diag[i] = 0.0;
+        for (int64_t t = A->rp[b + i]; t < A->rp[b + i + 1]; ++t) {
+            const int64_t j = A->ci[t];
+            if (j >= b && j < e) {
+                if (j - b == i)
+                    diag[i] = A->va[t];
+                else
+                    ++m;
+            }
+        }
+    }
+    int64_t* gci = xmalloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+    double* gw = xmalloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+    int64_t pos = 0;
+    grp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double* wl = w + b;
+        for (int64_t t = A->rp[b + i]; t < A->rp[b + i + 1]; ++t) {
+            const int64_t jg = A->ci[t];
+            if (jg < b || jg >= e) continue;
+            const int64_t j = jg - b;
+            if (j == i) continue; /* no self-loops */
+            const double num = 2.0 * A->va[t] * wl[i] * wl[j];
+            const double den = diag[i] * wl[i] * wl[i] + diag[j] * wl[j] * wl[j];
+            double weight = 1.0 - num / den;
+            if (!isfinite(weight)) weight = -1e300; /* kClampedWeight, matching.hpp:29 */
+            gci[pos] = j;
+            gw[pos] = weight;
+            ++pos;
+        }
+        grp[i + 1] = pos;
+    }
+
+    suitor_run(n, grp, gci, gw, mode, mate);
     free(grp);
     free(diag);
     free(gci);
     free(gw);
-    free(suitor);
-    free(sw);
 }
 
 /* build_pairwise_prolongator (amg.cpp:38-77) for one rank block: aggregates
@@ -905,6 +951,13 @@ int orc_vcycle(void* h, const double* r, double* x) {
 
 /* Flexible PCG (Alg. 1), same iteration
  * convention and vector-update order as ref_driver.cpp's orc_solve. */
+int orc_set_solve(void* h, double rtol, int max_iters) {
+    session_t* s = h;
+    s->cfg.rtol = rtol;
+    s->cfg.max_iters = max_iters;
+    return 0;
+}
+
 int orc_solve(void* h, const double* b, double* u_out, double* hist, int hist_cap, int* iters,
               double* relres, double* t_solve) {
     session_t* s = h;

@@ -383,6 +383,47 @@ int orc_vcycle(void* h, const double* r, double* x) {
 // Vector-update operation order (also used by the CUDA path):
 //   d = w - (gamma/rho_prev) d;  q = v - (gamma/rho_prev) q;
 //   u = u + (alpha/rho) d;       r = r - (alpha/rho) q.
+int64_t orc_build_weights(int64_t n, const int64_t* rp, const int64_t* col, const double* val,
+                          const double* w, int64_t* grp, int64_t* gcol, double* gw) {
+    int64_t out = -1;
+    guarded([&] {
+        CsrMatrix B(n, n);
+        for (index_t i = 0; i <= n; ++i) B.row_ptr[i] = rp[i];
+        B.col_idx.assign(col, col + rp[n]);
+        B.values.assign(val, val + rp[n]);
+        const WeightedGraph g = build_weights(B, std::span<const real_t>(w, static_cast<std::size_t>(n)));
+        for (index_t i = 0; i <= n; ++i) grp[i] = g.adj.row_ptr[i];
+        std::copy(g.adj.col_idx.begin(), g.adj.col_idx.end(), gcol);
+        std::copy(g.adj.values.begin(), g.adj.values.end(), gw);
+        out = g.adj.nnz();
+    });
+    return out;
+}
+
+int orc_match_graph(int64_t n, const int64_t* rp, const int64_t* col, const double* w, int mode,
+                    int64_t* mate) {
+    return guarded([&] {
+        if (mode != 0)
+            throw Error(ErrorCode::invalid_argument, "reference suitor has only the strict acceptor");
+        WeightedGraph g;
+        g.n = n;
+        g.adj = CsrMatrix(n, n);
+        for (index_t i = 0; i <= n; ++i) g.adj.row_ptr[i] = rp[i];
+        g.adj.col_idx.assign(col, col + rp[n]);
+        g.adj.values.assign(w, w + rp[n]);
+        const Matching m = suitor_match(g);
+        std::copy(m.mate.begin(), m.mate.end(), mate);
+    });
+}
+
+int orc_set_solve(void* h, double rtol, int max_iters) {
+    return guarded([&] {
+        Session* s = S(h);
+        s->cfg.rtol = rtol;
+        s->cfg.max_iters = max_iters;
+    });
+}
+
 int orc_solve(void* h, const double* b, double* u, double* hist, int hist_cap, int* iters,
               double* relres, double* t_solve) {
     return guarded([&] {

@@ -34,6 +34,7 @@ EXPORTS = [
     "pairamg_prolongator_export", "pairamg_num_matchings", "pairamg_matching_export",
     "pairamg_get_setup_stats", "pairamg_set_kernel_timing", "pairamg_kernel_timing", "pairamg_launch_count",
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
+    "pairamg_match_graph",
 ]
 
 
@@ -133,6 +134,7 @@ def lib() -> C.CDLL:
         "pairamg_poisson_nnz": ([C.c_int, i64, i64, i64, i64, i64], i64),
         "pairamg_poisson_host": ([C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
         "pairamg_poisson_device": ([vp, C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
+        "pairamg_match_graph": ([vp, i64, vp, vp, vp, vp], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -179,6 +181,16 @@ def poisson(stencil: int, nx: int, ny: int, nz: int, row_begin: int = 0, row_end
 def uniform_partition(n: int, p: int) -> np.ndarray:
     """Partition::uniform (runtime.cpp:13-22)."""
     return np.array([(n // p) * r + min(n % p, r) for r in range(p + 1)], np.int64)
+
+
+def match_graph(rt: "Runtime", row_ptr, col, weight) -> np.ndarray:
+    """GPU parallel Suitor (total-order ties) on a weighted graph CSR -> mate."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col, np.int64)
+    w = np.ascontiguousarray(weight, np.float64)
+    mate = np.empty(len(rp) - 1, np.int64)
+    _check(lib().pairamg_match_graph(rt.h, len(rp) - 1, _ptr(rp), _ptr(ci), _ptr(w), _ptr(mate)))
+    return mate
 
 
 class Runtime:

@@ -54,6 +54,11 @@ struct Hierarchy {
     int nl() const { return static_cast<int>(levels.size()); }
 };
 
+// Parallel Suitor on a weighted graph CSR already on the device (the
+// k_suitor / k_mate kernels of the setup; exposed for matching KATs).
+void suitor_match_device(const int64_t* rp, const int32_t* col, const double* w, int64_t n, int64_t* mate,
+                         cudaStream_t s);
+
 // setup_hierarchy (amg.cpp:144-295) on the device.  The input is the owned
 // row block in global-column CSR (device buffers, ownership taken).
 void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBuf<int64_t>&& rp,

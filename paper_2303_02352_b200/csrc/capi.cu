@@ -452,6 +452,32 @@ pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* o
     });
 }
 
+pairamg_status pairamg_match_graph(pairamg_runtime* rt, int64_t n, const int64_t* row_ptr, const int64_t* col,
+                                   const double* weight, int64_t* mate) {
+    return guarded([&] {
+        if (!rt || n < 0 || !row_ptr) pb::fail(PAIRAMG_INVALID_ARGUMENT, "match_graph: bad arguments");
+        PB_CUDA(cudaSetDevice(rt->rt->device()));
+        cudaStream_t st = rt->rt->stream();
+        const int64_t m = row_ptr[n];
+        std::vector<int32_t> c32(static_cast<size_t>(m));
+        for (int64_t t = 0; t < m; ++t) {
+            if (col[t] < 0 || col[t] >= n) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "match_graph: column out of range");
+            c32[static_cast<size_t>(t)] = static_cast<int32_t>(col[t]);
+        }
+        pb::DBuf<int64_t> drp(static_cast<size_t>(n + 1), st), dm(static_cast<size_t>(n), st);
+        pb::DBuf<int32_t> dc(static_cast<size_t>(m), st);
+        pb::DBuf<double> dw(static_cast<size_t>(m), st);
+        PB_CUDA(cudaMemcpyAsync(drp.get(), row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, st));
+        if (m) {
+            PB_CUDA(cudaMemcpyAsync(dc.get(), c32.data(), 4 * m, cudaMemcpyHostToDevice, st));
+            PB_CUDA(cudaMemcpyAsync(dw.get(), weight, 8 * m, cudaMemcpyHostToDevice, st));
+        }
+        if (n) pb::suitor_match_device(drp.get(), dc.get(), dw.get(), n, dm.get(), st);
+        if (n) PB_CUDA(cudaMemcpyAsync(mate, dm.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 pairamg_status pairamg_set_kernel_timing(pairamg_solver* s, int enabled) {
     return guarded([&] { S(s).timing = enabled != 0; });
 }

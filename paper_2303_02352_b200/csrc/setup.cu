@@ -583,6 +583,15 @@ void extend_p(Runtime& rt, DevMatrix& A, const int32_t* pcol, const double* pval
 
 }  // namespace
 
+void suitor_match_device(const int64_t* rp, const int32_t* col, const double* w, int64_t n, int64_t* mate,
+                         cudaStream_t s) {
+    DBuf<ull> slot(static_cast<size_t>(2 * n), s);
+    slot.zero(s);
+    LAUNCH(k_suitor, n, rp, col, w, n, slot.get());
+    LAUNCH(k_mate, n, slot.get(), n, mate);
+    PB_CUDA(cudaStreamSynchronize(s));
+}
+
 void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBuf<int64_t>&& rp,
                      DBuf<int64_t>&& gcol, DBuf<double>&& val, int64_t nnz, const double* d_w0,
                      const SetupConfig& cfg) {

@@ -1,0 +1,94 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/*.h declares, carries sm_100a SASS, and the product never
+imports the oracle (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for h in os.listdir(os.path.join(ROOT, "include")):
+        if not h.endswith(".h"):
+            continue
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(pairamg_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import paper_2303_02352_b200 as pb
+    from paper_2303_02352_b200 import build
+
+    build.build()
+    return pb.lib()
+
+
+def test_header_declares_boundary():
+    names = declared_functions()
+    for must in ("pairamg_setup", "pairamg_solve", "pairamg_vcycle", "pairamg_spmv", "pairamg_runtime_create"):
+        assert must in names
+
+
+def test_every_declared_symbol_exported(lib):
+    import paper_2303_02352_b200 as pb
+
+    for name in declared_functions():
+        assert hasattr(lib, name), f"{name} declared in include/ but not exported"
+    assert set(pb.EXPORTS) == set(declared_functions())
+
+
+def test_status_names(lib):
+    import paper_2303_02352_b200 as pb
+
+    assert pb.lib().pairamg_abi_version() == 1
+    for i, name in enumerate(pb.ERROR_NAMES):
+        assert lib.pairamg_status_name(i).decode() == name
+
+
+def test_host_poisson_generator(lib):
+    """pairamg_poisson_host equals the oracle's generator."""
+    import numpy as np
+
+    import oracle
+    import paper_2303_02352_b200 as pb
+
+    for st, dims in ((7, (5, 4, 3)), (27, (4, 4, 4)), (7, (1, 1, 1))):
+        o = oracle.Oracle("restatement", stencil=st, nx=dims[0], ny=dims[1], nz=dims[2])
+        ref = o.input_csr()
+        got = pb.poisson(st, *dims)
+        for a, b in zip(got, ref):
+            np.testing.assert_array_equal(a, b)
+        n = dims[0] * dims[1] * dims[2]
+        # any row block
+        b0, b1 = n // 3, n - n // 4
+        rp, ci, va = pb.poisson(st, *dims, b0, b1)
+        np.testing.assert_array_equal(ci, ref[1][ref[0][b0]:ref[0][b1]])
+        np.testing.assert_array_equal(rp, ref[0][b0:b1 + 1] - ref[0][b0])
+
+
+def test_sm100a_code_present(lib):
+    import paper_2303_02352_b200 as pb
+
+    out = subprocess.run(["cuobjdump", "--list-elf", pb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_does_not_use_oracle():
+    pkg = os.path.join(ROOT, "paper_2303_02352_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "oracle_api.h" not in src and "libpairamg_ref" not in src, f
+    import paper_2303_02352_b200 as pb
+
+    out = subprocess.run(["ldd", pb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "pairamg_oracle" not in out and "pairamg_ref" not in out
