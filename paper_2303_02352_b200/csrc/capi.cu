@@ -486,7 +486,7 @@ pairamg_status pairamg_kernel_timing(pairamg_solver* s, int kclass, int64_t* lau
                                      double* bytes_per_launch) {
     return guarded([&] {
         pb::Solver& sv = S(s);
-        if (kclass < 0 || kclass >= 4) pb::fail(PAIRAMG_INVALID_ARGUMENT, "kernel class out of range");
+        if (kclass < 0 || kclass >= pb::kNumClasses) pb::fail(PAIRAMG_INVALID_ARGUMENT, "kernel class out of range");
         if (launches) *launches = sv.ktime[kclass].launches;
         if (ms) *ms = sv.ktime[kclass].ms;
         if (bytes_per_launch) *bytes_per_launch = sv.ktime[kclass].bytes_per_launch;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -37,6 +38,13 @@ private:
 #define PB_CHECK_LAUNCH() PB_CUDA(cudaGetLastError())
 
 constexpr int kSmCount = 148;  // B200: 148 SMs on two dies
+
+// Development switches (A/B of format and fusion choices), default on.
+inline bool env_flag(const char* name, bool dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
+}
 
 inline int blocks_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;

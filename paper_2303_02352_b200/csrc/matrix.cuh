@@ -55,11 +55,33 @@ struct DevMatrix {
 };
 
 struct Sell {
+    enum Format { kPlain = 0, kDict = 1 };
+    int format = kPlain;
     int64_t nrows = 0, nslices = 0, padded_nnz = 0;
-    DBuf<int64_t> slice_off;  // nslices+1, in elements (multiples of 32)
-    DBuf<int32_t> col;        // padded local column ids, -1 = pad
-    DBuf<double> val;
+    DBuf<int64_t> slice_off;  // nslices+1; elements (PLAIN) or 32-bit code words (DICT), multiples of 32
+    DBuf<int32_t> col;        // PLAIN: padded local column ids, -1 = pad
+    DBuf<double> val;         // PLAIN: values
+    DBuf<uint32_t> code;      // DICT: 4 one-byte codes per word, 0xFF = pad; [slice][word][lane]
+    int words = 0;            // DICT: words per row (uniform)
+    DBuf<int32_t> dcol;       // DICT: column - row per code
+    DBuf<double> dval;        // DICT: value per code
+    int ndict = 0;
     DBuf<int32_t> rows;       // row id of each SELL row; empty = identity
+};
+
+// Operators of the SELL kernels (sell.cu)
+enum SellOp { kSpmv = 0, kJacobi = 1, kResid = 2, kJacobiZero = 3, kJacobiProl = 4 };
+
+struct SellOpArgs {
+    int op = kSpmv;
+    const double* x = nullptr;  // iterate (gathered)
+    double* y = nullptr;        // output rows
+    const double* r = nullptr;  // right-hand side
+    const double* d = nullptr;  // l1 diagonal
+    double omega = 1.0;
+    const int32_t* pcol = nullptr;  // kJacobiProl: prolongator of the coarser level
+    const double* pval = nullptr;
+    const double* e = nullptr;      // kJacobiProl: coarse correction
 };
 
 // ---- sparse.cu ----
@@ -71,8 +93,12 @@ void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gco
               DBuf<double>&& val, int64_t nnz);
 // Global ids of M's columns (export).
 void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s);
-// SELL-32 copy of the rows listed in `rows` (nullptr = all rows).
-void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s);
+// ---- sell.cu ----
+// SELL-32 copy of the rows listed in `rows` (nullptr = all rows); DICT
+// encoding when allowed and the rows have <= 255 distinct (col-row, value).
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s,
+                bool allow_dict = true);
+double sell_bytes(const Sell& S);  // stored matrix bytes (codes+dictionary or cols+values)
 // l1_diagonal_dist (cycle.cpp:55-75); throws singular_smoother.
 void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s);
 // x_halo[h] <- owner's x for every halo slot (pack, NCCL send/recv). On `s`.
@@ -81,13 +107,8 @@ void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_ha
 void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_t* a_halo,
                         const double* b_owned, double* b_halo, cudaStream_t s);
 
-// Apply kernels on a Sell (all sums in CSR order, exactly rounded):
-//   SPMV   : y[row] = A x
-//   JACOBI : y[row] = x[row] + (omega*(r[row] - (A x)))/d[row]
-//   RESID  : y[row] = r[row] - (A x)
-enum SellOp { kSpmv = 0, kJacobi = 1, kResid = 2 };
-void sell_apply(const Sell& S, int op, const double* x, double* y, const double* r, const double* d,
-                double omega, cudaStream_t s);
+// Apply one operator (SellOp) on a Sell; all row sums in CSR order, exactly rounded.
+void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s);
 // v = A w plus per-block partials of (w.r, w.v, w.q) (FCG lines 10-13).
 // Returns the number of partial triples written.
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,

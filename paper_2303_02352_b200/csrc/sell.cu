@@ -1,0 +1,545 @@
+// sell.cu -- SELL-32 storage and the row-sum kernels of the solve path.
+//
+// Two lossless encodings of the same rows (matrix.cuh):
+//  * PLAIN : per-slice width, int32 column + f64 value per entry (12 B),
+//            pad column -1, slice offsets in `slice_off`.
+//  * DICT  : one byte per entry indexing a per-matrix dictionary of distinct
+//            (column - row, value) pairs (<= 255 pairs; code 0xFF = pad),
+//            packed 4 per 32-bit word; every row padded to the same W words
+//            so a lane's words sit at code[(slice*W + w)*32 + lane] (no offset
+//            table on the critical path).  Chosen automatically when the rows
+//            have <= 255 distinct pairs (every level of the slab-aligned
+//            Poisson hierarchies has 7 or 27).  The dictionary is staged in
+//            shared memory.  Columns and values are reproduced exactly, so
+//            every row sum is bit-identical to PLAIN and to spmv_local.
+//
+// Operators (one warp per slice, one lane per row, CSR-order sums with
+// separately rounded multiply/add; the row's own operands are loaded before
+// the gather chain so their latency overlaps it):
+//   kSpmv        y = A x                                  (spmv_dist, dist.cpp:277-300)
+//   kJacobi      y = x + (omega*(r - A x))/d              (cycle.cpp:96-100)
+//   kResid       y = r - A x                              (cycle.cpp:141-143)
+//   kJacobiZero  zero-start sweep (cycle.cpp:89-93) fused into the next sweep,
+//                x1 = (omega*r)/d recomputed per gathered column
+//   kJacobiProl  prolongate_add (cycle.cpp:117-124) fused into the first post-sweep
+//   spmv+dots    v = A w with the FCG dot triple (w.r, w.v, w.q) (Alg. 1 l.10-13)
+// The two fused operators trade stored bytes for per-entry recomputation; on
+// B200 they measured slower than the separate kernels and are
+// off by default (PAIRAMG_FUSE=1 enables them).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace pb {
+
+namespace {
+
+using ull = unsigned long long;
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kDictMax = 255;
+constexpr int kTableCap = 1024;
+constexpr ull kEmptyLo = 0x8000000000000000ULL;
+
+struct SellArgs {
+    const int64_t* soff;  // PLAIN
+    const int32_t* col;
+    const double* val;
+    const uint32_t* code;  // DICT
+    int words;             // DICT: words per row
+    const int32_t* dcol;
+    const double* dval;
+    int ndict;
+    const int32_t* rows;
+    int64_t nslices, nrows;
+    const double* x;
+    double* y;
+    const double* r;
+    const double* d;
+    double omega;
+    const int32_t* pcol;
+    const double* pval;
+    const double* e;
+    const double* q;
+    double* partials;
+};
+
+template <int OP>
+__device__ __forceinline__ double xval(const SellArgs& a, int c) {
+    if (OP == kJacobiZero) return ddiv(dmul(a.omega, __ldg(a.r + c)), __ldg(a.d + c));
+    if (OP == kJacobiProl) return dadd(__ldg(a.x + c), dmul(__ldg(a.pval + c), __ldg(a.e + __ldg(a.pcol + c))));
+    return __ldg(a.x + c);
+}
+
+template <int OP>
+__device__ __forceinline__ double row_sum_plain(const SellArgs& a, int64_t slice, int lane) {
+    const int64_t beg = a.soff[slice];
+    const int width = static_cast<int>((a.soff[slice + 1] - beg) >> 5);
+    const int32_t* cp = a.col + beg + lane;
+    const double* vp = a.val + beg + lane;
+    double sum = 0.0;
+    for (int k = 0; k < width; k += 8) {
+        int c[8];
+        double av[8], xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const bool in = k + j < width;
+            c[j] = in ? __ldg(cp + (k + j) * 32) : -1;
+            av[j] = in ? __ldg(vp + (k + j) * 32) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = c[j] >= 0 ? xval<OP>(a, c[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (c[j] >= 0) sum = dadd(sum, dmul(av[j], xv[j]));
+    }
+    return sum;
+}
+
+// DICT row sum: the lane's words are code[(slice*W + w)*32 + lane]; 32-bit
+// index math throughout (the encoded matrix is < 2^31 words).
+template <int OP>
+__device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int lane, int row,
+                                               const int32_t* sdcol, const double* sdval) {
+    const int W = a.words;
+    const uint32_t* cp = a.code + (slice * W) * 32 + lane;
+    double sum = 0.0;
+    for (int w0 = 0; w0 < W; w0 += 2) {
+        const uint32_t wa = __ldg(cp + w0 * 32);
+        const uint32_t wb = w0 + 1 < W ? __ldg(cp + (w0 + 1) * 32) : 0xFFFFFFFFu;
+        uint32_t e[8];
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = ((j < 4 ? wa : wb) >> (8 * (j & 3))) & 0xFFu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = e[j] != 0xFFu ? xval<OP>(a, row + sdcol[e[j]]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (e[j] != 0xFFu) sum = dadd(sum, dmul(sdval[e[j]], xv[j]));
+    }
+    return sum;
+}
+
+template <bool DICT>
+__device__ __forceinline__ void load_dict(const SellArgs& a, int32_t* sdcol, double* sdval) {
+    if (DICT) {
+        for (int i = threadIdx.x; i < a.ndict; i += blockDim.x) {
+            sdcol[i] = a.dcol[i];
+            sdval[i] = a.dval[i];
+        }
+        __syncthreads();
+    }
+}
+
+template <int OP, bool ROWS, bool DICT>
+__global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
+    __shared__ int32_t sdcol[DICT ? kDictMax : 1];
+    __shared__ double sdval[DICT ? kDictMax : 1];
+    load_dict<DICT>(a, sdcol, sdval);
+    const int lane = threadIdx.x & 31;
+    const int slice = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (slice >= a.nslices) return;
+    const int sr = slice * 32 + lane;
+    const bool valid = sr < a.nrows;
+    const int row = !valid ? 0 : (ROWS ? a.rows[sr] : sr);
+    // own-row operands first: their latency overlaps the gather chain
+    double xi = 0.0, ri = 0.0, di = 1.0;
+    if (valid) {
+        if (OP == kJacobi || OP == kJacobiZero || OP == kJacobiProl) {
+            ri = a.r[row];
+            di = a.d[row];
+        }
+        if (OP == kResid) ri = a.r[row];
+        if (OP == kJacobi) xi = a.x[row];
+    }
+    const double sum = DICT ? row_sum_dict<OP>(a, slice, lane, row, sdcol, sdval) : row_sum_plain<OP>(a, slice, lane);
+    if (!valid) return;
+    if (OP == kSpmv) {
+        a.y[row] = sum;
+    } else if (OP == kResid) {
+        a.y[row] = dsub(ri, sum);
+    } else {
+        if (OP != kJacobi) xi = xval<OP>(a, row);
+        a.y[row] = dadd(xi, ddiv(dmul(a.omega, dsub(ri, sum)), di));
+    }
+}
+
+// v = A w with block partials of (w.r, w.v, w.q); grid-stride over slices so
+// the partial count is bounded by the grid (fixed order -> deterministic).
+template <bool DICT>
+__global__ void __launch_bounds__(kThreads) k_sell_spmv_dots(SellArgs a) {
+    __shared__ int32_t sdcol[DICT ? kDictMax : 1];
+    __shared__ double sdval[DICT ? kDictMax : 1];
+    load_dict<DICT>(a, sdcol, sdval);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    for (int slice = blockIdx.x * kWarps + warp; slice < a.nslices; slice += gridDim.x * kWarps) {
+        const int row = slice * 32 + lane;
+        const bool valid = row < a.nrows;
+        double wi = 0.0, rr = 0.0, qq = 0.0;
+        if (valid) {
+            wi = a.x[row];
+            rr = a.r[row];
+            qq = a.q[row];
+        }
+        const double sum = DICT ? row_sum_dict<kSpmv>(a, slice, lane, row, sdcol, sdval)
+                                : row_sum_plain<kSpmv>(a, slice, lane);
+        if (valid) {
+            a.y[row] = sum;
+            sa = dadd(sa, dmul(wi, rr));
+            sb = dadd(sb, dmul(wi, sum));
+            sg = dadd(sg, dmul(wi, qq));
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    __shared__ double red[3][kWarps];
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int i = 0; i < kWarps; ++i) acc = dadd(acc, red[threadIdx.x][i]);
+        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}
+
+// ------------------------------------------------------------- building ---
+
+__global__ void k_sell_width(const int64_t* __restrict__ rp, const int32_t* __restrict__ rows, int64_t nrows,
+                             int64_t nslices, int64_t* __restrict__ width) {
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= nslices) return;
+    const int64_t sr = s * 32 + lane;
+    int len = 0;
+    if (sr < nrows) {
+        const int64_t row = rows ? rows[sr] : sr;
+        len = static_cast<int>(rp[row + 1] - rp[row]);
+    }
+    for (int o = 16; o; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+    if (lane == 0) width[s] = 32LL * len;
+}
+
+__global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                            const int64_t* __restrict__ soff, int32_t* __restrict__ scol, double* __restrict__ sval) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : sr;
+    const int64_t base = soff[sr >> 5] + (sr & 31);
+    const int64_t b = rp[row], e = rp[row + 1];
+    for (int64_t t = b; t < e; ++t) {
+        scol[base + (t - b) * 32] = col[t];
+        sval[base + (t - b) * 32] = val[t];
+    }
+}
+
+__device__ __forceinline__ void ld_slot(const ull* p, ull& lo, ull& hi) {
+    asm volatile(
+        "{\n\t.reg .b128 v;\n\t"
+        "ld.relaxed.gpu.global.b128 v, [%2];\n\t"
+        "mov.b128 {%0, %1}, v;\n\t}"
+        : "=l"(lo), "=l"(hi)
+        : "l"(p)
+        : "memory");
+}
+
+__device__ __forceinline__ bool cas_slot(ull* p, ull cmp_lo, ull cmp_hi, ull new_lo, ull new_hi) {
+    ull old_lo, old_hi;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%3, %4};\n\t"
+        "mov.b128 n, {%5, %6};\n\t"
+        "atom.relaxed.gpu.global.cas.b128 o, [%2], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old_lo), "=l"(old_hi)
+        : "l"(p), "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi)
+        : "memory");
+    return old_lo == cmp_lo && old_hi == cmp_hi;
+}
+
+__device__ __forceinline__ unsigned slot_hash(ull lo, ull hi) {
+    ull h = lo * 0x9E3779B97F4A7C15ULL ^ (hi + 0x632BE59BD9B4E019ULL) * 0xC2B2AE3D27D4EB4FULL;
+    return static_cast<unsigned>(h >> 40) & (kTableCap - 1);
+}
+
+// Find (or insert) key (delta, value bits) in the open-addressing table;
+// returns the slot, or -1 on overflow / absence.  Slots go empty -> key once
+// (128-bit CAS) and are read with single-copy-atomic 128-bit loads.
+__device__ int table_find(ull* table, ull lo, ull hi, bool insert, unsigned* count, int* overflow) {
+    unsigned h = slot_hash(lo, hi);
+    for (int probe = 0; probe < kTableCap; ++probe, h = (h + 1) & (kTableCap - 1)) {
+        ull slo, shi;
+        ld_slot(table + 2 * h, slo, shi);
+        if (slo == lo && shi == hi) return static_cast<int>(h);
+        if (slo == kEmptyLo && shi == 0) {
+            if (!insert) return -1;
+            if (*reinterpret_cast<volatile int*>(overflow)) return -1;
+            if (cas_slot(table + 2 * h, kEmptyLo, 0, lo, hi)) {
+                if (atomicAdd(count, 1u) >= static_cast<unsigned>(kDictMax)) atomicExch(overflow, 1);
+                return static_cast<int>(h);
+            }
+            ld_slot(table + 2 * h, slo, shi);  // lost the race: the winner's key is there now
+            if (slo == lo && shi == hi) return static_cast<int>(h);
+        }
+    }
+    if (overflow) atomicExch(overflow, 1);
+    return -1;
+}
+
+__global__ void k_table_init(ull* table) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kTableCap) {
+        table[2 * i] = kEmptyLo;
+        table[2 * i + 1] = 0;
+    }
+}
+
+__global__ void k_dict_insert(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                              ull* table, unsigned* count, int* overflow, unsigned* maxlen) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : sr;
+    atomicMax(maxlen, static_cast<unsigned>(rp[row + 1] - rp[row]));
+    for (int64_t t = rp[row]; t < rp[row + 1]; ++t) {
+        if (*reinterpret_cast<volatile int*>(overflow)) return;
+        const ull lo = static_cast<ull>(static_cast<int64_t>(col[t]) - row);
+        const ull hi = static_cast<ull>(__double_as_longlong(val[t]));
+        if (table_find(table, lo, hi, true, count, overflow) < 0) return;
+    }
+}
+
+__global__ void k_sell_fill_dict(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                                 int W, ull* table, const int* __restrict__ slot_code, uint32_t* __restrict__ code,
+                                 int* bad) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : sr;
+    const int64_t base = (sr >> 5) * W * 32 + (sr & 31);
+    const int64_t b = rp[row], e = rp[row + 1];
+    for (int w = 0; w < W; ++w) {
+        uint32_t word = 0xFFFFFFFFu;
+        for (int j = 0; j < 4; ++j) {
+            const int64_t t = b + 4 * w + j;
+            if (t >= e) break;
+            const ull lo = static_cast<ull>(static_cast<int64_t>(col[t]) - row);
+            const ull hi = static_cast<ull>(__double_as_longlong(val[t]));
+            const int slot = table_find(table, lo, hi, false, nullptr, nullptr);
+            const int c = slot < 0 ? -1 : slot_code[slot];
+            if (c < 0) {
+                atomicExch(bad, 1);
+                continue;
+            }
+            word = (word & ~(0xFFu << (8 * j))) | (static_cast<uint32_t>(c) << (8 * j));
+        }
+        code[base + static_cast<int64_t>(w) * 32] = word;
+    }
+}
+
+template <typename F>
+void cub_call(F&& f, cudaStream_t s) {
+    size_t bytes = 0;
+    PB_CUDA(f(nullptr, bytes));
+    DBuf<uint8_t> tmp(bytes ? bytes : 1, s);
+    PB_CUDA(f(tmp.get(), bytes));
+}
+
+bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) {
+    if (S.nrows == 0) return false;
+    if (S.nslices * 32 >= (int64_t(1) << 31) / 8) return false;  // 32-bit code index range
+    DBuf<ull> table(2 * kTableCap, s);
+    DBuf<unsigned> cnt(2, s);  // [0] distinct pairs, [1] longest row
+    DBuf<int> flags(2, s);
+    cnt.zero(s);
+    flags.zero(s);
+    k_table_init<<<kTableCap / 256, 256, 0, s>>>(table.get());
+    k_dict_insert<<<blocks_for(S.nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, S.nrows,
+                                                            table.get(), cnt.get(), flags.get(), cnt.get() + 1);
+    PB_CHECK_LAUNCH();
+    int over = 0;
+    unsigned hc[2] = {0, 0};
+    PB_CUDA(cudaMemcpyAsync(&over, flags.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaMemcpyAsync(hc, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
+    std::vector<ull> h(2 * kTableCap);
+    PB_CUDA(cudaMemcpyAsync(h.data(), table.get(), 16 * kTableCap, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (over) return false;
+    // deterministic code order: ascending (delta, value bits)
+    std::vector<std::pair<std::pair<int64_t, int64_t>, int>> keys;
+    for (int i = 0; i < kTableCap; ++i)
+        if (!(h[2 * i] == kEmptyLo && h[2 * i + 1] == 0))
+            keys.push_back({{static_cast<int64_t>(h[2 * i]), static_cast<int64_t>(h[2 * i + 1])}, i});
+    if (keys.empty() || keys.size() > static_cast<size_t>(kDictMax)) return false;
+    std::sort(keys.begin(), keys.end());
+    std::vector<int> slot_code(kTableCap, -1);
+    std::vector<int32_t> dcol(keys.size());
+    std::vector<double> dval(keys.size());
+    for (size_t c = 0; c < keys.size(); ++c) {
+        slot_code[keys[c].second] = static_cast<int>(c);
+        dcol[c] = static_cast<int32_t>(keys[c].first.first);
+        const int64_t bitsv = keys[c].first.second;
+        std::memcpy(&dval[c], &bitsv, 8);
+    }
+    S.ndict = static_cast<int>(keys.size());
+    S.words = static_cast<int>((hc[1] + 3) / 4);
+    if (S.words == 0) S.words = 1;
+    S.dcol.alloc(keys.size(), s);
+    S.dval.alloc(keys.size(), s);
+    PB_CUDA(cudaMemcpyAsync(S.dcol.get(), dcol.data(), 4 * dcol.size(), cudaMemcpyHostToDevice, s));
+    PB_CUDA(cudaMemcpyAsync(S.dval.get(), dval.data(), 8 * dval.size(), cudaMemcpyHostToDevice, s));
+    DBuf<int> dsc(kTableCap, s);
+    PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
+    S.padded_nnz = S.nslices * 32 * S.words;  // in words
+    S.code.alloc(static_cast<size_t>(S.padded_nnz), s);
+    PB_CUDA(cudaMemsetAsync(S.code.get(), 0xff, 4 * S.padded_nnz, s));
+    k_sell_fill_dict<<<blocks_for(S.nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, S.nrows,
+                                                              S.words, table.get(), dsc.get(), S.code.get(),
+                                                              flags.get() + 1);
+    PB_CHECK_LAUNCH();
+    int bad = 0;
+    PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (bad) fail(PAIRAMG_INTERNAL, "sell: dictionary encoding lost an entry");
+    S.format = Sell::kDict;
+    return true;
+}
+
+SellArgs args_of(const Sell& S) {
+    SellArgs a{};
+    a.soff = S.slice_off.get();
+    a.col = S.col.get();
+    a.val = S.val.get();
+    a.code = S.code.get();
+    a.words = S.words;
+    a.dcol = S.dcol.get();
+    a.dval = S.dval.get();
+    a.ndict = S.ndict;
+    a.rows = S.rows.empty() ? nullptr : S.rows.get();
+    a.nslices = S.nslices;
+    a.nrows = S.nrows;
+    return a;
+}
+
+template <int OP>
+void launch_op(const Sell& S, const SellArgs& a, cudaStream_t s) {
+    const int grid = blocks_for(S.nslices, kWarps);
+    const bool rows = a.rows != nullptr;
+    if (S.format == Sell::kDict) {
+        if (rows)
+            k_sell<OP, true, true><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_sell<OP, false, true><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        if (rows)
+            k_sell<OP, true, false><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_sell<OP, false, false><<<grid, kThreads, 0, s>>>(a);
+    }
+    PB_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict) {
+    S = Sell();
+    S.nrows = nrows;
+    S.nslices = (nrows + 31) / 32;
+    if (S.nslices * 32 >= (int64_t(1) << 31))
+        fail(PAIRAMG_INVALID_ARGUMENT, "sell: more than 2^31 rows per rank");
+    if (rows) {
+        S.rows.alloc(static_cast<size_t>(nrows), s);
+        if (nrows) PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
+    }
+    if (allow_dict && try_dict(M, rows, S, s)) return;
+    S.format = Sell::kPlain;
+    S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
+    PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
+    if (S.nslices) {
+        k_sell_width<<<blocks_for(S.nslices * 32, 256), 256, 0, s>>>(M.rp.get(), rows, S.nrows, S.nslices,
+                                                                     S.slice_off.get());
+        PB_CHECK_LAUNCH();
+        cub_call([&](void* t, size_t& bytes) {
+            return cub::DeviceScan::ExclusiveSum(t, bytes, S.slice_off.get(), S.slice_off.get(), S.nslices + 1, s);
+        }, s);
+    }
+    PB_CUDA(cudaMemcpyAsync(&S.padded_nnz, S.slice_off.get() + S.nslices, 8, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    S.col.alloc(static_cast<size_t>(S.padded_nnz), s);
+    S.val.alloc(static_cast<size_t>(S.padded_nnz), s);
+    if (S.padded_nnz) {
+        PB_CUDA(cudaMemsetAsync(S.col.get(), 0xff, 4 * S.padded_nnz, s));
+        PB_CUDA(cudaMemsetAsync(S.val.get(), 0, 8 * S.padded_nnz, s));
+    }
+    if (nrows) {
+        k_sell_fill<<<blocks_for(nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, nrows,
+                                                           S.slice_off.get(), S.col.get(), S.val.get());
+        PB_CHECK_LAUNCH();
+    }
+}
+
+double sell_bytes(const Sell& S) {
+    if (S.format == Sell::kDict) return 4.0 * S.padded_nnz + 12.0 * S.ndict;
+    return 12.0 * S.padded_nnz + 8.0 * (S.nslices + 1);
+}
+
+void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
+    if (!S.nslices) return;
+    SellArgs a = args_of(S);
+    a.x = o.x;
+    a.y = o.y;
+    a.r = o.r;
+    a.d = o.d;
+    a.omega = o.omega;
+    a.pcol = o.pcol;
+    a.pval = o.pval;
+    a.e = o.e;
+    switch (o.op) {
+        case kSpmv: launch_op<kSpmv>(S, a, s); break;
+        case kJacobi: launch_op<kJacobi>(S, a, s); break;
+        case kResid: launch_op<kResid>(S, a, s); break;
+        case kJacobiZero: launch_op<kJacobiZero>(S, a, s); break;
+        case kJacobiProl: launch_op<kJacobiProl>(S, a, s); break;
+        default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
+    }
+}
+
+int sell_dots_grid(const Sell& S) {
+    const int64_t want = (S.nslices + kWarps - 1) / kWarps;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
+}
+
+int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q, double* partials,
+                   int max_blocks, cudaStream_t s) {
+    if (!S.rows.empty()) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: row-list SELL not supported");
+    const int grid = sell_dots_grid(S);
+    if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
+    SellArgs a = args_of(S);
+    a.x = w;
+    a.y = v;
+    a.r = r;
+    a.q = q;
+    a.partials = partials;
+    if (S.format == Sell::kDict)
+        k_sell_spmv_dots<true><<<grid, kThreads, 0, s>>>(a);
+    else
+        k_sell_spmv_dots<false><<<grid, kThreads, 0, s>>>(a);
+    PB_CHECK_LAUNCH();
+    return grid;
+}
+
+}  // namespace pb

@@ -191,6 +191,7 @@ int red_grid(int64_t n) {
 }  // namespace
 
 Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
+    fuse = env_flag("PAIRAMG_FUSE", false);
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
@@ -281,7 +282,7 @@ void Solver::end_time(int kc) {
 
 void Solver::collect_times() {
     if (!timing) return;
-    for (int kc = 0; kc < 4; ++kc)
+    for (int kc = 0; kc < kNumClasses; ++kc)
         for (int i = 0; i < tcount_[kc]; ++i) {
             float ms = 0.f;
             PB_CUDA(cudaEventElapsedTime(&ms, tev_[kc][i].first, tev_[kc][i].second));
@@ -290,29 +291,43 @@ void Solver::collect_times() {
         }
 }
 
-void Solver::apply(int k, int op, const double* x, double* y, const double* r, const double* d, double omega,
-                   int kc) {
+void Solver::apply(int k, const SellOpArgs& o, int kc) {
     Level& L = *h.levels[k];
     begin_time(kc);
     if (L.A.halo.has_traffic()) {
+        if (o.op == kJacobiZero || o.op == kJacobiProl)
+            fail(PAIRAMG_INTERNAL, "fused sweeps need a level without halo traffic");
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
-        halo_exchange(rt, L.A.halo, x, const_cast<double*>(x) + L.A.n, rt.comm_stream());
+        halo_exchange(rt, L.A.halo, o.x, const_cast<double*>(o.x) + L.A.n, rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += L.A.halo.send_off.back() ? 1 : 0;
     }
     if (L.A.halo.n_halo > 0) {
-        sell_apply(L.sell_int, op, x, y, r, d, omega, s_);
+        sell_apply(L.sell_int, o, s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        sell_apply(L.sell_bnd, op, x, y, r, d, omega, s_);
+        sell_apply(L.sell_bnd, o, s_);
         launches_ += 2;
     } else {
         if (L.A.halo.has_traffic()) PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        sell_apply(L.sell_all, op, x, y, r, d, omega, s_);
+        sell_apply(L.sell_all, o, s_);
         launches_ += 1;
     }
     end_time(kc);
 }
+
+static SellOpArgs jacobi_args(int op, const double* x, double* y, const double* rhs, const double* d, double omega) {
+    SellOpArgs o;
+    o.op = op;
+    o.x = x;
+    o.y = y;
+    o.r = rhs;
+    o.d = d;
+    o.omega = omega;
+    return o;
+}
+
+bool Solver::fusable(int k) const { return fuse && !h.levels[k]->A.halo.has_traffic(); }
 
 void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
                     bool l0) {
@@ -323,16 +338,19 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
         return;
     }
     int sweep = 0;
-    if (zero_start) {
-        begin_time(l0 ? 0 : -1);
+    if (zero_start && nu >= 2 && fusable(k)) {
+        // sweeps 1+2 in one pass: x1 = (omega*r)/d is formed at every gathered column
+        apply(k, jacobi_args(kJacobiZero, nullptr, xc, rhs, L.l1.get(), omega), l0 ? 4 : -1);
+        sweep = 2;
+    } else if (zero_start) {
+        begin_time(-1);
         if (n) k_zero_start<<<blocks_for(n, 256), 256, 0, s_>>>(rhs, L.l1.get(), xc, n, omega);
         PB_CHECK_LAUNCH();
-        end_time(l0 ? 0 : -1);
         launches_ += 1;
-        ++sweep;
+        sweep = 1;
     }
     for (; sweep < nu; ++sweep) {
-        apply(k, kJacobi, xc, xo, rhs, L.l1.get(), omega, l0 ? 0 : -1);
+        apply(k, jacobi_args(kJacobi, xc, xo, rhs, L.l1.get(), omega), l0 ? 0 : -1);
         std::swap(xc, xo);
     }
 }
@@ -348,7 +366,14 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         return;
     }
     smooth(k, true, cc.pre_sweeps, rhs, xc, xo, cc.relax_weight, l0);
-    apply(k, kResid, xc, L.res.get(), rhs, nullptr, 0.0, l0 ? 1 : -1);
+    {
+        SellOpArgs o;
+        o.op = kResid;
+        o.x = xc;
+        o.y = L.res.get();
+        o.r = rhs;
+        apply(k, o, l0 ? 1 : -1);
+    }
     Level& C = *h.levels[k + 1];
     if (C.A.n) k_restrict<<<blocks_for(C.A.n, 256), 256, 0, s_>>>(C.rrp.get(), C.rcol.get(), C.rval.get(),
                                                                     L.res.get(), C.rhs.get(), C.A.n);
@@ -356,10 +381,22 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     launches_ += 1;
     double* e = nullptr;
     vcycle_enqueue(k + 1, C.rhs.get(), e, cc);
-    if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(C.pcol.get(), C.pval.get(), e, xc, L.A.n);
-    PB_CHECK_LAUNCH();
-    launches_ += 1;
-    smooth(k, false, cc.post_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+    int post = cc.post_sweeps;
+    if (post >= 1 && fusable(k)) {
+        // prolongate_add fused into the first post-sweep: x_j + p_j*e_agg(j) on the fly
+        SellOpArgs o = jacobi_args(kJacobiProl, xc, xo, rhs, L.l1.get(), cc.relax_weight);
+        o.pcol = C.pcol.get();
+        o.pval = C.pval.get();
+        o.e = e;
+        apply(k, o, l0 ? 5 : -1);
+        std::swap(xc, xo);
+        --post;
+    } else {
+        if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(C.pcol.get(), C.pval.get(), e, xc, L.A.n);
+        PB_CHECK_LAUNCH();
+        launches_ += 1;
+    }
+    smooth(k, false, post, rhs, xc, xo, cc.relax_weight, l0);
     out = xc;
 }
 
@@ -411,7 +448,11 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         end_time(2);
         launches_ += 1;
     } else {
-        apply(0, kSpmv, w, v_.get(), nullptr, nullptr, 0.0, 2);
+        SellOpArgs o;
+        o.op = kSpmv;
+        o.x = w;
+        o.y = v_.get();
+        apply(0, o, 2);
         k_dots3<<<red_grid(n_), kRedThreads, 0, s_>>>(w, v_.get(), r_.get(), q_.get(), n_, partials_.get());
         PB_CHECK_LAUNCH();
         launches_ += 1;
@@ -434,11 +475,18 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
         fail(PAIRAMG_INVALID_ARGUMENT, "cycle config: sweep counts must be >= 0");
     Level& L0 = *h.levels[0];
     for (auto& kt : ktime) kt = KernelClassTiming{};
-    const double nnz0 = static_cast<double>(L0.A.nnz), n0 = static_cast<double>(n_);
-    ktime[0].bytes_per_launch = 12.0 * nnz0 + 36.0 * n0;  // Jacobi sweep
-    ktime[1].bytes_per_launch = 12.0 * nnz0 + 28.0 * n0;  // residual
-    ktime[2].bytes_per_launch = 12.0 * nnz0 + 36.0 * n0;  // SpMV + dot triple (reads r, q)
-    ktime[3].bytes_per_launch = 80.0 * n0;                // 6 vectors read, 4 written
+    // Algorithmic bytes per level-0 launch of the stored format (matrix
+    // entries once + every vector once; gathers counted once).
+    const double n0 = static_cast<double>(n_);
+    const double mat = L0.A.halo.n_halo > 0 ? sell_bytes(L0.sell_int) + sell_bytes(L0.sell_bnd)
+                                            : sell_bytes(L0.sell_all);
+    const double nc1 = h.nl() > 1 ? static_cast<double>(h.levels[1]->A.n) : 0.0;
+    ktime[0].bytes_per_launch = mat + 32.0 * n0;              // x, r, d read; y written
+    ktime[1].bytes_per_launch = mat + 24.0 * n0;              // x, r read; y written
+    ktime[2].bytes_per_launch = mat + 32.0 * n0;              // w, r, q read; v written
+    ktime[3].bytes_per_launch = 80.0 * n0;                    // 6 vectors read, 4 written
+    ktime[4].bytes_per_launch = mat + 24.0 * n0;              // r, d read; y written
+    ktime[5].bytes_per_launch = mat + 44.0 * n0 + 8.0 * nc1;  // x, p, pcol, r, d read, e; y written
 
     cudaEvent_t e0, e1;
     PB_CUDA(cudaEventCreate(&e0));
@@ -453,7 +501,14 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     }
     const bool timing_save = timing;
     timing = false;
-    apply(0, kResid, u_.get(), r_.get(), d_b, nullptr, 0.0, -1);
+    {
+        SellOpArgs o;
+        o.op = kResid;
+        o.x = u_.get();
+        o.y = r_.get();
+        o.r = d_b;
+        apply(0, o, -1);
+    }
     k_norm_partials<<<red_grid(n_), kRedThreads, 0, s_>>>(r_.get(), n_, partials_.get());
     PB_CHECK_LAUNCH();
     launches_ += 1;
@@ -538,7 +593,11 @@ void Solver::spmv(int level, const double* d_x, double* d_y) {
     if (L.A.n) PB_CUDA(cudaMemcpyAsync(L.xt.get(), d_x, 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
     const bool t = timing;
     timing = false;
-    apply(level, kSpmv, L.xt.get(), L.res.get(), nullptr, nullptr, 0.0, -1);
+    SellOpArgs o;
+    o.op = kSpmv;
+    o.x = L.xt.get();
+    o.y = L.res.get();
+    apply(level, o, -1);
     timing = t;
     if (L.A.n) PB_CUDA(cudaMemcpyAsync(d_y, L.res.get(), 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
     PB_CUDA(cudaStreamSynchronize(s_));

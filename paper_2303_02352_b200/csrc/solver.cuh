@@ -19,6 +19,11 @@ struct FcgState {
     int status;                      // 0 ok, 1 breakdown
 };
 
+// Timed kernel classes (level 0): 0 plain l1-Jacobi sweep, 1 residual,
+// 2 SpMV + dot triple, 3 FCG vector update, 4 fused zero-start sweep,
+// 5 fused prolongation sweep.
+constexpr int kNumClasses = 6;
+
 struct KernelClassTiming {
     int64_t launches = 0;
     double ms = 0.0;
@@ -42,15 +47,16 @@ public:
     Hierarchy h;
     bool ready = false;
     bool timing = false;
-    std::array<KernelClassTiming, 4> ktime{};
+    bool fuse = true;  // fused zero-start / prolongation sweeps on halo-free levels
+    std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
 private:
     // enqueue helpers (host-side pointer bookkeeping; graph-capturable)
     void smooth(int k, bool zero_start, int nu, const double* rhs, double*& xcur, double*& xoth, double omega,
                 bool time_l0);
-    void apply(int k, int op, const double* x, double* y, const double* r, const double* d, double omega,
-               int kclass);
+    void apply(int k, const SellOpArgs& o, int kclass);
+    bool fusable(int k) const;
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
     void reduce_dots_enqueue();
@@ -78,9 +84,9 @@ private:
     std::vector<cudaEvent_t> ev_pool_;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     // per-class event pairs recorded in the captured iteration
-    std::array<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>, 4> tev_{};
-    std::array<int, 4> tcount_{};
-    std::array<int, 4> topen_{};
+    std::array<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>, kNumClasses> tev_{};
+    std::array<int, kNumClasses> tcount_{};
+    std::array<int, kNumClasses> topen_{};
     int64_t launches_ = 0;
 };
 

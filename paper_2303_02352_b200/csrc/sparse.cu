@@ -103,134 +103,6 @@ __global__ void k_l1(const int64_t* __restrict__ rp, const int32_t* __restrict__
     d[i] = acc;
 }
 
-// SELL widths: one warp per slice, width = longest row of the slice.
-__global__ void k_sell_width(const int64_t* __restrict__ rp, const int32_t* __restrict__ rows,
-                             int64_t nrows, int64_t nslices, int64_t* __restrict__ w32) {
-    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (s >= nslices) return;
-    const int64_t sr = s * 32 + lane;
-    int len = 0;
-    if (sr < nrows) {
-        const int64_t row = rows ? rows[sr] : sr;
-        len = static_cast<int>(rp[row + 1] - rp[row]);
-    }
-    for (int o = 16; o; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
-    if (lane == 0) w32[s] = 32LL * len;
-}
-
-__global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                            const double* __restrict__ val, const int32_t* __restrict__ rows,
-                            int64_t nrows, const int64_t* __restrict__ soff, int32_t* __restrict__ scol,
-                            double* __restrict__ sval) {
-    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (sr >= nrows) return;
-    const int64_t row = rows ? rows[sr] : sr;
-    const int64_t s = sr >> 5;
-    const int lane = static_cast<int>(sr & 31);
-    const int64_t base = soff[s] + lane;
-    const int64_t b = rp[row], e = rp[row + 1];
-    for (int64_t t = b; t < e; ++t) {
-        scol[base + (t - b) * 32] = col[t];
-        sval[base + (t - b) * 32] = val[t];
-    }
-}
-
-constexpr int kSellThreads = 256;
-constexpr int kSellWarps = kSellThreads / 32;
-constexpr int kChunk = 8;
-
-// Row sum of one SELL lane in CSR order: sum = 0.0; sum += a*x (exact).
-__device__ __forceinline__ double sell_row_sum(const int32_t* __restrict__ cp,
-                                               const double* __restrict__ vp, int width,
-                                               const double* __restrict__ x) {
-    double sum = 0.0;
-    for (int k = 0; k < width; k += kChunk) {
-        int c[kChunk];
-        double a[kChunk], xv[kChunk];
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-            const bool in = k + j < width;
-            c[j] = in ? __ldg(cp + (k + j) * 32) : -1;
-            a[j] = in ? __ldg(vp + (k + j) * 32) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j)
-            if (c[j] >= 0) sum = dadd(sum, dmul(a[j], xv[j]));
-    }
-    return sum;
-}
-
-template <int OP, bool ROWS>
-__global__ void __launch_bounds__(kSellThreads)
-    k_sell(const int64_t* __restrict__ soff, const int32_t* __restrict__ col,
-           const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nslices,
-           int64_t nrows, const double* __restrict__ x, double* __restrict__ y,
-           const double* __restrict__ r, const double* __restrict__ d, double omega) {
-    const int lane = threadIdx.x & 31;
-    const int64_t slice = static_cast<int64_t>(blockIdx.x) * kSellWarps + (threadIdx.x >> 5);
-    if (slice >= nslices) return;
-    const int64_t beg = soff[slice];
-    const int width = static_cast<int>((soff[slice + 1] - beg) >> 5);
-    const double sum = sell_row_sum(col + beg + lane, val + beg + lane, width, x);
-    const int64_t sr = slice * 32 + lane;
-    if (sr >= nrows) return;
-    const int64_t row = ROWS ? rows[sr] : sr;
-    if (OP == kSpmv) {
-        y[row] = sum;
-    } else if (OP == kJacobi) {
-        y[row] = dadd(x[row], ddiv(dmul(omega, dsub(r[row], sum)), d[row]));
-    } else {
-        y[row] = dsub(r[row], sum);
-    }
-}
-
-// v = A w and block partials of (w.r, w.v, w.q): grid-stride over slices so
-// the number of partials is bounded by the grid (deterministic fixed order).
-__global__ void __launch_bounds__(kSellThreads)
-    k_sell_spmv_dots(const int64_t* __restrict__ soff, const int32_t* __restrict__ col,
-                     const double* __restrict__ val, int64_t nslices, int64_t nrows,
-                     const double* __restrict__ w, double* __restrict__ v,
-                     const double* __restrict__ r, const double* __restrict__ q,
-                     double* __restrict__ partials) {
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    double sa = 0.0, sb = 0.0, sg = 0.0;
-    for (int64_t slice = static_cast<int64_t>(blockIdx.x) * kSellWarps + warp; slice < nslices;
-         slice += static_cast<int64_t>(gridDim.x) * kSellWarps) {
-        const int64_t beg = soff[slice];
-        const int width = static_cast<int>((soff[slice + 1] - beg) >> 5);
-        const double sum = sell_row_sum(col + beg + lane, val + beg + lane, width, w);
-        const int64_t row = slice * 32 + lane;
-        if (row < nrows) {
-            v[row] = sum;
-            const double wi = w[row];
-            sa = dadd(sa, dmul(wi, r[row]));
-            sb = dadd(sb, dmul(wi, sum));
-            sg = dadd(sg, dmul(wi, q[row]));
-        }
-    }
-    for (int o = 16; o; o >>= 1) {
-        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
-        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
-        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
-    }
-    __shared__ double red[3][kSellWarps];
-    if (lane == 0) {
-        red[0][warp] = sa;
-        red[1][warp] = sb;
-        red[2][warp] = sg;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        double acc = 0.0;
-        for (int i = 0; i < kSellWarps; ++i) acc = dadd(acc, red[threadIdx.x][i]);
-        partials[blockIdx.x * 3 + threadIdx.x] = acc;
-    }
-}
-
 template <typename F>
 void cub_call(F&& f, cudaStream_t s) {
     size_t bytes = 0;
@@ -386,40 +258,6 @@ void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s) {
     PB_CHECK_LAUNCH();
 }
 
-void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s) {
-    S.nrows = nrows;
-    S.nslices = (nrows + 31) / 32;
-    S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
-    PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
-    if (S.nslices) {
-        k_sell_width<<<blocks_for(S.nslices * 32, 256), 256, 0, s>>>(M.rp.get(), rows, nrows, S.nslices,
-                                                                     S.slice_off.get());
-        PB_CHECK_LAUNCH();
-        cub_call([&](void* t, size_t& bytes) {
-            return cub::DeviceScan::ExclusiveSum(t, bytes, S.slice_off.get(), S.slice_off.get(),
-                                                 S.nslices + 1, s);
-        }, s);
-    }
-    S.padded_nnz = read_i64(S.slice_off.get() + S.nslices, s);
-    S.col.alloc(static_cast<size_t>(S.padded_nnz), s);
-    S.val.alloc(static_cast<size_t>(S.padded_nnz), s);
-    if (S.padded_nnz) {
-        PB_CUDA(cudaMemsetAsync(S.col.get(), 0xff, 4 * S.padded_nnz, s));
-        PB_CUDA(cudaMemsetAsync(S.val.get(), 0, 8 * S.padded_nnz, s));
-    }
-    if (rows) {
-        S.rows.alloc(static_cast<size_t>(nrows), s);
-        if (nrows) PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
-    } else {
-        S.rows.reset();
-    }
-    if (nrows) {
-        k_sell_fill<<<blocks_for(nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, nrows,
-                                                           S.slice_off.get(), S.col.get(), S.val.get());
-        PB_CHECK_LAUNCH();
-    }
-}
-
 void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s) {
     if (!M.n) return;
     DBuf<unsigned long long> zr(1, s);
@@ -479,45 +317,6 @@ void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_
         PB_NCCL(ncclRecv(b_halo + H.recv_off[i], c, ncclDouble, H.recv_peers[i], rt.nccl(), s));
     }
     PB_NCCL(ncclGroupEnd());
-}
-
-void sell_apply(const Sell& S, int op, const double* x, double* y, const double* r, const double* d,
-                double omega, cudaStream_t s) {
-    if (!S.nslices) return;
-    const int grid = blocks_for(S.nslices, kSellWarps);
-    const bool rows = !S.rows.empty();
-#define PB_SELL(OP)                                                                                  \
-    if (rows)                                                                                        \
-        k_sell<OP, true><<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), \
-                                                       S.rows.get(), S.nslices, S.nrows, x, y, r, d,  \
-                                                       omega);                                        \
-    else                                                                                             \
-        k_sell<OP, false><<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), \
-                                                        nullptr, S.nslices, S.nrows, x, y, r, d, omega);
-    switch (op) {
-        case kSpmv: PB_SELL(kSpmv) break;
-        case kJacobi: PB_SELL(kJacobi) break;
-        case kResid: PB_SELL(kResid) break;
-        default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
-    }
-#undef PB_SELL
-    PB_CHECK_LAUNCH();
-}
-
-int sell_dots_grid(const Sell& S) {
-    const int64_t want = (S.nslices + kSellWarps - 1) / kSellWarps;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
-}
-
-int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
-                   double* partials, int max_blocks, cudaStream_t s) {
-    if (!S.rows.empty()) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: row-list SELL not supported");
-    const int grid = sell_dots_grid(S);
-    if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
-    k_sell_spmv_dots<<<grid, kSellThreads, 0, s>>>(S.slice_off.get(), S.col.get(), S.val.get(), S.nslices,
-                                                    S.nrows, w, v, r, q, partials);
-    PB_CHECK_LAUNCH();
-    return grid;
 }
 
 }  // namespace pb
