@@ -45,6 +45,10 @@ inline bool env_flag(const char* name, bool dflt) {
     if (!v || !*v) return dflt;
     return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
 }
+inline int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
 
 inline int blocks_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;

@@ -55,7 +55,13 @@ struct DevMatrix {
 };
 
 struct Sell {
-    enum Format { kPlain = 0, kDict = 1 };
+    // PAT  : one byte per ROW naming its row pattern (the row's full sequence
+    //        of (column - row, value) entries; <= 255 distinct patterns); the
+    //        pattern table (16-byte records) and the per-pattern l1 diagonal
+    //        live in global memory (L1-resident).  Preferred when it applies.
+    // DICT : one byte per entry (<= 255 distinct (column - row, value)).
+    // PLAIN: int32 column + f64 value per entry.
+    enum Format { kPlain = 0, kDict = 1, kPat = 2 };
     int format = kPlain;
     int64_t nrows = 0, nslices = 0, padded_nnz = 0;
     DBuf<int64_t> slice_off;  // nslices+1; elements (PLAIN) or 32-bit code words (DICT), multiples of 32
@@ -63,9 +69,14 @@ struct Sell {
     DBuf<double> val;         // PLAIN: values
     DBuf<uint32_t> code;      // DICT: 4 one-byte codes per word, 0xFF = pad; [slice][word][lane]
     int words = 0;            // DICT: words per row (uniform)
-    DBuf<int32_t> dcol;       // DICT: column - row per code
-    DBuf<double> dval;        // DICT: value per code
+    DBuf<ulonglong2> dict;    // DICT: 256 records {value bits, column - row}; [255] = pad {0, 0}
     int ndict = 0;
+    DBuf<uint8_t> pid;        // PAT: pattern id per row (indexed by row id)
+    DBuf<ulonglong2> ptab;    // PAT: pattern records {value bits, column - row}
+    DBuf<int2> pmeta;         // PAT: {first record, length} per pattern
+    DBuf<double> pdiag;       // PAT: l1 diagonal per pattern (bitwise = l1_diagonal)
+    int npat = 0, maxlen = 0;
+    int64_t xlen = 0;         // gathered vector length (owned + halo slots)
     DBuf<int32_t> rows;       // row id of each SELL row; empty = identity
 };
 
@@ -96,9 +107,12 @@ void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s);
 // ---- sell.cu ----
 // SELL-32 copy of the rows listed in `rows` (nullptr = all rows); DICT
 // encoding when allowed and the rows have <= 255 distinct (col-row, value).
+// PAT is tried first (needs the level's l1 diagonal to verify the per-pattern
+// diagonal bitwise), then DICT, then PLAIN.
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s,
-                bool allow_dict = true);
-double sell_bytes(const Sell& S);  // stored matrix bytes (codes+dictionary or cols+values)
+                bool allow_dict = true, const double* l1 = nullptr);
+double sell_bytes(const Sell& S);               // stored matrix bytes of the format
+double sell_op_bytes(const Sell& S, int op);    // algorithmic bytes of one launch (op, or -1 = spmv+dots)
 // l1_diagonal_dist (cycle.cpp:55-75); throws singular_smoother.
 void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s);
 // x_halo[h] <- owner's x for every halo slot (pack, NCCL send/recv). On `s`.

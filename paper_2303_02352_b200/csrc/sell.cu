@@ -52,9 +52,7 @@ struct SellArgs {
     const double* val;
     const uint32_t* code;  // DICT
     int words;             // DICT: words per row
-    const int32_t* dcol;
-    const double* dval;
-    int ndict;
+    const ulonglong2* dict;  // DICT: 256 records {value bits, column offset}
     const int32_t* rows;
     int64_t nslices, nrows;
     const double* x;
@@ -101,11 +99,19 @@ __device__ __forceinline__ double row_sum_plain(const SellArgs& a, int64_t slice
     return sum;
 }
 
+// Dictionary entry e = {value bits, column offset} is one 16-byte record of
+// a 256-entry table in global memory (4 KB, L1-resident; slot 255 = pad =
+// {0, 0}); interior slices read the same record on every lane (broadcast).
+__device__ __forceinline__ void dict_entry(const ulonglong2* dict, uint32_t e, double& v, int& dc) {
+    const ulonglong2 r = __ldg(dict + e);
+    v = __longlong_as_double(static_cast<long long>(r.x));
+    dc = static_cast<int>(r.y);
+}
+
 // DICT row sum: the lane's words are code[(slice*W + w)*32 + lane]; 32-bit
 // index math throughout (the encoded matrix is < 2^31 words).
 template <int OP>
-__device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int lane, int row,
-                                               const int32_t* sdcol, const double* sdval) {
+__device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int lane, int row) {
     const int W = a.words;
     const uint32_t* cp = a.code + (slice * W) * 32 + lane;
     double sum = 0.0;
@@ -113,34 +119,24 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int
         const uint32_t wa = __ldg(cp + w0 * 32);
         const uint32_t wb = w0 + 1 < W ? __ldg(cp + (w0 + 1) * 32) : 0xFFFFFFFFu;
         uint32_t e[8];
-        double xv[8];
+        double av[8], xv[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) e[j] = ((j < 4 ? wa : wb) >> (8 * (j & 3))) & 0xFFu;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xv[j] = e[j] != 0xFFu ? xval<OP>(a, row + sdcol[e[j]]) : 0.0;
+        for (int j = 0; j < 8; ++j) {  // branch-free: slot 255 (pad) holds {0, 0}
+            int dc;
+            dict_entry(a.dict, e[j], av[j], dc);
+            xv[j] = e[j] != 0xFFu ? xval<OP>(a, row + dc) : 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (e[j] != 0xFFu) sum = dadd(sum, dmul(sdval[e[j]], xv[j]));
+            if (e[j] != 0xFFu) sum = dadd(sum, dmul(av[j], xv[j]));
     }
     return sum;
 }
 
-template <bool DICT>
-__device__ __forceinline__ void load_dict(const SellArgs& a, int32_t* sdcol, double* sdval) {
-    if (DICT) {
-        for (int i = threadIdx.x; i < a.ndict; i += blockDim.x) {
-            sdcol[i] = a.dcol[i];
-            sdval[i] = a.dval[i];
-        }
-        __syncthreads();
-    }
-}
-
 template <int OP, bool ROWS, bool DICT>
 __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
-    __shared__ int32_t sdcol[DICT ? kDictMax : 1];
-    __shared__ double sdval[DICT ? kDictMax : 1];
-    load_dict<DICT>(a, sdcol, sdval);
     const int lane = threadIdx.x & 31;
     const int slice = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (slice >= a.nslices) return;
@@ -157,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
         if (OP == kResid) ri = a.r[row];
         if (OP == kJacobi) xi = a.x[row];
     }
-    const double sum = DICT ? row_sum_dict<OP>(a, slice, lane, row, sdcol, sdval) : row_sum_plain<OP>(a, slice, lane);
+    const double sum = DICT ? row_sum_dict<OP>(a, slice, lane, row) : row_sum_plain<OP>(a, slice, lane);
     if (!valid) return;
     if (OP == kSpmv) {
         a.y[row] = sum;
@@ -172,10 +168,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
 // v = A w with block partials of (w.r, w.v, w.q); grid-stride over slices so
 // the partial count is bounded by the grid (fixed order -> deterministic).
 template <bool DICT>
-__global__ void __launch_bounds__(kThreads) k_sell_spmv_dots(SellArgs a) {
-    __shared__ int32_t sdcol[DICT ? kDictMax : 1];
-    __shared__ double sdval[DICT ? kDictMax : 1];
-    load_dict<DICT>(a, sdcol, sdval);
+__global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double sa = 0.0, sb = 0.0, sg = 0.0;
@@ -188,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) k_sell_spmv_dots(SellArgs a) {
             rr = a.r[row];
             qq = a.q[row];
         }
-        const double sum = DICT ? row_sum_dict<kSpmv>(a, slice, lane, row, sdcol, sdval)
+        const double sum = DICT ? row_sum_dict<kSpmv>(a, slice, lane, row)
                                 : row_sum_plain<kSpmv>(a, slice, lane);
         if (valid) {
             a.y[row] = sum;
@@ -214,6 +207,205 @@ __global__ void __launch_bounds__(kThreads) k_sell_spmv_dots(SellArgs a) {
         for (int i = 0; i < kWarps; ++i) acc = dadd(acc, red[threadIdx.x][i]);
         a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
     }
+}
+
+// ------------------------------------------------------------------ PAT ---
+//
+// One thread per row: pid -> {first record, length} -> records {value,
+// column - row} in CSR order.  Rows of a warp are consecutive, so on the
+// interior of a stencil operator all lanes read the same records (L1
+// broadcast) and run the same trip count; the row's l1 diagonal comes from
+// the pattern (no per-row d stream).
+
+#ifndef PB_PAT_BLOCKS
+#define PB_PAT_BLOCKS 4
+#endif
+constexpr int kPatBlocks = PB_PAT_BLOCKS;  // resident blocks/SM the register budget targets
+
+struct PatArgs {
+    const uint8_t* pid;
+    const ulonglong2* ptab;
+    const int2* pmeta;
+    const double* pdiag;
+    int maxlen;
+    int xlen;  // length of the gathered vector (owned + halo slots)
+    const int32_t* rows;
+    int64_t nrows;
+    const double* x;
+    double* y;
+    const double* r;
+    double omega;
+    const double* q;
+    double* partials;
+};
+
+// All record and gather loads are unconditional so they issue back to back
+// before the first multiply: the table is padded with 8 records past its end
+// and out-of-pattern gathers are clamped into x (their values are never
+// accumulated -- the add itself is predicated, keeping the CSR-order sum exact).
+// Empty asm statements that consume all eight values of a load batch: ptxas
+// must issue the whole batch before them, so a batch costs one memory
+// latency instead of eight (without them it interleaves each multiply with
+// the next load to save registers, serialising the gathers).
+__device__ __forceinline__ void batch_fence(const double (&v)[8]) {
+    asm volatile("" ::"d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "d"(v[4]), "d"(v[5]), "d"(v[6]), "d"(v[7]));
+}
+__device__ __forceinline__ void batch_fence(const ulonglong2 (&v)[8]) {
+    asm volatile("" ::"l"(v[0].y), "l"(v[1].y), "l"(v[2].y), "l"(v[3].y), "l"(v[4].y), "l"(v[5].y), "l"(v[6].y),
+                 "l"(v[7].y));
+}
+
+__device__ __forceinline__ double pat_row_sum(const PatArgs& a, int row, int2 m) {
+    double sum = 0.0;
+    for (int k0 = 0; k0 < a.maxlen; k0 += 8) {
+        ulonglong2 rec[8];
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rec[j] = __ldg(a.ptab + m.x + k0 + j);
+        batch_fence(rec);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = min(max(row + static_cast<int>(rec[j].y), 0), a.xlen - 1);
+            xv[j] = __ldg(a.x + c);
+        }
+        batch_fence(xv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < m.y) sum = dadd(sum, dmul(__longlong_as_double(static_cast<long long>(rec[j].x)), xv[j]));
+    }
+    return sum;
+}
+
+template <int OP, bool ROWS>
+__global__ void __launch_bounds__(kThreads, kPatBlocks) k_pat(PatArgs a) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= a.nrows) return;
+    const int row = ROWS ? a.rows[i] : i;
+    const int p = a.pid[row];
+    const int2 m = __ldg(a.pmeta + p);
+    double xi = 0.0, ri = 0.0, di = 1.0;
+    if (OP != kSpmv) ri = a.r[row];
+    if (OP == kJacobi) {
+        xi = a.x[row];
+        di = __ldg(a.pdiag + p);
+    }
+    const double sum = pat_row_sum(a, row, m);
+    if (OP == kSpmv)
+        a.y[row] = sum;
+    else if (OP == kResid)
+        a.y[row] = dsub(ri, sum);
+    else
+        a.y[row] = dadd(xi, ddiv(dmul(a.omega, dsub(ri, sum)), di));
+}
+
+// v = A w + block partials of (w.r, w.v, w.q), grid-stride (fixed order).
+__global__ void __launch_bounds__(kThreads) k_pat_spmv_dots(PatArgs a) {
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x; i < a.nrows;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int row = static_cast<int>(i);
+        const int p = a.pid[row];
+        const int2 m = __ldg(a.pmeta + p);
+        const double wi = a.x[row], rr = a.r[row], qq = a.q[row];
+        const double sum = pat_row_sum(a, row, m);
+        a.y[row] = sum;
+        sa = dadd(sa, dmul(wi, rr));
+        sb = dadd(sb, dmul(wi, sum));
+        sg = dadd(sg, dmul(wi, qq));
+    }
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    __shared__ double red[3][kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int k = 0; k < kWarps; ++k) acc = dadd(acc, red[threadIdx.x][k]);
+        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}
+
+// --- PAT building: hash every row's entry sequence, collect <= 255 patterns
+// (representative = smallest row), then assign + verify exactly on device.
+
+__device__ __forceinline__ ull mix64(ull h, ull v) {
+    h ^= v + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
+    h *= 0xBF58476D1CE4E5B9ULL;
+    return h ^ (h >> 31);
+}
+
+__device__ ull row_hash(const int64_t* rp, const int32_t* col, const double* val, int64_t row) {
+    ull h = mix64(0x243F6A8885A308D3ULL, static_cast<ull>(rp[row + 1] - rp[row]));
+    for (int64_t t = rp[row]; t < rp[row + 1]; ++t) {
+        h = mix64(h, static_cast<ull>(static_cast<int64_t>(col[t]) - row));
+        h = mix64(h, static_cast<ull>(__double_as_longlong(val[t])));
+    }
+    return h | 1ULL;  // 0 marks an empty slot
+}
+
+__global__ void k_pat_insert(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                             ull* keys, unsigned long long* rep, unsigned* count, int* overflow) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    if (*reinterpret_cast<volatile int*>(overflow)) return;
+    const int64_t row = rows ? rows[i] : i;
+    const ull h = row_hash(rp, col, val, row);
+    unsigned s = static_cast<unsigned>(h >> 20) & (kTableCap - 1);
+    for (int probe = 0; probe < kTableCap; ++probe, s = (s + 1) & (kTableCap - 1)) {
+        const ull old = atomicCAS(keys + s, 0ULL, h);
+        if (old == 0ULL || old == h) {
+            atomicMin(rep + s, static_cast<unsigned long long>(row));
+            if (old == 0ULL && atomicAdd(count, 1u) >= static_cast<unsigned>(kDictMax)) atomicExch(overflow, 1);
+            return;
+        }
+    }
+    atomicExch(overflow, 1);
+}
+
+__global__ void k_pat_assign(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                             const ull* __restrict__ keys, const int* __restrict__ slot_pid,
+                             const ulonglong2* __restrict__ ptab, const int2* __restrict__ pmeta,
+                             const double* __restrict__ pdiag, const double* __restrict__ l1, uint8_t* __restrict__ pid,
+                             int* bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int64_t row = rows ? rows[i] : i;
+    const ull h = row_hash(rp, col, val, row);
+    unsigned s = static_cast<unsigned>(h >> 20) & (kTableCap - 1);
+    int p = -1;
+    for (int probe = 0; probe < kTableCap; ++probe, s = (s + 1) & (kTableCap - 1)) {
+        if (keys[s] == h) {
+            p = slot_pid[s];
+            break;
+        }
+        if (keys[s] == 0ULL) break;
+    }
+    bool ok = p >= 0;
+    if (ok) {
+        const int2 m = pmeta[p];
+        ok = m.y == rp[row + 1] - rp[row];
+        for (int k = 0; ok && k < m.y; ++k) {
+            const int64_t t = rp[row] + k;
+            ok = ptab[m.x + k].x == static_cast<ull>(__double_as_longlong(val[t])) &&
+                 static_cast<int64_t>(static_cast<long long>(ptab[m.x + k].y)) == static_cast<int64_t>(col[t]) - row;
+        }
+        ok = ok && __double_as_longlong(pdiag[p]) == __double_as_longlong(l1[row]);
+    }
+    if (!ok) {
+        atomicExch(bad, 1);
+        return;
+    }
+    pid[row] = static_cast<uint8_t>(p);
 }
 
 // ------------------------------------------------------------- building ---
@@ -398,10 +590,14 @@ bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) 
     S.ndict = static_cast<int>(keys.size());
     S.words = static_cast<int>((hc[1] + 3) / 4);
     if (S.words == 0) S.words = 1;
-    S.dcol.alloc(keys.size(), s);
-    S.dval.alloc(keys.size(), s);
-    PB_CUDA(cudaMemcpyAsync(S.dcol.get(), dcol.data(), 4 * dcol.size(), cudaMemcpyHostToDevice, s));
-    PB_CUDA(cudaMemcpyAsync(S.dval.get(), dval.data(), 8 * dval.size(), cudaMemcpyHostToDevice, s));
+    std::vector<ulonglong2> rec(256, make_ulonglong2(0ULL, 0ULL));  // slot 255 = pad
+    for (size_t c = 0; c < keys.size(); ++c) {
+        ull vb;
+        std::memcpy(&vb, &dval[c], 8);
+        rec[c] = make_ulonglong2(vb, static_cast<ull>(static_cast<int64_t>(dcol[c])));
+    }
+    S.dict.alloc(256, s);
+    PB_CUDA(cudaMemcpyAsync(S.dict.get(), rec.data(), 16 * 256, cudaMemcpyHostToDevice, s));
     DBuf<int> dsc(kTableCap, s);
     PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
     S.padded_nnz = S.nslices * 32 * S.words;  // in words
@@ -419,6 +615,121 @@ bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) 
     return true;
 }
 
+__global__ void k_max_len(const int64_t* __restrict__ rp, const int32_t* __restrict__ rows, int64_t nrows,
+                          unsigned long long* mx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int64_t row = rows ? rows[i] : i;
+    atomicMax(mx, static_cast<unsigned long long>(rp[row + 1] - rp[row]));
+}
+
+void max_row_len(const DevMatrix& M, const int32_t* rows, int64_t nrows, int64_t* d_out, cudaStream_t s) {
+    if (!nrows) return;
+    k_max_len<<<blocks_for(nrows, 256), 256, 0, s>>>(M.rp.get(), rows, nrows,
+                                                     reinterpret_cast<unsigned long long*>(d_out));
+    PB_CHECK_LAUNCH();
+}
+
+bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
+    if (S.nrows == 0 || !l1) return false;
+    DBuf<ull> keys(kTableCap, s), rep(kTableCap, s);
+    DBuf<unsigned> cnt(1, s);
+    DBuf<int> flags(2, s);
+    keys.zero(s);
+    cnt.zero(s);
+    flags.zero(s);
+    PB_CUDA(cudaMemsetAsync(rep.get(), 0xff, 8 * kTableCap, s));
+    k_pat_insert<<<blocks_for(S.nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, S.nrows,
+                                                           keys.get(), rep.get(), cnt.get(), flags.get());
+    PB_CHECK_LAUNCH();
+    int over = 0;
+    std::vector<ull> hk(kTableCap), hr(kTableCap);
+    PB_CUDA(cudaMemcpyAsync(&over, flags.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), 8 * kTableCap, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaMemcpyAsync(hr.data(), rep.get(), 8 * kTableCap, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (over) return false;
+    std::vector<std::pair<ull, int>> pats;  // (representative row, slot)
+    for (int i = 0; i < kTableCap; ++i)
+        if (hk[i]) pats.push_back({hr[i], i});
+    if (pats.empty() || pats.size() > static_cast<size_t>(kDictMax)) return false;
+    std::sort(pats.begin(), pats.end());
+    std::vector<int> slot_pid(kTableCap, -1);
+    std::vector<ulonglong2> rec;
+    std::vector<int2> meta;
+    std::vector<double> pd;
+    int maxlen = 0;
+    for (size_t p = 0; p < pats.size(); ++p) {
+        const int64_t row = static_cast<int64_t>(pats[p].first);
+        slot_pid[pats[p].second] = static_cast<int>(p);
+        int64_t b_e[2];
+        PB_CUDA(cudaMemcpyAsync(b_e, M.rp.get() + row, 16, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaStreamSynchronize(s));
+        const int64_t len = b_e[1] - b_e[0];
+        std::vector<int32_t> c(static_cast<size_t>(len));
+        std::vector<double> v(static_cast<size_t>(len));
+        if (len) {
+            PB_CUDA(cudaMemcpyAsync(c.data(), M.col.get() + b_e[0], 4 * len, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaMemcpyAsync(v.data(), M.val.get() + b_e[0], 8 * len, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaStreamSynchronize(s));
+        }
+        meta.push_back(make_int2(static_cast<int>(rec.size()), static_cast<int>(len)));
+        // l1 diagonal of the pattern in CSR order (cycle.cpp:60-67): a_ii + sum |a_ij|
+        double acc = 0.0;
+        for (int64_t k = 0; k < len; ++k) {
+            const int64_t delta = static_cast<int64_t>(c[k]) - row;
+            ull vb;
+            std::memcpy(&vb, &v[k], 8);
+            rec.push_back(make_ulonglong2(vb, static_cast<ull>(delta)));
+            acc += delta == 0 ? v[k] : std::fabs(v[k]);
+        }
+        pd.push_back(acc);
+        maxlen = std::max<int>(maxlen, static_cast<int>(len));
+    }
+    S.npat = static_cast<int>(pats.size());
+    S.maxlen = maxlen;
+    rec.resize(rec.size() + static_cast<size_t>((maxlen + 7) / 8) * 8, make_ulonglong2(0ULL, 0ULL));  // load padding
+    S.ptab.alloc(std::max<size_t>(rec.size(), 1), s);
+    S.pmeta.alloc(meta.size(), s);
+    S.pdiag.alloc(pd.size(), s);
+    if (!rec.empty()) PB_CUDA(cudaMemcpyAsync(S.ptab.get(), rec.data(), 16 * rec.size(), cudaMemcpyHostToDevice, s));
+    PB_CUDA(cudaMemcpyAsync(S.pmeta.get(), meta.data(), 8 * meta.size(), cudaMemcpyHostToDevice, s));
+    PB_CUDA(cudaMemcpyAsync(S.pdiag.get(), pd.data(), 8 * pd.size(), cudaMemcpyHostToDevice, s));
+    DBuf<int> dsp(kTableCap, s);
+    PB_CUDA(cudaMemcpyAsync(dsp.get(), slot_pid.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
+    S.pid.alloc(static_cast<size_t>(M.n), s);
+    k_pat_assign<<<blocks_for(S.nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), M.val.get(), rows, S.nrows,
+                                                           keys.get(), dsp.get(), S.ptab.get(), S.pmeta.get(),
+                                                           S.pdiag.get(), l1, S.pid.get(), flags.get() + 1);
+    PB_CHECK_LAUNCH();
+    int bad = 0;
+    PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (bad) {  // hash collision or l1 mismatch: keep an exact format instead
+        S.pid.reset();
+        S.ptab.reset();
+        S.pmeta.reset();
+        S.pdiag.reset();
+        S.npat = 0;
+        return false;
+    }
+    S.format = Sell::kPat;
+    return true;
+}
+
+PatArgs pat_args_of(const Sell& S) {
+    PatArgs a{};
+    a.pid = S.pid.get();
+    a.ptab = S.ptab.get();
+    a.pmeta = S.pmeta.get();
+    a.pdiag = S.pdiag.get();
+    a.maxlen = S.maxlen;
+    a.xlen = static_cast<int>(S.xlen);
+    a.rows = S.rows.empty() ? nullptr : S.rows.get();
+    a.nrows = S.nrows;
+    return a;
+}
+
 SellArgs args_of(const Sell& S) {
     SellArgs a{};
     a.soff = S.slice_off.get();
@@ -426,9 +737,7 @@ SellArgs args_of(const Sell& S) {
     a.val = S.val.get();
     a.code = S.code.get();
     a.words = S.words;
-    a.dcol = S.dcol.get();
-    a.dval = S.dval.get();
-    a.ndict = S.ndict;
+    a.dict = S.dict.get();
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
     a.nslices = S.nslices;
     a.nrows = S.nrows;
@@ -455,17 +764,38 @@ void launch_op(const Sell& S, const SellArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict) {
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict,
+                const double* l1) {
     S = Sell();
     S.nrows = nrows;
     S.nslices = (nrows + 31) / 32;
+    S.xlen = M.n + M.halo.n_halo;
     if (S.nslices * 32 >= (int64_t(1) << 31))
         fail(PAIRAMG_INVALID_ARGUMENT, "sell: more than 2^31 rows per rank");
     if (rows) {
         S.rows.alloc(static_cast<size_t>(nrows), s);
         if (nrows) PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
     }
-    if (allow_dict && try_dict(M, rows, S, s)) return;
+    // Format choice (measured on B200): DICT keeps 32 registers
+    // and full occupancy, best for short rows; PAT removes the per-entry code
+    // stream, best once rows are long (27-point: 187 vs 198 us per L0 sweep).
+    if (allow_dict) {
+        int maxlen = 0;
+        {
+            DBuf<int64_t> mx(1, s);
+            mx.zero(s);
+            max_row_len(M, rows, nrows, mx.get(), s);
+            int64_t h = 0;
+            PB_CUDA(cudaMemcpyAsync(&h, mx.get(), 8, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaStreamSynchronize(s));
+            maxlen = static_cast<int>(h);
+        }
+        const int pref = env_int("PAIRAMG_SELL_PAT", -1);  // 1 force PAT, 0 never, -1 auto
+        const bool want_pat = pref == 1 || (pref == -1 && maxlen > 16);
+        if (want_pat && try_pattern(M, S.rows.empty() ? nullptr : S.rows.get(), S, l1, s)) return;
+        if (try_dict(M, rows, S, s)) return;
+        if (pref != 0 && !want_pat && try_pattern(M, S.rows.empty() ? nullptr : S.rows.get(), S, l1, s)) return;
+    }
     S.format = Sell::kPlain;
     S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
     PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
@@ -493,12 +823,46 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
 }
 
 double sell_bytes(const Sell& S) {
-    if (S.format == Sell::kDict) return 4.0 * S.padded_nnz + 12.0 * S.ndict;
+    if (S.format == Sell::kPat) return 1.0 * S.nrows + 16.0 * S.ptab.size() + 16.0 * S.npat;
+    if (S.format == Sell::kDict) return 4.0 * S.padded_nnz + 16.0 * S.ndict;
     return 12.0 * S.padded_nnz + 8.0 * (S.nslices + 1);
+}
+
+double sell_op_bytes(const Sell& S, int op) {
+    const double n = static_cast<double>(S.nrows), mat = sell_bytes(S);
+    switch (op) {
+        case kSpmv: return mat + 16.0 * n;                                             // x, y
+        case kJacobi: return mat + (S.format == Sell::kPat ? 24.0 : 32.0) * n;        // x, r, (d), y
+        case kResid: return mat + 24.0 * n;                                            // x, r, y
+        default: return mat + 32.0 * n;                                                // spmv+dots: w, r, q, v
+    }
 }
 
 void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
     if (!S.nslices) return;
+    if (S.format == Sell::kPat) {
+        PatArgs a = pat_args_of(S);
+        a.x = o.x;
+        a.y = o.y;
+        a.r = o.r;
+        a.omega = o.omega;
+        const int grid = blocks_for(S.nrows, kThreads);
+        const bool rows = a.rows != nullptr;
+#define PB_PAT(OP)                                             \
+    if (rows)                                                  \
+        k_pat<OP, true><<<grid, kThreads, 0, s>>>(a);          \
+    else                                                       \
+        k_pat<OP, false><<<grid, kThreads, 0, s>>>(a);
+        switch (o.op) {
+            case kSpmv: PB_PAT(kSpmv) break;
+            case kJacobi: PB_PAT(kJacobi) break;
+            case kResid: PB_PAT(kResid) break;
+            default: fail(PAIRAMG_INTERNAL, "sell_apply: fused operators need PAIRAMG_SELL_PAT=0");
+        }
+#undef PB_PAT
+        PB_CHECK_LAUNCH();
+        return;
+    }
     SellArgs a = args_of(S);
     a.x = o.x;
     a.y = o.y;
@@ -519,7 +883,7 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
 }
 
 int sell_dots_grid(const Sell& S) {
-    const int64_t want = (S.nslices + kWarps - 1) / kWarps;
+    const int64_t want = S.format == Sell::kPat ? (S.nrows + kThreads - 1) / kThreads : (S.nslices + kWarps - 1) / kWarps;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
 }
 
@@ -528,6 +892,17 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
     if (!S.rows.empty()) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: row-list SELL not supported");
     const int grid = sell_dots_grid(S);
     if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
+    if (S.format == Sell::kPat) {
+        PatArgs p = pat_args_of(S);
+        p.x = w;
+        p.y = v;
+        p.r = r;
+        p.q = q;
+        p.partials = partials;
+        k_pat_spmv_dots<<<grid, kThreads, 0, s>>>(p);
+        PB_CHECK_LAUNCH();
+        return grid;
+    }
     SellArgs a = args_of(S);
     a.x = w;
     a.y = v;

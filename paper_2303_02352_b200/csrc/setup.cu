@@ -774,10 +774,11 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         L.l1.alloc(static_cast<size_t>(n), s);
         l1_diagonal(L.A, L.l1.get(), s);
         if (L.A.halo.n_halo > 0) {
-            build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, env_flag("PAIRAMG_SELL_DICT", true));
+            build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, env_flag("PAIRAMG_SELL_DICT", true),
+                       L.l1.get());
             build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s, /*allow_dict=*/false);
         } else {
-            build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true));
+            build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true), L.l1.get());
         }
         L.x.alloc(static_cast<size_t>(next), s);
         L.xt.alloc(static_cast<size_t>(next), s);

@@ -82,8 +82,35 @@ __global__ void __launch_bounds__(kRedThreads)
              const FcgState* __restrict__ st, double* __restrict__ partials) {
     const double c = st->c, a = st->a;
     double rr = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+    // 16-byte vector accesses (all vectors are 256-byte aligned), scalar tail
+    const int64_t n2 = n >> 1;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    double2* d2 = reinterpret_cast<double2*>(d);
+    double2* q2 = reinterpret_cast<double2*>(q);
+    double2* u2 = reinterpret_cast<double2*>(u);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 wi = __ldcs(w2 + i), vi = __ldcs(v2 + i), di = d2[i], qi = q2[i], ui = u2[i], ri = r2[i];
+        double2 dn, qn, un, rn;
+        dn.x = dsub(wi.x, dmul(c, di.x));
+        dn.y = dsub(wi.y, dmul(c, di.y));
+        qn.x = dsub(vi.x, dmul(c, qi.x));
+        qn.y = dsub(vi.y, dmul(c, qi.y));
+        un.x = dadd(ui.x, dmul(a, dn.x));
+        un.y = dadd(ui.y, dmul(a, dn.y));
+        rn.x = dsub(ri.x, dmul(a, qn.x));
+        rn.y = dsub(ri.y, dmul(a, qn.y));
+        d2[i] = dn;
+        q2[i] = qn;
+        u2[i] = un;
+        r2[i] = rn;
+        rr = dadd(rr, dmul(rn.x, rn.x));
+        rr = dadd(rr, dmul(rn.y, rn.y));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = n - 1;
         const double dn = dsub(w[i], dmul(c, d[i]));
         const double qn = dsub(v[i], dmul(c, q[i]));
         d[i] = dn;
@@ -481,9 +508,13 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     const double mat = L0.A.halo.n_halo > 0 ? sell_bytes(L0.sell_int) + sell_bytes(L0.sell_bnd)
                                             : sell_bytes(L0.sell_all);
     const double nc1 = h.nl() > 1 ? static_cast<double>(h.levels[1]->A.n) : 0.0;
-    ktime[0].bytes_per_launch = mat + 32.0 * n0;              // x, r, d read; y written
-    ktime[1].bytes_per_launch = mat + 24.0 * n0;              // x, r read; y written
-    ktime[2].bytes_per_launch = mat + 32.0 * n0;              // w, r, q read; v written
+    auto op_bytes = [&](int op) {
+        return L0.A.halo.n_halo > 0 ? sell_op_bytes(L0.sell_int, op) + sell_op_bytes(L0.sell_bnd, op)
+                                    : sell_op_bytes(L0.sell_all, op);
+    };
+    ktime[0].bytes_per_launch = op_bytes(kJacobi);            // x, r, (d) read; y written
+    ktime[1].bytes_per_launch = op_bytes(kResid);             // x, r read; y written
+    ktime[2].bytes_per_launch = op_bytes(-1);                 // w, r, q read; v written
     ktime[3].bytes_per_launch = 80.0 * n0;                    // 6 vectors read, 4 written
     ktime[4].bytes_per_launch = mat + 24.0 * n0;              // r, d read; y written
     ktime[5].bytes_per_launch = mat + 44.0 * n0 + 8.0 * nc1;  // x, p, pcol, r, d read, e; y written

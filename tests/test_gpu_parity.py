@@ -83,6 +83,29 @@ def test_spmv_and_vcycle_bitexact(runtime, case):
     np.testing.assert_array_equal(bits(s.vcycle(r)), bits(orc.vcycle(r)))
 
 
+FORMATS = {  # solve-time storage of every level (csrc/sell.cu): all must be bit-identical
+    "pat": {"PAIRAMG_SELL_PAT": "1"},
+    "dict": {"PAIRAMG_SELL_PAT": "0"},
+    "plain": {"PAIRAMG_SELL_DICT": "0"},
+}
+
+
+@pytest.mark.parametrize("fmt", sorted(FORMATS))
+@pytest.mark.parametrize("case", [CASES[1], CASES[3], CASES[4]], ids=lambda c: f"{c[0]}pt-{c[1]}x{c[2]}x{c[3]}")
+def test_storage_formats_bitexact(runtime, case, fmt, monkeypatch):
+    for k, v in FORMATS[fmt].items():
+        monkeypatch.setenv(k, v)
+    orc, s = build_pair(runtime, *case)
+    rng = np.random.default_rng(11)
+    for k in range(orc.num_levels):
+        x = rng.standard_normal(orc.level_size(k)[0])
+        np.testing.assert_array_equal(bits(s.spmv(k, x)), bits(orc.spmv(k, x)), err_msg=f"{fmt} spmv level {k}")
+    r = rng.standard_normal(orc.n)
+    np.testing.assert_array_equal(bits(s.vcycle(r)), bits(orc.vcycle(r)), err_msg=f"{fmt} vcycle")
+    st = s.solve(np.ones(orc.n))
+    assert st.converged and abs(st.iterations - orc.solve()["iterations"]) <= 1
+
+
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}pt-{c[1]}x{c[2]}x{c[3]}")
 def test_fcg_solve(runtime, case):
     import paper_2303_02352_b200 as pb
