@@ -52,7 +52,26 @@ struct Hierarchy {
     std::vector<std::string> warnings;
     std::vector<DBuf<int64_t>> matchings;  // owned-block global mates per pairwise step
     int nl() const { return static_cast<int>(levels.size()); }
+
+    // Coarse-level replication (nranks > 1): levels >= rep_level are also held
+    // in full on every rank (rep[k - rep_level]); the V-cycle gathers the
+    // restricted right-hand side once (padded ncclAllGather) and runs those
+    // levels redundantly without halo traffic.  Row sums are the same, so the
+    // result is bit-identical to the distributed cycle.
+    int rep_level = -1;
+    std::vector<std::unique_ptr<Level>> rep;
+    std::vector<int64_t> rep_counts, rep_offsets;  // owned rows of level rep_level per rank
+    int64_t rep_max = 0;
+    DBuf<double> rep_send, rep_recv;                // rep_max, nranks * rep_max
 };
+
+// Replicate every level whose global size is <= max_rows (nranks > 1).
+void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows);
+// Padded allgather of per-rank segments (counts[r] elements each) into a
+// contiguous vector on `s` (graph-capturable).
+void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* sendbuf, double* recvbuf,
+                     int64_t maxcount, const std::vector<int64_t>& offsets, const std::vector<int64_t>& counts,
+                     double* d_out, cudaStream_t s);
 
 // Parallel Suitor on a weighted graph CSR already on the device (the
 // k_suitor / k_mate kernels of the setup; exposed for matching KATs).

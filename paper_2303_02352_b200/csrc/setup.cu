@@ -583,6 +583,158 @@ void extend_p(Runtime& rt, DevMatrix& A, const int32_t* pcol, const double* pval
 
 }  // namespace
 
+// ------------------------------------------------- coarse replication ---
+
+namespace {
+
+constexpr int kMaxRanks = 64;
+
+struct SegInfo {
+    int64_t off[kMaxRanks];
+    int64_t cnt[kMaxRanks];
+    int64_t max;
+    int p;
+};
+
+template <typename T>
+__global__ void k_unpad(const T* __restrict__ recv, SegInfo si, T* __restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= si.max * si.p) return;
+    const int r = static_cast<int>(t / si.max);
+    const int64_t i = t - r * si.max;
+    if (i < si.cnt[r]) out[si.off[r] + i] = recv[t];
+}
+
+__global__ void k_rowlen(const int64_t* __restrict__ rp, int64_t n, int64_t* __restrict__ len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) len[i] = rp[i + 1] - rp[i];
+    if (i == n) len[n] = 0;
+}
+
+__global__ void k_to_i32(const int64_t* __restrict__ a, int64_t n, int32_t* __restrict__ b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = static_cast<int32_t>(a[i]);
+}
+
+__global__ void k_shift_i32(const int32_t* __restrict__ a, int64_t n, int64_t shift, int32_t* __restrict__ b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = static_cast<int32_t>(a[i] + shift);
+}
+
+SegInfo seg_info(const std::vector<int64_t>& counts) {
+    if (counts.size() > static_cast<size_t>(kMaxRanks)) fail(PAIRAMG_INVALID_ARGUMENT, "more than 64 ranks");
+    SegInfo si{};
+    si.p = static_cast<int>(counts.size());
+    int64_t off = 0;
+    for (int r = 0; r < si.p; ++r) {
+        si.off[r] = off;
+        si.cnt[r] = counts[r];
+        off += counts[r];
+        si.max = std::max(si.max, counts[r]);
+    }
+    return si;
+}
+
+// Setup-time allgatherv of a device array (padded ncclAllGather + unpad).
+template <typename T>
+int64_t allgatherv(Runtime& rt, const T* d_local, int64_t count, DBuf<T>& out) {
+    cudaStream_t s = rt.stream();
+    const std::vector<int64_t> counts = rt.allgather_i64(count);
+    const SegInfo si = seg_info(counts);
+    const int64_t total = si.off[si.p - 1] + si.cnt[si.p - 1];
+    DBuf<T> send(static_cast<size_t>(std::max<int64_t>(si.max, 1)), s), recv(static_cast<size_t>(std::max<int64_t>(si.max * si.p, 1)), s);
+    if (count) PB_CUDA(cudaMemcpyAsync(send.get(), d_local, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
+    PB_NCCL(ncclAllGather(send.get(), recv.get(), sizeof(T) * si.max, ncclChar, rt.nccl(), s));
+    out.alloc(static_cast<size_t>(total), s);
+    if (si.max) k_unpad<T><<<blocks_for(si.max * si.p, 256), 256, 0, s>>>(recv.get(), si, out.get());
+    PB_CHECK_LAUNCH();
+    PB_CUDA(cudaStreamSynchronize(s));
+    return total;
+}
+
+}  // namespace
+
+void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* sendbuf, double* recvbuf,
+                     int64_t maxcount, const std::vector<int64_t>& offsets, const std::vector<int64_t>& counts,
+                     double* d_out, cudaStream_t s) {
+    SegInfo si = seg_info(counts);
+    (void)offsets;
+    if (count) PB_CUDA(cudaMemcpyAsync(sendbuf, d_local, 8 * count, cudaMemcpyDeviceToDevice, s));
+    PB_NCCL(ncclAllGather(sendbuf, recvbuf, static_cast<size_t>(maxcount), ncclDouble, rt.nccl(), s));
+    if (maxcount) k_unpad<double><<<blocks_for(maxcount * si.p, 256), 256, 0, s>>>(recvbuf, si, d_out);
+    PB_CHECK_LAUNCH();
+}
+
+void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows) {
+    h.rep_level = -1;
+    h.rep.clear();
+    if (rt.nranks() == 1) return;
+    cudaStream_t s = rt.stream();
+    int kr = -1;
+    for (int k = 1; k < h.nl(); ++k)
+        if (h.levels[k]->A.n_global <= max_rows) {
+            kr = k;
+            break;
+        }
+    if (kr < 0) return;
+    const bool dict = env_flag("PAIRAMG_SELL_DICT", true);
+    for (int k = kr; k < h.nl(); ++k) {
+        Level& D = *h.levels[k];
+        auto R = std::make_unique<Level>();
+        // global CSR (rows in rank order = global order)
+        DBuf<int64_t> len(static_cast<size_t>(D.A.n + 1), s), glen;
+        LAUNCH(k_rowlen, D.A.n + 1, D.A.rp.get(), D.A.n, len.get());
+        const int64_t ng = allgatherv(rt, len.get(), D.A.n, glen);
+        DBuf<int64_t> rp(static_cast<size_t>(ng + 1), s);
+        PB_CUDA(cudaMemsetAsync(rp.get() + ng, 0, 8, s));
+        if (ng) PB_CUDA(cudaMemcpyAsync(rp.get(), glen.get(), 8 * ng, cudaMemcpyDeviceToDevice, s));
+        cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, rp.get(), rp.get(), ng + 1, s); }, s);
+        DBuf<int64_t> gcol_local(static_cast<size_t>(std::max<int64_t>(D.A.nnz, 1)), s), gcol;
+        global_columns(D.A, gcol_local.get(), s);
+        DBuf<double> gval;
+        const int64_t nnz = allgatherv(rt, gcol_local.get(), D.A.nnz, gcol);
+        allgatherv(rt, D.A.val.get(), D.A.nnz, gval);
+        R->A.starts = {0, ng};
+        R->A.n = ng;
+        R->A.n_global = ng;
+        R->A.row_begin = 0;
+        R->A.nnz = nnz;
+        R->A.rp = std::move(rp);
+        R->A.col.alloc(static_cast<size_t>(nnz), s);
+        LAUNCH(k_to_i32, nnz, gcol.get(), nnz, R->A.col.get());
+        R->A.val = std::move(gval);
+        R->l1.alloc(static_cast<size_t>(ng), s);
+        l1_diagonal(R->A, R->l1.get(), s);
+        build_sell(R->A, nullptr, ng, R->sell_all, s, dict, R->l1.get());
+        R->x.alloc(static_cast<size_t>(ng), s);
+        R->xt.alloc(static_cast<size_t>(ng), s);
+        R->x.zero(s);
+        R->xt.zero(s);
+        R->rhs.alloc(static_cast<size_t>(ng), s);
+        R->res.alloc(static_cast<size_t>(ng), s);
+        if (k > kr) {  // replicated transfer from the (replicated) finer level
+            const Level& Df = *h.levels[k - 1];
+            DBuf<int32_t> pg(static_cast<size_t>(std::max<int64_t>(Df.A.n, 1)), s);
+            LAUNCH(k_shift_i32, Df.A.n, D.pcol.get(), Df.A.n, D.A.row_begin, pg.get());
+            const int64_t nf = allgatherv(rt, pg.get(), Df.A.n, R->pcol);
+            allgatherv(rt, D.pval.get(), Df.A.n, R->pval);
+            build_R(R->pcol.get(), R->pval.get(), nf, ng, R->rrp, R->rcol, R->rval, s);
+        }
+        h.rep.push_back(std::move(R));
+    }
+    h.rep_counts = rt.allgather_i64(h.levels[kr]->A.n);
+    h.rep_offsets.assign(h.rep_counts.size(), 0);
+    h.rep_max = 0;
+    for (size_t r = 0; r < h.rep_counts.size(); ++r) {
+        h.rep_offsets[r] = r ? h.rep_offsets[r - 1] + h.rep_counts[r - 1] : 0;
+        h.rep_max = std::max(h.rep_max, h.rep_counts[r]);
+    }
+    h.rep_send.alloc(static_cast<size_t>(std::max<int64_t>(h.rep_max, 1)), s);
+    h.rep_recv.alloc(static_cast<size_t>(std::max<int64_t>(h.rep_max * rt.nranks(), 1)), s);
+    h.rep_level = kr;
+    PB_CUDA(cudaStreamSynchronize(s));
+}
+
 void suitor_match_device(const int64_t* rp, const int32_t* col, const double* w, int64_t n, int64_t* mate,
                          cudaStream_t s) {
     DBuf<ull> slot(static_cast<size_t>(2 * n), s);
@@ -792,6 +944,11 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
     double opc = 0.0;
     for (int64_t z : h.level_nnz) opc += static_cast<double>(z) / static_cast<double>(h.level_nnz[0]);
     h.opc = opc;
+    {
+        const auto tc = Clock::now();
+        replicate_coarse_levels(rt, h, env_int("PAIRAMG_REPLICATE_ROWS", 300000));
+        h.stats.t_spmm_comm += since(tc);
+    }
     PB_CUDA(cudaStreamSynchronize(s));
     h.stats.t_total = since(t_start);
 }

@@ -318,8 +318,13 @@ void Solver::collect_times() {
         }
 }
 
-void Solver::apply(int k, const SellOpArgs& o, int kc) {
-    Level& L = *h.levels[k];
+Level& Solver::lvl(int k) {
+    return (h.rep_level >= 0 && k >= h.rep_level) ? *h.rep[static_cast<size_t>(k - h.rep_level)] : *h.levels[k];
+}
+
+void Solver::apply(int k, const SellOpArgs& o, int kc) { apply_on(lvl(k), o, kc); }
+
+void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
     begin_time(kc);
     if (L.A.halo.has_traffic()) {
         if (o.op == kJacobiZero || o.op == kJacobiProl)
@@ -354,11 +359,11 @@ static SellOpArgs jacobi_args(int op, const double* x, double* y, const double* 
     return o;
 }
 
-bool Solver::fusable(int k) const { return fuse && !h.levels[k]->A.halo.has_traffic(); }
+bool Solver::fusable(int k) { return fuse && !lvl(k).A.halo.has_traffic(); }
 
 void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
                     bool l0) {
-    Level& L = *h.levels[k];
+    Level& L = lvl(k);
     const int64_t n = L.A.n;
     if (nu == 0) {
         if (zero_start && n) PB_CUDA(cudaMemsetAsync(xc, 0, 8 * n, s_));
@@ -383,7 +388,7 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
 }
 
 void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc) {
-    Level& L = *h.levels[k];
+    Level& L = lvl(k);
     double* xc = L.x.get();
     double* xo = L.xt.get();
     const bool l0 = k == 0;
@@ -401,25 +406,35 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         o.r = rhs;
         apply(k, o, l0 ? 1 : -1);
     }
-    Level& C = *h.levels[k + 1];
-    if (C.A.n) k_restrict<<<blocks_for(C.A.n, 256), 256, 0, s_>>>(C.rrp.get(), C.rcol.get(), C.rval.get(),
-                                                                    L.res.get(), C.rhs.get(), C.A.n);
+    // T holds the transfer operators into level k+1 (the distributed owned
+    // blocks when level k+1 is the first replicated level), C its vectors.
+    const bool gather = h.rep_level >= 0 && k + 1 == h.rep_level;
+    Level& T = gather ? *h.levels[k + 1] : lvl(k + 1);
+    Level& C = lvl(k + 1);
+    if (T.A.n) k_restrict<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rval.get(),
+                                                                    L.res.get(), T.rhs.get(), T.A.n);
     PB_CHECK_LAUNCH();
     launches_ += 1;
+    if (gather) {  // one padded allgather of the restricted rhs, then redundant coarse levels
+        gather_segments(rt, T.rhs.get(), T.A.n, h.rep_send.get(), h.rep_recv.get(), h.rep_max, h.rep_offsets,
+                        h.rep_counts, C.rhs.get(), s_);
+        launches_ += 2;
+    }
     double* e = nullptr;
     vcycle_enqueue(k + 1, C.rhs.get(), e, cc);
+    if (gather) e += h.rep_offsets[static_cast<size_t>(rt.rank())];
     int post = cc.post_sweeps;
     if (post >= 1 && fusable(k)) {
         // prolongate_add fused into the first post-sweep: x_j + p_j*e_agg(j) on the fly
         SellOpArgs o = jacobi_args(kJacobiProl, xc, xo, rhs, L.l1.get(), cc.relax_weight);
-        o.pcol = C.pcol.get();
-        o.pval = C.pval.get();
+        o.pcol = T.pcol.get();
+        o.pval = T.pval.get();
         o.e = e;
         apply(k, o, l0 ? 5 : -1);
         std::swap(xc, xo);
         --post;
     } else {
-        if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(C.pcol.get(), C.pval.get(), e, xc, L.A.n);
+        if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pval.get(), e, xc, L.A.n);
         PB_CHECK_LAUNCH();
         launches_ += 1;
     }
@@ -628,7 +643,7 @@ void Solver::spmv(int level, const double* d_x, double* d_y) {
     o.op = kSpmv;
     o.x = L.xt.get();
     o.y = L.res.get();
-    apply(level, o, -1);
+    apply_on(L, o, -1);  // the distributed level (spmv_dist semantics), never the replicated copy
     timing = t;
     if (L.A.n) PB_CUDA(cudaMemcpyAsync(d_y, L.res.get(), 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
     PB_CUDA(cudaStreamSynchronize(s_));

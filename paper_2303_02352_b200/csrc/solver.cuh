@@ -56,7 +56,9 @@ private:
     void smooth(int k, bool zero_start, int nu, const double* rhs, double*& xcur, double*& xoth, double omega,
                 bool time_l0);
     void apply(int k, const SellOpArgs& o, int kclass);
-    bool fusable(int k) const;
+    void apply_on(Level& L, const SellOpArgs& o, int kclass);
+    bool fusable(int k);
+    Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
     void reduce_dots_enqueue();

@@ -20,7 +20,7 @@ def test_distributed_parity(world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
            os.path.join(ROOT, "tests", "mp_parity.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(["timeout", "-k", "10", "300", *cmd], capture_output=True, text=True, timeout=400, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("MP_PARITY_OK") == 5, out[-4000:]
