@@ -77,7 +77,8 @@ struct Sell {
     DBuf<double> pdiag;       // PAT: l1 diagonal per pattern (bitwise = l1_diagonal)
     int npat = 0, maxlen = 0;
     int64_t xlen = 0;         // gathered vector length (owned + halo slots)
-    DBuf<int32_t> rows;       // row id of each SELL row; empty = identity
+    DBuf<int32_t> rows;       // row id of each SELL row; empty = row0 + index
+    int64_t row0 = 0;
 };
 
 // Operators of the SELL kernels (sell.cu)

@@ -10,8 +10,13 @@ Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
     if (nranks < 1 || rank < 0 || rank >= nranks)
         fail(PAIRAMG_INVALID_ARGUMENT, "runtime: need 0 <= rank < nranks");
     PB_CUDA(cudaSetDevice(device));
-    PB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    PB_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+    // The halo stream gets the highest priority: its pack + NCCL blocks are
+    // dispatched ahead of the remaining interior-row blocks, so the exchange
+    // overlaps the interior pass instead of queueing behind it.
+    int prio_lo = 0, prio_hi = 0;
+    PB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    PB_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_lo));
+    PB_CUDA(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, prio_hi));
     // Keep freed stream-ordered allocations cached in the pool.
     cudaMemPool_t pool;
     PB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

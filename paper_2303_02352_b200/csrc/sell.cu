@@ -54,6 +54,7 @@ struct SellArgs {
     int words;             // DICT: words per row
     const ulonglong2* dict;  // DICT: 256 records {value bits, column offset}
     const int32_t* rows;
+    int row0;  // first row when the row set is a contiguous range (rows == nullptr)
     int64_t nslices, nrows;
     const double* x;
     double* y;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
     if (slice >= a.nslices) return;
     const int sr = slice * 32 + lane;
     const bool valid = sr < a.nrows;
-    const int row = !valid ? 0 : (ROWS ? a.rows[sr] : sr);
+    const int row = !valid ? 0 : (ROWS ? a.rows[sr] : a.row0 + sr);
     // own-row operands first: their latency overlaps the gather chain
     double xi = 0.0, ri = 0.0, di = 1.0;
     if (valid) {
@@ -167,14 +168,15 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
 
 // v = A w with block partials of (w.r, w.v, w.q); grid-stride over slices so
 // the partial count is bounded by the grid (fixed order -> deterministic).
-template <bool DICT>
+template <bool DICT, bool ROWS>
 __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double sa = 0.0, sb = 0.0, sg = 0.0;
     for (int slice = blockIdx.x * kWarps + warp; slice < a.nslices; slice += gridDim.x * kWarps) {
-        const int row = slice * 32 + lane;
-        const bool valid = row < a.nrows;
+        const int sr = slice * 32 + lane;
+        const bool valid = sr < a.nrows;
+        const int row = !valid ? 0 : (ROWS ? a.rows[sr] : a.row0 + sr);
         double wi = 0.0, rr = 0.0, qq = 0.0;
         if (valid) {
             wi = a.x[row];
@@ -230,6 +232,7 @@ struct PatArgs {
     int maxlen;
     int xlen;  // length of the gathered vector (owned + halo slots)
     const int32_t* rows;
+    int row0;  // first row when the row set is a contiguous range (rows == nullptr)
     int64_t nrows;
     const double* x;
     double* y;
@@ -280,7 +283,7 @@ template <int OP, bool ROWS>
 __global__ void __launch_bounds__(kThreads, kPatBlocks) k_pat(PatArgs a) {
     const int i = blockIdx.x * kThreads + threadIdx.x;
     if (i >= a.nrows) return;
-    const int row = ROWS ? a.rows[i] : i;
+    const int row = ROWS ? a.rows[i] : a.row0 + i;
     const int p = a.pid[row];
     const int2 m = __ldg(a.pmeta + p);
     double xi = 0.0, ri = 0.0, di = 1.0;
@@ -299,11 +302,12 @@ __global__ void __launch_bounds__(kThreads, kPatBlocks) k_pat(PatArgs a) {
 }
 
 // v = A w + block partials of (w.r, w.v, w.q), grid-stride (fixed order).
+template <bool ROWS>
 __global__ void __launch_bounds__(kThreads) k_pat_spmv_dots(PatArgs a) {
     double sa = 0.0, sb = 0.0, sg = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x; i < a.nrows;
          i += static_cast<int64_t>(gridDim.x) * kThreads) {
-        const int row = static_cast<int>(i);
+        const int row = ROWS ? a.rows[i] : a.row0 + static_cast<int>(i);
         const int p = a.pid[row];
         const int2 m = __ldg(a.pmeta + p);
         const double wi = a.x[row], rr = a.r[row], qq = a.q[row];
@@ -726,6 +730,7 @@ PatArgs pat_args_of(const Sell& S) {
     a.maxlen = S.maxlen;
     a.xlen = static_cast<int>(S.xlen);
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
+    a.row0 = static_cast<int>(S.row0);
     a.nrows = S.nrows;
     return a;
 }
@@ -739,6 +744,7 @@ SellArgs args_of(const Sell& S) {
     a.words = S.words;
     a.dict = S.dict.get();
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
+    a.row0 = static_cast<int>(S.row0);
     a.nslices = S.nslices;
     a.nrows = S.nrows;
     return a;
@@ -772,9 +778,19 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
     S.xlen = M.n + M.halo.n_halo;
     if (S.nslices * 32 >= (int64_t(1) << 31))
         fail(PAIRAMG_INVALID_ARGUMENT, "sell: more than 2^31 rows per rank");
-    if (rows) {
-        S.rows.alloc(static_cast<size_t>(nrows), s);
-        if (nrows) PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
+    if (rows && nrows) {
+        // An ascending row set that is one contiguous range (the interior of a
+        // slab partition) is addressed by offset: no row-id load per row.
+        int32_t ends[2] = {0, 0};
+        PB_CUDA(cudaMemcpyAsync(&ends[0], rows, 4, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaMemcpyAsync(&ends[1], rows + nrows - 1, 4, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaStreamSynchronize(s));
+        if (static_cast<int64_t>(ends[1]) - ends[0] == nrows - 1) {
+            S.row0 = ends[0];
+        } else {
+            S.rows.alloc(static_cast<size_t>(nrows), s);
+            PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
+        }
     }
     // Format choice (measured on B200): DICT keeps 32 registers
     // and full occupancy, best for short rows; PAT removes the per-entry code
@@ -792,9 +808,9 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
         }
         const int pref = env_int("PAIRAMG_SELL_PAT", -1);  // 1 force PAT, 0 never, -1 auto
         const bool want_pat = pref == 1 || (pref == -1 && maxlen > 16);
-        if (want_pat && try_pattern(M, S.rows.empty() ? nullptr : S.rows.get(), S, l1, s)) return;
+        if (want_pat && try_pattern(M, rows, S, l1, s)) return;
         if (try_dict(M, rows, S, s)) return;
-        if (pref != 0 && !want_pat && try_pattern(M, S.rows.empty() ? nullptr : S.rows.get(), S, l1, s)) return;
+        if (pref != 0 && !want_pat && try_pattern(M, rows, S, l1, s)) return;
     }
     S.format = Sell::kPlain;
     S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
@@ -889,9 +905,10 @@ int sell_dots_grid(const Sell& S) {
 
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q, double* partials,
                    int max_blocks, cudaStream_t s) {
-    if (!S.rows.empty()) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: row-list SELL not supported");
+    if (!S.nrows) return 0;
     const int grid = sell_dots_grid(S);
     if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
+    const bool rows = !S.rows.empty();
     if (S.format == Sell::kPat) {
         PatArgs p = pat_args_of(S);
         p.x = w;
@@ -899,7 +916,10 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
         p.r = r;
         p.q = q;
         p.partials = partials;
-        k_pat_spmv_dots<<<grid, kThreads, 0, s>>>(p);
+        if (rows)
+            k_pat_spmv_dots<true><<<grid, kThreads, 0, s>>>(p);
+        else
+            k_pat_spmv_dots<false><<<grid, kThreads, 0, s>>>(p);
         PB_CHECK_LAUNCH();
         return grid;
     }
@@ -909,10 +929,17 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
     a.r = r;
     a.q = q;
     a.partials = partials;
-    if (S.format == Sell::kDict)
-        k_sell_spmv_dots<true><<<grid, kThreads, 0, s>>>(a);
-    else
-        k_sell_spmv_dots<false><<<grid, kThreads, 0, s>>>(a);
+    if (S.format == Sell::kDict) {
+        if (rows)
+            k_sell_spmv_dots<true, true><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_sell_spmv_dots<true, false><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        if (rows)
+            k_sell_spmv_dots<false, true><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_sell_spmv_dots<false, false><<<grid, kThreads, 0, s>>>(a);
+    }
     PB_CHECK_LAUNCH();
     return grid;
 }

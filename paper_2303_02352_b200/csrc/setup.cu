@@ -946,7 +946,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
     h.opc = opc;
     {
         const auto tc = Clock::now();
-        replicate_coarse_levels(rt, h, env_int("PAIRAMG_REPLICATE_ROWS", 300000));
+        replicate_coarse_levels(rt, h, env_int("PAIRAMG_REPLICATE_ROWS", 2500000));
         h.stats.t_spmm_comm += since(tc);
     }
     PB_CUDA(cudaStreamSynchronize(s));

@@ -42,38 +42,6 @@ __global__ void k_prolong(const int32_t* __restrict__ pcol, const double* __rest
     if (i < n) x[i] = dadd(x[i], dmul(pval[i], e[pcol[i]]));
 }
 
-// Block partials of (w.r, w.v, w.q) for the halo path (grid-stride, fixed grid).
-__global__ void __launch_bounds__(kRedThreads)
-    k_dots3(const double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ r,
-            const double* __restrict__ q, int64_t n, double* __restrict__ partials) {
-    double sa = 0.0, sb = 0.0, sg = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double wi = w[i];
-        sa = dadd(sa, dmul(wi, r[i]));
-        sb = dadd(sb, dmul(wi, v[i]));
-        sg = dadd(sg, dmul(wi, q[i]));
-    }
-    __shared__ double red[3][kRedThreads / 32];
-    for (int o = 16; o; o >>= 1) {
-        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
-        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
-        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        red[0][warp] = sa;
-        red[1][warp] = sb;
-        red[2][warp] = sg;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        double acc = 0.0;
-        for (int k = 0; k < kRedThreads / 32; ++k) acc = dadd(acc, red[threadIdx.x][k]);
-        partials[blockIdx.x * 3 + threadIdx.x] = acc;
-    }
-}
-
 // FCG vector updates (Alg. 1 lines 16-19), op order shared with the oracle:
 //   d = w - c d ; q = v - c q ; u = u + a d ; r = r - a q ;  plus |r|^2 partials.
 __global__ void __launch_bounds__(kRedThreads)
@@ -263,7 +231,7 @@ void Solver::ensure_vectors() {
     d_.alloc(static_cast<size_t>(n_), s_);
     q_.alloc(static_cast<size_t>(n_), s_);
     max_blocks_ = kSmCount * 8;
-    partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
+    partials_.alloc(static_cast<size_t>(2 * 3 * max_blocks_), s_);  // interior + boundary launches
     local_.alloc(8, s_);
     gathered_.alloc(static_cast<size_t>(4 * rt.nranks()), s_);
     state_.alloc(1, s_);
@@ -446,7 +414,7 @@ void Solver::reduce_dots_enqueue() {
     const int p = rt.nranks();
     // partial count G is encoded by the producer; it is fixed for the level
     Level& L0 = *h.levels[0];
-    const int G = L0.A.halo.has_traffic() ? red_grid(n_) : sell_dots_grid(L0.sell_all);
+    const int G = dots_grid_;  // partial triples written by the SpMV+dots launches
     k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), G, 3, local_.get());
     PB_CHECK_LAUNCH();
     const double* g = local_.get();
@@ -484,21 +452,27 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     }
     w_out_ = w;
     // v = A w and the dot triple (Alg. 1 lines 10-13)
-    if (!L0.A.halo.has_traffic()) {
-        begin_time(2);
-        sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
-        end_time(2);
-        launches_ += 1;
-    } else {
-        SellOpArgs o;
-        o.op = kSpmv;
-        o.x = w;
-        o.y = v_.get();
-        apply(0, o, 2);
-        k_dots3<<<red_grid(n_), kRedThreads, 0, s_>>>(w, v_.get(), r_.get(), q_.get(), n_, partials_.get());
-        PB_CHECK_LAUNCH();
+    begin_time(2);
+    if (L0.A.halo.has_traffic()) {  // halo of w in flight while the interior rows run
+        PB_CUDA(cudaEventRecord(ev_fork_, s_));
+        PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
+        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, rt.comm_stream());
+        PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }
+    if (L0.A.halo.n_halo > 0) {
+        const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
+        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        const int g2 = sell_spmv_dots(L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get() + 3 * g1,
+                                      max_blocks_, s_);
+        dots_grid_ = g1 + g2;
+        launches_ += 2;
+    } else {
+        if (L0.A.halo.has_traffic()) PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
+        launches_ += 1;
+    }
+    end_time(2);
     reduce_dots_enqueue();
     begin_time(3);
     k_update<<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(), n_,

@@ -77,6 +77,7 @@ private:
     DBuf<FcgState> state_;
     FcgState* h_state_ = nullptr;  // pinned
     int max_blocks_ = 0;
+    int dots_grid_ = 0;  // partial triples of the last SpMV+dots enqueue
     double* w_out_ = nullptr;      // buffer holding w_i after the captured V-cycle
     cudaGraphExec_t graph_ = nullptr;
     CycleConfig graph_cc_{};
