@@ -339,64 +339,71 @@ __device__ void galerkin_team(const GalerkinArgs& a, int64_t c, int lane, int te
         if (!NUMERIC && lane == 0) a.cnt[c] = -1;
         return;
     }
-    if (!NUMERIC) {
-        int distinct = 0;
-        for (int q = lane; q < m; q += team) {
-            const int64_t g = sgc[q];
-            bool first = true;
-            for (int q2 = 0; q2 < q; ++q2)
-                if (sgc[q2] == g) {
-                    first = false;
-                    break;
+    // Sort keys (coarse column << 16 | encounter position) with a team-wide
+    // bitonic network: equal columns become contiguous segments whose
+    // elements stay in encounter order (t ascending, then CSR order).
+    uint64_t* key = reinterpret_cast<uint64_t*>(sgc);  // in place over the gathered columns
+    int p2 = 2;
+    while (p2 < m) p2 <<= 1;
+    for (int q = lane; q < p2; q += team)
+        key[q] = q < m ? (static_cast<uint64_t>(sgc[q]) << 16) | static_cast<uint64_t>(q) : ~0ULL;
+    sync();
+    for (int k = 2; k <= p2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < p2; i += team) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t x = key[i], y = key[ixj];
+                    if ((x > y) == ((i & k) == 0)) {
+                        key[i] = y;
+                        key[ixj] = x;
+                    }
                 }
-            distinct += first ? 1 : 0;
-        }
-        // team reduce
-        for (int o = 16; o; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
-        if (!block_sync) {
-            if (lane == 0) a.cnt[c] = distinct;
-        } else {
-            __shared__ int red[32];
-            if ((lane & 31) == 0) red[lane >> 5] = distinct;
-            __syncthreads();
-            if (lane == 0) {
-                int tot = 0;
-                for (int k = 0; k < (team + 31) / 32; ++k) tot += red[k];
-                a.cnt[c] = tot;
             }
-            __syncthreads();
+            sync();
         }
+    // segment starts -> distinct count and output rank (team exclusive scan
+    // over contiguous per-thread chunks)
+    const int chunk = (p2 + team - 1) / team;
+    const int c0 = lane * chunk, c1 = min(c0 + chunk, m);
+    int mine = 0;
+    for (int i = c0; i < c1; ++i) mine += (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16)) ? 1 : 0;
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((lane & 31) >= o) incl += v;
+    }
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    int base = incl - mine;
+    if (block_sync) {
+        __shared__ int wsum[32];
+        if ((lane & 31) == 31) wsum[lane >> 5] = incl;
+        __syncthreads();
+        int before = 0;
+        total = 0;
+        for (int w = 0; w < (team + 31) / 32; ++w) {
+            if (w < (lane >> 5)) before += wsum[w];
+            total += wsum[w];
+        }
+        base += before;
+        __syncthreads();
+    }
+    if (!NUMERIC) {
+        if (lane == 0) a.cnt[c] = total;
         return;
     }
     const int64_t ob = a.orp[c];
-    for (int q = lane; q < m; q += team) {
-        const int64_t g = sgc[q];
-        bool first = true;
-        for (int q2 = 0; q2 < q; ++q2)
-            if (sgc[q2] == g) {
-                first = false;
-                break;
-            }
-        if (!first) continue;
-        // rank among distinct columns = number of distinct columns < g
-        int rank = 0;
-        for (int q2 = 0; q2 < m; ++q2) {
-            const int64_t g2 = sgc[q2];
-            if (g2 >= g) continue;
-            bool f2 = true;
-            for (int q3 = 0; q3 < q2; ++q3)
-                if (sgc[q3] == g2) {
-                    f2 = false;
-                    break;
-                }
-            rank += f2 ? 1 : 0;
-        }
-        // reference-order accumulation
+    int rank = base;
+    for (int i = c0; i < c1; ++i) {
+        const uint64_t g = key[i] >> 16;
+        if (!(i == 0 || g != (key[i - 1] >> 16))) continue;
+        // reference-order accumulation over the segment
         bool acc_set = false, ct_set = false;
         double acc = 0.0, ct = 0.0, rt = 0.0;
         int cur_t = -1;
-        for (int q2 = 0; q2 < m; ++q2) {
-            const int t2 = st[q2];
+        for (int j = i; j < m && (key[j] >> 16) == g; ++j) {
+            const int q = static_cast<int>(key[j] & 0xFFFFu);
+            const int t2 = st[q];
             if (t2 != cur_t) {
                 if (ct_set) {
                     const double contrib = dmul(rt, ct);
@@ -405,19 +412,18 @@ __device__ void galerkin_team(const GalerkinArgs& a, int64_t c, int lane, int te
                 }
                 ct_set = false;
                 cur_t = t2;
-                rt = sr[q2];
+                rt = sr[q];
             }
-            if (sgc[q2] == g) {
-                ct = ct_set ? dadd(ct, sv[q2]) : sv[q2];
-                ct_set = true;
-            }
+            ct = ct_set ? dadd(ct, sv[q]) : sv[q];
+            ct_set = true;
         }
         if (ct_set) {
             const double contrib = dmul(rt, ct);
             acc = acc_set ? dadd(acc, contrib) : contrib;
         }
-        a.ocol[ob + rank] = g;
+        a.ocol[ob + rank] = static_cast<int64_t>(g);
         a.oval[ob + rank] = acc;
+        ++rank;
     }
 }
 
