@@ -42,10 +42,13 @@ def launches(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for r in rows[hi + 1:]:
         if len(r) <= vi:
+            continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
             continue
         try:
             v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)  # -> us
