@@ -70,6 +70,7 @@ struct Sell {
     DBuf<uint32_t> code;      // DICT: 4 one-byte codes per word, 0xFF = pad; [slice][word][lane]
     int words = 0;            // DICT: words per row (uniform)
     DBuf<ulonglong2> dict;    // DICT: 256 records {value bits, column - row}; [255] = pad {0, 0}
+    std::vector<ulonglong2> hdict;  // DICT: host copy, passed to the kernels as a __grid_constant__ parameter
     int ndict = 0;
     DBuf<uint8_t> pid;        // PAT: pattern id per row (indexed by row id)
     DBuf<ulonglong2> ptab;    // PAT: pattern records {value bits, column - row}

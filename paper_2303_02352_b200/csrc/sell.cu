@@ -100,11 +100,22 @@ __device__ __forceinline__ double row_sum_plain(const SellArgs& a, int64_t slice
     return sum;
 }
 
-// Dictionary entry e = {value bits, column offset} is one 16-byte record of
-// a 256-entry table in global memory (4 KB, L1-resident; slot 255 = pad =
-// {0, 0}); interior slices read the same record on every lane (broadcast).
-__device__ __forceinline__ void dict_entry(const ulonglong2* dict, uint32_t e, double& v, int& dc) {
-    const ulonglong2 r = __ldg(dict + e);
+// The dictionary (256 records {value bits, column offset}; slot 255 = pad =
+// {0, 0}) travels as a 4 KB __grid_constant__ kernel parameter: lookups are
+// indexed constant-bank loads (LDC), served by the constant cache --
+// broadcast when a warp's lanes share a code (interior slices) -- instead
+// of competing with the gathers for L1TEX bandwidth.
+template <bool DICT>
+struct DictParam {
+    ulonglong2 e[256];
+};
+template <>
+struct DictParam<false> {
+    int unused;
+};
+
+__device__ __forceinline__ void dict_entry(const DictParam<true>& dp, uint32_t e, double& v, int& dc) {
+    const ulonglong2 r = dp.e[e];
     v = __longlong_as_double(static_cast<long long>(r.x));
     dc = static_cast<int>(r.y);
 }
@@ -112,7 +123,8 @@ __device__ __forceinline__ void dict_entry(const ulonglong2* dict, uint32_t e, d
 // DICT row sum: the lane's words are code[(slice*W + w)*32 + lane]; 32-bit
 // index math throughout (the encoded matrix is < 2^31 words).
 template <int OP>
-__device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int lane, int row) {
+__device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictParam<true>& dp, int slice, int lane,
+                                               int row) {
     const int W = a.words;
     const uint32_t* cp = a.code + (slice * W) * 32 + lane;
     double sum = 0.0;
@@ -126,7 +138,7 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int
 #pragma unroll
         for (int j = 0; j < 8; ++j) {  // branch-free: slot 255 (pad) holds {0, 0}
             int dc;
-            dict_entry(a.dict, e[j], av[j], dc);
+            dict_entry(dp, e[j], av[j], dc);
             xv[j] = e[j] != 0xFFu ? xval<OP>(a, row + dc) : 0.0;
         }
 #pragma unroll
@@ -136,8 +148,16 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int slice, int
     return sum;
 }
 
+template <int OP, bool DICT>
+__device__ __forceinline__ double row_sum(const SellArgs& a, const DictParam<DICT>& dp, int slice, int lane, int row) {
+    if constexpr (DICT)
+        return row_sum_dict<OP>(a, dp, slice, lane, row);
+    else
+        return row_sum_plain<OP>(a, slice, lane);
+}
+
 template <int OP, bool ROWS, bool DICT>
-__global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
+__global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_constant__ DictParam<DICT> dp) {
     const int lane = threadIdx.x & 31;
     const int slice = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (slice >= a.nslices) return;
@@ -154,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
         if (OP == kResid) ri = a.r[row];
         if (OP == kJacobi) xi = a.x[row];
     }
-    const double sum = DICT ? row_sum_dict<OP>(a, slice, lane, row) : row_sum_plain<OP>(a, slice, lane);
+    const double sum = row_sum<OP, DICT>(a, dp, slice, lane, row);
     if (!valid) return;
     if (OP == kSpmv) {
         a.y[row] = sum;
@@ -166,10 +186,11 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a) {
     }
 }
 
-// v = A w with block partials of (w.r, w.v, w.q); grid-stride over slices so
-// the partial count is bounded by the grid (fixed order -> deterministic).
+// v = A w with block partials of (w.r, w.v, w.q) (fixed order ->
+// deterministic).  Launched with one warp per slice like the sweeps; the
+// grid-stride loop only matters for capped grids.
 template <bool DICT, bool ROWS>
-__global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a) {
+__global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, const __grid_constant__ DictParam<DICT> dp) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double sa = 0.0, sb = 0.0, sg = 0.0;
@@ -183,8 +204,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a) {
             rr = a.r[row];
             qq = a.q[row];
         }
-        const double sum = DICT ? row_sum_dict<kSpmv>(a, slice, lane, row)
-                                : row_sum_plain<kSpmv>(a, slice, lane);
+        const double sum = row_sum<kSpmv, DICT>(a, dp, slice, lane, row);
         if (valid) {
             a.y[row] = sum;
             sa = dadd(sa, dmul(wi, rr));
@@ -602,6 +622,7 @@ bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) 
     }
     S.dict.alloc(256, s);
     PB_CUDA(cudaMemcpyAsync(S.dict.get(), rec.data(), 16 * 256, cudaMemcpyHostToDevice, s));
+    S.hdict = rec;  // host copy: passed by value to the kernels (constant bank)
     DBuf<int> dsc(kTableCap, s);
     PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
     S.padded_nnz = S.nslices * 32 * S.words;  // in words
@@ -750,20 +771,28 @@ SellArgs args_of(const Sell& S) {
     return a;
 }
 
+DictParam<true> dict_param(const Sell& S) {
+    DictParam<true> dp;
+    for (int i = 0; i < 256; ++i) dp.e[i] = i < static_cast<int>(S.hdict.size()) ? S.hdict[i] : make_ulonglong2(0ULL, 0ULL);
+    return dp;
+}
+
 template <int OP>
 void launch_op(const Sell& S, const SellArgs& a, cudaStream_t s) {
     const int grid = blocks_for(S.nslices, kWarps);
     const bool rows = a.rows != nullptr;
     if (S.format == Sell::kDict) {
+        const DictParam<true> dp = dict_param(S);
         if (rows)
-            k_sell<OP, true, true><<<grid, kThreads, 0, s>>>(a);
+            k_sell<OP, true, true><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell<OP, false, true><<<grid, kThreads, 0, s>>>(a);
+            k_sell<OP, false, true><<<grid, kThreads, 0, s>>>(a, dp);
     } else {
+        const DictParam<false> dp{0};
         if (rows)
-            k_sell<OP, true, false><<<grid, kThreads, 0, s>>>(a);
+            k_sell<OP, true, false><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell<OP, false, false><<<grid, kThreads, 0, s>>>(a);
+            k_sell<OP, false, false><<<grid, kThreads, 0, s>>>(a, dp);
     }
     PB_CHECK_LAUNCH();
 }
@@ -899,7 +928,8 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
 }
 
 int sell_dots_grid(const Sell& S) {
-    const int64_t want = S.format == Sell::kPat ? (S.nrows + kThreads - 1) / kThreads : (S.nslices + kWarps - 1) / kWarps;
+    if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
+    const int64_t want = (S.nrows + kThreads - 1) / kThreads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
 }
 
@@ -930,15 +960,17 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
     a.q = q;
     a.partials = partials;
     if (S.format == Sell::kDict) {
+        const DictParam<true> dp = dict_param(S);
         if (rows)
-            k_sell_spmv_dots<true, true><<<grid, kThreads, 0, s>>>(a);
+            k_sell_spmv_dots<true, true><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell_spmv_dots<true, false><<<grid, kThreads, 0, s>>>(a);
+            k_sell_spmv_dots<true, false><<<grid, kThreads, 0, s>>>(a, dp);
     } else {
+        const DictParam<false> dp{0};
         if (rows)
-            k_sell_spmv_dots<false, true><<<grid, kThreads, 0, s>>>(a);
+            k_sell_spmv_dots<false, true><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell_spmv_dots<false, false><<<grid, kThreads, 0, s>>>(a);
+            k_sell_spmv_dots<false, false><<<grid, kThreads, 0, s>>>(a, dp);
     }
     PB_CHECK_LAUNCH();
     return grid;

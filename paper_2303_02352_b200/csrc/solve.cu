@@ -136,6 +136,29 @@ __global__ void __launch_bounds__(kRedThreads)
     }
 }
 
+constexpr int kStage = 256;
+
+// First stage for large partial counts: block b reduces the contiguous chunk
+// [b*G/gridDim, (b+1)*G/gridDim) of K-tuples in a fixed order.
+__global__ void __launch_bounds__(kRedThreads)
+    k_reduce_chunks(const double* __restrict__ partials, int G, int K, double* __restrict__ out) {
+    __shared__ double red[kRedThreads];
+    const int64_t g0 = static_cast<int64_t>(G) * blockIdx.x / gridDim.x;
+    const int64_t g1 = static_cast<int64_t>(G) * (blockIdx.x + 1) / gridDim.x;
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int64_t g = g0 + threadIdx.x; g < g1; g += kRedThreads) s = dadd(s, partials[g * K + k]);
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] = dadd(red[threadIdx.x], red[threadIdx.x + w]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[blockIdx.x * K + k] = red[0];
+        __syncthreads();
+    }
+}
+
 // Cross-rank sums in rank order (runtime.cpp:388-396), then the FCG scalar
 // recurrences (Alg. 1 lines 4-5, 14; breakdown check SPEC.md:478).
 __global__ void k_fcg_scalars(const double* __restrict__ g, int p, FcgState* __restrict__ st) {
@@ -230,8 +253,13 @@ void Solver::ensure_vectors() {
     v_.alloc(static_cast<size_t>(n_), s_);
     d_.alloc(static_cast<size_t>(n_), s_);
     q_.alloc(static_cast<size_t>(n_), s_);
-    max_blocks_ = kSmCount * 8;
-    partials_.alloc(static_cast<size_t>(2 * 3 * max_blocks_), s_);  // interior + boundary launches
+    // partial triples of the SpMV+dots launches (interior + boundary, one
+    // block per 8 slices) and of the grid-stride reductions
+    const int64_t dots_blocks = L0.A.halo.n_halo > 0 ? int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd)
+                                                     : int64_t(sell_dots_grid(L0.sell_all));
+    max_blocks_ = static_cast<int>(std::max<int64_t>(dots_blocks, kSmCount * 8));
+    partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
+    stage_.alloc(static_cast<size_t>(3 * kStage), s_);
     local_.alloc(8, s_);
     gathered_.alloc(static_cast<size_t>(4 * rt.nranks()), s_);
     state_.alloc(1, s_);
@@ -415,7 +443,14 @@ void Solver::reduce_dots_enqueue() {
     // partial count G is encoded by the producer; it is fixed for the level
     Level& L0 = *h.levels[0];
     const int G = dots_grid_;  // partial triples written by the SpMV+dots launches
-    k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), G, 3, local_.get());
+    if (G > kStage) {  // two fixed-order stages: kStage blocks over contiguous chunks, then one block
+        k_reduce_chunks<<<kStage, kRedThreads, 0, s_>>>(partials_.get(), G, 3, stage_.get());
+        PB_CHECK_LAUNCH();
+        k_reduce<<<1, kRedThreads, 0, s_>>>(stage_.get(), kStage, 3, local_.get());
+        launches_ += 1;
+    } else {
+        k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), G, 3, local_.get());
+    }
     PB_CHECK_LAUNCH();
     const double* g = local_.get();
     if (p > 1) {

@@ -73,7 +73,7 @@ private:
     cudaStream_t s_;
     int64_t n_ = 0, next_ = 0;
     DBuf<double> u_, r_, w_, v_, d_, q_;
-    DBuf<double> partials_, local_, gathered_;
+    DBuf<double> partials_, stage_, local_, gathered_;
     DBuf<FcgState> state_;
     FcgState* h_state_ = nullptr;  // pinned
     int max_blocks_ = 0;
