@@ -44,13 +44,16 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_key: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def ncu_traffic(kernel_key: str, workload: str, n_gpus: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set
+    full summary, only when it was captured on this workload (1 GPU)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+            d = json.load(f).get(kernel_key, {})
+        if n_gpus != 1 or d.get("workload") != workload:
+            return None
+        return d.get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -361,7 +364,7 @@ def bench_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return None
-    traffic = ncu_traffic("l1_jacobi_sweep_L0")
+    traffic = ncu_traffic("l1_jacobi_sweep_L0", config_dict(args, world)["workload"], world)
     line = {
         "metric": METRIC, "value": t_solve, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_solve * 1e3, "higher_is_better": False,

@@ -935,6 +935,10 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, env_flag("PAIRAMG_SELL_DICT", true),
                        L.l1.get());
             build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s, /*allow_dict=*/false);
+            // whole level incl. halo columns, for the exchange-then-compute
+            // schedule (slab partitions keep constant halo column offsets,
+            // so DICT/PAT usually still apply)
+            build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true), L.l1.get());
         } else {
             build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true), L.l1.get());
         }

@@ -210,6 +210,7 @@ int red_grid(int64_t n) {
 
 Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
     fuse = env_flag("PAIRAMG_FUSE", false);
+    overlap = env_flag("PAIRAMG_OVERLAP", true);
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
@@ -322,6 +323,14 @@ void Solver::apply(int k, const SellOpArgs& o, int kc) { apply_on(lvl(k), o, kc)
 
 void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
     begin_time(kc);
+    if (L.A.halo.has_traffic() && !overlap) {
+        // exchange first (on the compute stream), then one kernel over all rows
+        halo_exchange(rt, L.A.halo, o.x, const_cast<double*>(o.x) + L.A.n, s_);
+        sell_apply(L.sell_all, o, s_);
+        launches_ += 1 + (L.A.halo.send_off.back() ? 1 : 0);
+        end_time(kc);
+        return;
+    }
     if (L.A.halo.has_traffic()) {
         if (o.op == kJacobiZero || o.op == kJacobiProl)
             fail(PAIRAMG_INTERNAL, "fused sweeps need a level without halo traffic");
@@ -488,14 +497,20 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     w_out_ = w;
     // v = A w and the dot triple (Alg. 1 lines 10-13)
     begin_time(2);
-    if (L0.A.halo.has_traffic()) {  // halo of w in flight while the interior rows run
+    if (L0.A.halo.has_traffic() && !overlap) {
+        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, s_);
+        dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
+        launches_ += 2;
+    } else if (L0.A.halo.has_traffic()) {  // halo of w in flight while the interior rows run
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
         halo_exchange(rt, L0.A.halo, w, w + L0.A.n, rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }
-    if (L0.A.halo.n_halo > 0) {
+    if (L0.A.halo.has_traffic() && !overlap) {
+        // done above
+    } else if (L0.A.halo.n_halo > 0) {
         const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         const int g2 = sell_spmv_dots(L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get() + 3 * g1,

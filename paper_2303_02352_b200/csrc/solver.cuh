@@ -47,7 +47,8 @@ public:
     Hierarchy h;
     bool ready = false;
     bool timing = false;
-    bool fuse = true;  // fused zero-start / prolongation sweeps on halo-free levels
+    bool fuse = true;     // fused zero-start / prolongation sweeps on halo-free levels
+    bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 

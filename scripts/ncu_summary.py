@@ -92,6 +92,7 @@ def main():
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--key", action="append", default=[], help="json_key=kernel-substring")
     ap.add_argument("--note", default="")
+    ap.add_argument("--workload", default="poisson7_256x256x256", help="bench config.workload of the capture")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
@@ -126,7 +127,7 @@ def main():
             if sel:
                 r = sel[0]
                 js[key] = {"kernel": r["kernel"], "dram_bytes_per_launch": r["dram_bytes"], "time_us_ncu": r.get("time"),
-                           "source": f"{a.tag} {r['rep']}"}
+                           "source": f"{a.tag} {r['rep']}", "workload": a.workload}
         json.dump(js, open(jp, "w"), indent=1)
     print(open(os.path.join(PROF, f"{a.tag}_launches.md")).read() if a.launches else "")
 
