@@ -186,6 +186,17 @@ __global__ void k_fcg_scalars(const double* __restrict__ g, int p, FcgState* __r
     st->rho = rho_new;
 }
 
+// Device-side stopping test of the graph loop (same operations as the host
+// loop: rel = sqrt(rr)/sqrt(rr0); stop on rel < rtol, max_iters or breakdown).
+__global__ void k_loop_ctl(const FcgState* __restrict__ st, double rtol, int max_iters, double* __restrict__ hist,
+                           cudaGraphConditionalHandle h) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double rel = ddiv(__dsqrt_rn(st->rr), __dsqrt_rn(st->rr0));
+    if (st->it <= max_iters) hist[st->it] = rel;
+    const bool stop = st->status != 0 || rel < rtol || st->it >= max_iters;
+    cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
 __global__ void k_norm_final(const double* __restrict__ g, int p, FcgState* __restrict__ st, int init) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double rr = 0.0;
@@ -233,6 +244,43 @@ Solver::~Solver() {
 void Solver::destroy_graph() {
     if (graph_) cudaGraphExecDestroy(graph_);
     graph_ = nullptr;
+    if (loop_graph_) cudaGraphExecDestroy(loop_graph_);
+    loop_graph_ = nullptr;
+}
+
+void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters) {
+    if (loop_graph_ && loop_cc_.pre_sweeps == cc.pre_sweeps && loop_cc_.post_sweeps == cc.post_sweeps &&
+        loop_cc_.coarsest_sweeps == cc.coarsest_sweeps && loop_cc_.relax_weight == cc.relax_weight &&
+        loop_prec_ == precflag && loop_rtol_ == rtol && loop_maxit_ == max_iters)
+        return;
+    if (loop_graph_) cudaGraphExecDestroy(loop_graph_);
+    loop_graph_ = nullptr;
+    hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
+    cudaGraph_t g;
+    PB_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle handle;
+    PB_CUDA(cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    PB_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const int64_t l0 = launches_;
+    PB_CUDA(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    iteration_enqueue(cc, precflag);
+    k_loop_ctl<<<1, 32, 0, s_>>>(state_.get(), rtol, max_iters, hist_.get(), handle);
+    PB_CHECK_LAUNCH();
+    PB_CUDA(cudaStreamEndCapture(s_, &body));
+    launches_ = l0;
+    PB_CUDA(cudaGraphInstantiate(&loop_graph_, g, 0));
+    PB_CUDA(cudaGraphDestroy(g));
+    loop_cc_ = cc;
+    loop_prec_ = precflag;
+    loop_rtol_ = rtol;
+    loop_maxit_ = max_iters;
 }
 
 void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t>&& col, DBuf<double>&& val,
@@ -611,18 +659,35 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             graph_prec_ = precflag;
             graph_timing_ = timing;
         }
-        while (true) {
-            PB_CUDA(cudaGraphLaunch(graph_, s_));
-            launches_ += per_iter_launches_;
+        const bool device_loop = loop_ok && rt.nranks() == 1 && !timing && env_flag("PAIRAMG_GRAPH_LOOP", true);
+        if (device_loop) {
+            // the whole iteration loop as ONE graph launch: a conditional WHILE
+            // node re-runs the captured iteration until k_loop_ctl clears it
+            ensure_loop_graph(cc, precflag, rtol, max_iters);
+            PB_CUDA(cudaGraphLaunch(loop_graph_, s_));
             PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
             PB_CUDA(cudaStreamSynchronize(s_));
-            collect_times();
-            if (h_state_->status)
-                fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(h_state_->it));
             it = h_state_->it;
-            rel = std::sqrt(h_state_->rr) / rnorm0;
-            hist.push_back(rel);
-            if (rel < rtol || it >= max_iters) break;
+            launches_ += (per_iter_launches_ + 1) * it;
+            if (h_state_->status) fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(it));
+            std::vector<double> dh(static_cast<size_t>(it) + 1);
+            PB_CUDA(cudaMemcpy(dh.data(), hist_.get(), 8 * (it + 1), cudaMemcpyDeviceToHost));
+            for (int i = 1; i <= it; ++i) hist.push_back(dh[static_cast<size_t>(i)]);
+            rel = dh[static_cast<size_t>(it)];
+        } else {
+            while (true) {
+                PB_CUDA(cudaGraphLaunch(graph_, s_));
+                launches_ += per_iter_launches_;
+                PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
+                PB_CUDA(cudaStreamSynchronize(s_));
+                collect_times();
+                if (h_state_->status)
+                    fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(h_state_->it));
+                it = h_state_->it;
+                rel = std::sqrt(h_state_->rr) / rnorm0;
+                hist.push_back(rel);
+                if (rel < rtol || it >= max_iters) break;
+            }
         }
     }
     if (n_) PB_CUDA(cudaMemcpyAsync(d_u, u_.get(), 8 * n_, cudaMemcpyDeviceToDevice, s_));

@@ -49,6 +49,7 @@ public:
     bool timing = false;
     bool fuse = true;     // fused zero-start / prolongation sweeps on halo-free levels
     bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
+    bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
@@ -84,6 +85,14 @@ private:
     CycleConfig graph_cc_{};
     bool graph_prec_ = true;
     bool graph_timing_ = false;
+    // whole-solve graph: conditional WHILE node around the captured iteration
+    cudaGraphExec_t loop_graph_ = nullptr;
+    CycleConfig loop_cc_{};
+    bool loop_prec_ = true;
+    double loop_rtol_ = 0.0;
+    int loop_maxit_ = 0;
+    DBuf<double> hist_;
+    void ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters);
     int64_t per_iter_launches_ = 0;
     std::vector<cudaEvent_t> ev_pool_;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
