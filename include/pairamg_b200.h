@@ -170,6 +170,11 @@ pairamg_status pairamg_hierarchy_info(pairamg_solver* s, int* nlevels, double* o
 pairamg_status pairamg_level_info(pairamg_solver* s, int level, int64_t* global_rows,
                                   int64_t* global_nnz, int64_t* row_begin, int64_t* local_rows,
                                   int64_t* local_nnz);
+/* Solve-time storage of level k's owned rows (B200 extension, no reference
+ * counterpart): 0 PLAIN SELL-32, 1 DICT, 2 PAT, 3 STEN -- for the interior
+ * row set when the level has halo traffic.  All formats give bitwise-equal
+ * results; this only reports which kernels run. */
+pairamg_status pairamg_level_storage(pairamg_solver* s, int level, int* format);
 /* Owned rows of A^k: row_ptr (local_rows+1), col (local_nnz, GLOBAL ids,
  * ascending), val; w^k and the l1 diagonal (local_rows).  Any pointer may be NULL. */
 pairamg_status pairamg_level_export(pairamg_solver* s, int level, int64_t* row_ptr, int64_t* col,

@@ -30,7 +30,7 @@ EXPORTS = [
     "pairamg_status_name", "pairamg_last_error", "pairamg_abi_version", "pairamg_comm_unique_id",
     "pairamg_runtime_create", "pairamg_runtime_destroy", "pairamg_solver_create", "pairamg_solver_destroy",
     "pairamg_setup", "pairamg_setup_device", "pairamg_solve", "pairamg_solve_device", "pairamg_vcycle",
-    "pairamg_spmv", "pairamg_hierarchy_info", "pairamg_level_info", "pairamg_level_export",
+    "pairamg_spmv", "pairamg_hierarchy_info", "pairamg_level_info", "pairamg_level_storage", "pairamg_level_export",
     "pairamg_prolongator_export", "pairamg_num_matchings", "pairamg_matching_export",
     "pairamg_get_setup_stats", "pairamg_set_kernel_timing", "pairamg_kernel_timing", "pairamg_launch_count",
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
@@ -102,6 +102,11 @@ def lib() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2303_02352_b200.build` "
                           "(the B200 path has no CPU fallback)")
+    # torch first: its bundled libnccl.so.2 (newer) must be the copy the
+    # process binds; loading ours first would bind the system one and break
+    # a later `import torch` (missing ncclDevCommCreate).
+    import torch  # noqa: F401
+
     L = C.CDLL(LIB_PATH)
     vp, i64, st = C.c_void_p, C.c_int64, C.c_int
     sig = {
@@ -122,6 +127,7 @@ def lib() -> C.CDLL:
         "pairamg_spmv": ([vp, C.c_int, vp, vp, C.c_int], st),
         "pairamg_hierarchy_info": ([vp, C.POINTER(C.c_int), C.POINTER(C.c_double)], st),
         "pairamg_level_info": ([vp, C.c_int] + [C.POINTER(i64)] * 5, st),
+        "pairamg_level_storage": ([vp, C.c_int, C.POINTER(C.c_int)], st),
         "pairamg_level_export": ([vp, C.c_int, vp, vp, vp, vp, vp], st),
         "pairamg_prolongator_export": ([vp, C.c_int, vp, vp], st),
         "pairamg_num_matchings": ([vp, C.POINTER(C.c_int)], st),
@@ -302,6 +308,14 @@ class Solver:
         v = [C.c_int64() for _ in range(5)]
         _check(lib().pairamg_level_info(self.h, k, *[C.byref(x) for x in v]))
         return dict(zip(["global_rows", "global_nnz", "row_begin", "local_rows", "local_nnz"], [x.value for x in v]))
+
+    STORAGE = ("plain", "dict", "pat", "sten")
+
+    def level_storage(self, k) -> str:
+        """Solve-time storage format of level k (which row kernels run)."""
+        f = C.c_int()
+        _check(lib().pairamg_level_storage(self.h, k, C.byref(f)))
+        return self.STORAGE[f.value]
 
     def level_sizes(self):
         return [(self.level_info(k)["global_rows"], self.level_info(k)["global_nnz"]) for k in range(self.num_levels)]

@@ -373,6 +373,17 @@ pairamg_status pairamg_level_info(pairamg_solver* s, int level, int64_t* global_
     });
 }
 
+pairamg_status pairamg_level_storage(pairamg_solver* s, int level, int* format) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!sv.ready) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "setup not run");
+        if (level < 0 || level >= sv.h.nl()) pb::fail(PAIRAMG_INVALID_ARGUMENT, "level out of range");
+        if (!format) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null format");
+        const pb::Level& L = *sv.h.levels[level];
+        *format = L.A.halo.n_halo > 0 && L.sell_int.nrows > 0 ? L.sell_int.format : L.sell_all.format;
+    });
+}
+
 pairamg_status pairamg_level_export(pairamg_solver* s, int level, int64_t* row_ptr, int64_t* col, double* val,
                                     double* w, double* l1) {
     return guarded([&] {

@@ -54,6 +54,18 @@ struct DevMatrix {
     int64_t n_boundary = 0;
 };
 
+// Shared-memory window plan of a DICT Sell (sell_win.cuh): the distinct
+// column offsets clustered into <= kWinMax contiguous windows per tile.
+constexpr int kWinMax = 12;
+struct SellWin {
+    bool ok = false;
+    int T = 0, nwin = 0, ntiles = 0, grid = 0;
+    int lo[kWinMax] = {}, len[kWinMax] = {}, soff[kWinMax] = {};
+    int r_soff = 0, d_soff = 0, q_soff = 0, c_soff = 0, stage = 0, al_r = 0, base0 = 0;
+    size_t smem = 0;                // dynamic shared memory per CTA (2 stages)
+    std::vector<ulonglong2> rec;   // 256 records {value bits, shared-memory base}
+};
+
 struct Sell {
     // PAT  : one byte per ROW naming its row pattern (the row's full sequence
     //        of (column - row, value) entries; <= 255 distinct patterns); the
@@ -61,7 +73,11 @@ struct Sell {
     //        live in global memory (L1-resident).  Preferred when it applies.
     // DICT : one byte per entry (<= 255 distinct (column - row, value)).
     // PLAIN: int32 column + f64 value per entry.
-    enum Format { kPlain = 0, kDict = 1, kPat = 2 };
+    // STEN : every row an order-preserving subset of one main pattern: PAT's
+    //        byte per row names the subset (absent-record mask + l1 diagonal);
+    //        the main records and the per-pattern data travel as a kernel
+    //        parameter.  Preferred whenever it applies (sell_sten.cuh).
+    enum Format { kPlain = 0, kDict = 1, kPat = 2, kSten = 3 };
     int format = kPlain;
     int64_t nrows = 0, nslices = 0, padded_nnz = 0;
     DBuf<int64_t> slice_off;  // nslices+1; elements (PLAIN) or 32-bit code words (DICT), multiples of 32
@@ -72,11 +88,21 @@ struct Sell {
     DBuf<ulonglong2> dict;    // DICT: 256 records {value bits, column - row}; [255] = pad {0, 0}
     std::vector<ulonglong2> hdict;  // DICT: host copy, passed to the kernels as a __grid_constant__ parameter
     int ndict = 0;
+    DBuf<uint8_t> dcode;            // DICT: l1 diagonal code per SELL row (empty = read the l1 array)
+    std::vector<double> hdiag;      // DICT: the distinct l1 values, passed with the dictionary
+    SellWin win;                    // DICT: shared-memory window plan (contiguous row sets)
     DBuf<uint8_t> pid;        // PAT: pattern id per row (indexed by row id)
     DBuf<ulonglong2> ptab;    // PAT: pattern records {value bits, column - row}
     DBuf<int2> pmeta;         // PAT: {first record, length} per pattern
     DBuf<double> pdiag;       // PAT: l1 diagonal per pattern (bitwise = l1_diagonal)
     int npat = 0, maxlen = 0;
+    std::vector<ulonglong2> hptab;  // PAT host copies (STEN conversion)
+    std::vector<int2> hpmeta;
+    std::vector<double> hpdiag;
+    int sten_L = 0, sten_offmin = 0, sten_offmax = 0;  // STEN: main pattern
+    std::vector<int> sten_off;
+    std::vector<double> sten_val;
+    std::vector<uint32_t> sten_mask;  // per pattern: absent main records
     int64_t xlen = 0;         // gathered vector length (owned + halo slots)
     DBuf<int32_t> rows;       // row id of each SELL row; empty = row0 + index
     int64_t row0 = 0;

@@ -9,9 +9,12 @@
 //            so a lane's words sit at code[(slice*W + w)*32 + lane] (no offset
 //            table on the critical path).  Chosen automatically when the rows
 //            have <= 255 distinct pairs (every level of the slab-aligned
-//            Poisson hierarchies has 7 or 27).  The dictionary is staged in
-//            shared memory.  Columns and values are reproduced exactly, so
-//            every row sum is bit-identical to PLAIN and to spmv_local.
+//            Poisson hierarchies has 7 or 27).  The dictionary travels in the
+//            constant bank (kernel parameter), with the distinct l1 diagonal
+//            values when a level has <= 256 of them (then a 1-byte code per
+//            row replaces the 8-byte diagonal stream).  Columns and values
+//            are reproduced exactly, so every row sum is bit-identical to
+//            PLAIN and to spmv_local.
 //
 // Operators (one warp per slice, one lane per row, CSR-order sums with
 // separately rounded multiply/add; the row's own operands are loaded before
@@ -66,6 +69,7 @@ struct SellArgs {
     const double* e;
     const double* q;
     double* partials;
+    const uint8_t* dcode;  // DICT: l1 diagonal code per SELL row (DictParam::dg), or null
 };
 
 template <int OP>
@@ -108,6 +112,7 @@ __device__ __forceinline__ double row_sum_plain(const SellArgs& a, int64_t slice
 template <bool DICT>
 struct DictParam {
     ulonglong2 e[256];
+    double dg[256];  // distinct l1 diagonal values (when SellArgs::dcode is set)
 };
 template <>
 struct DictParam<false> {
@@ -122,6 +127,13 @@ __device__ __forceinline__ void dict_entry(const DictParam<true>& dp, uint32_t e
 
 // DICT row sum: the lane's words are code[(slice*W + w)*32 + lane]; 32-bit
 // index math throughout (the encoded matrix is < 2^31 words).
+//
+// Pads are not predicated away: code 0xFF is the record {+0.0, 0}, so a pad
+// gathers the row's own x and adds +0.0 * x = +-0.  The sum starts at +0.0
+// and a round-to-nearest sum that starts at +0 never becomes -0, so adding
+// +-0 leaves every bit of it unchanged (for finite x): the CSR-order sum is
+// reproduced exactly with 5 fewer instructions per entry (predicate, two
+// selects, zeroing) on this issue-bound loop.
 template <int OP>
 __device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictParam<true>& dp, int slice, int lane,
                                                int row) {
@@ -136,14 +148,13 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictPara
 #pragma unroll
         for (int j = 0; j < 8; ++j) e[j] = ((j < 4 ? wa : wb) >> (8 * (j & 3))) & 0xFFu;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {  // branch-free: slot 255 (pad) holds {0, 0}
+        for (int j = 0; j < 8; ++j) {
             int dc;
             dict_entry(dp, e[j], av[j], dc);
-            xv[j] = e[j] != 0xFFu ? xval<OP>(a, row + dc) : 0.0;
+            xv[j] = xval<OP>(a, row + dc);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (e[j] != 0xFFu) sum = dadd(sum, dmul(av[j], xv[j]));
+        for (int j = 0; j < 8; ++j) sum = dadd(sum, dmul(av[j], xv[j]));
     }
     return sum;
 }
@@ -169,7 +180,10 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
     if (valid) {
         if (OP == kJacobi || OP == kJacobiZero || OP == kJacobiProl) {
             ri = a.r[row];
-            di = a.d[row];
+            if constexpr (DICT)
+                di = a.dcode ? dp.dg[a.dcode[sr]] : a.d[row];
+            else
+                di = a.d[row];
         }
         if (OP == kResid) ri = a.r[row];
         if (OP == kJacobi) xi = a.x[row];
@@ -230,6 +244,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, cons
         a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
     }
 }
+
+#include "sell_win.cuh"
+#include "sell_sten.cuh"
 
 // ------------------------------------------------------------------ PAT ---
 //
@@ -567,6 +584,30 @@ __global__ void k_sell_fill_dict(const int64_t* __restrict__ rp, const int32_t* 
     }
 }
 
+// l1 diagonal codes: key (0, value bits) in the same open-addressing table.
+__global__ void k_diag_insert(const double* __restrict__ l1, const int32_t* __restrict__ rows, int64_t row0,
+                              int64_t nrows, ull* table, unsigned* count, int* overflow) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows || *reinterpret_cast<volatile int*>(overflow)) return;
+    const int64_t row = rows ? rows[sr] : row0 + sr;
+    table_find(table, 0, static_cast<ull>(__double_as_longlong(l1[row])), true, count, overflow);
+}
+
+__global__ void k_diag_fill(const double* __restrict__ l1, const int32_t* __restrict__ rows, int64_t row0,
+                            int64_t nrows, ull* table, const int* __restrict__ slot_code, uint8_t* __restrict__ dcode,
+                            int* bad) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : row0 + sr;
+    const int slot = table_find(table, 0, static_cast<ull>(__double_as_longlong(l1[row])), false, nullptr, nullptr);
+    const int c = slot < 0 ? -1 : slot_code[slot];
+    if (c < 0) {
+        atomicExch(bad, 1);
+        return;
+    }
+    dcode[sr] = static_cast<uint8_t>(c);
+}
+
 template <typename F>
 void cub_call(F&& f, cudaStream_t s) {
     size_t bytes = 0;
@@ -575,7 +616,168 @@ void cub_call(F&& f, cudaStream_t s) {
     PB_CUDA(f(tmp.get(), bytes));
 }
 
-bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) {
+// Window plan (sell_win.cuh) from the dictionary's column offsets.
+void plan_windows(Sell& S, const std::vector<int32_t>& dcol, const std::vector<double>& dval) {
+    SellWin& P = S.win;
+    P = SellWin();
+    std::vector<int64_t> offs(dcol.begin(), dcol.end());
+    offs.push_back(0);  // pads read the row's own x
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    constexpr int64_t kWinGap = 8;
+    std::vector<std::pair<int64_t, int64_t>> win;  // [lo, hi]
+    for (int64_t o : offs) {
+        if (!win.empty() && o - win.back().second <= kWinGap)
+            win.back().second = o;
+        else
+            win.push_back({o, o});
+    }
+    if (win.size() > static_cast<size_t>(kWinMax)) return;
+    const int T = std::max(64, env_int("PAIRAMG_WIN_T", 512) / 64 * 64);
+    P.T = T;
+    P.nwin = static_cast<int>(win.size());
+    int off = 0;
+    std::vector<int> al(win.size());
+    for (size_t k = 0; k < win.size(); ++k) {
+        const int64_t lo = win[k].first, span = win[k].second - win[k].first;
+        al[k] = static_cast<int>((S.row0 + lo) & 1);
+        P.lo[k] = static_cast<int>(lo);
+        P.len[k] = static_cast<int>((al[k] + T + span + 1) & ~int64_t(1));
+        P.soff[k] = off;
+        off += P.len[k];
+    }
+    P.al_r = static_cast<int>(S.row0 & 1);
+    P.r_soff = off;
+    off += T + 2;
+    P.d_soff = off;
+    off += T + 2;
+    P.q_soff = off;
+    off += T + 2;
+    P.c_soff = off;
+    off += T * S.words / 2;
+    P.stage = off;
+    P.smem = static_cast<size_t>(2) * off * 8;
+    if (P.smem > static_cast<size_t>(kWinSmemCap)) return;
+    auto base_of = [&](int64_t o) {
+        for (size_t k = 0; k < win.size(); ++k)
+            if (o >= win[k].first && o <= win[k].second)
+                return P.soff[k] + al[k] + static_cast<int>(o - win[k].first);
+        return -1;
+    };
+    P.base0 = base_of(0);
+    P.rec.assign(256, make_ulonglong2(0ULL, static_cast<ull>(P.base0)));
+    for (size_t c = 0; c < dcol.size(); ++c) {
+        ull vb;
+        std::memcpy(&vb, &dval[c], 8);
+        P.rec[c] = make_ulonglong2(vb, static_cast<ull>(base_of(dcol[c])));
+    }
+    P.ntiles = static_cast<int>((S.nslices * 32 + T - 1) / T);
+    int per_sm = 0;
+    const void* fns[] = {reinterpret_cast<const void*>(&k_win<kSpmv>), reinterpret_cast<const void*>(&k_win<kJacobi>),
+                         reinterpret_cast<const void*>(&k_win<kResid>), reinterpret_cast<const void*>(&k_win<-1>)};
+    for (const void* f : fns) {
+        // one ceiling for every Sell (the attribute is per function, last write wins)
+        PB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemCap));
+        int nb = 0;
+        PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kWinThreads, P.smem));
+        per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
+    }
+    if (per_sm < 1) return;
+    P.grid = std::min(P.ntiles, kSmCount * per_sm);
+    P.ok = true;
+}
+
+WinArgs win_args_of(const Sell& S) {
+    const SellWin& P = S.win;
+    WinArgs a{};
+    a.code = S.code.get();
+    a.words = S.words;
+    a.row0 = static_cast<int>(S.row0);
+    a.nrows = static_cast<int>(S.nrows);
+    a.nslices = static_cast<int>(S.nslices);
+    a.ntiles = P.ntiles;
+    a.T = P.T;
+    a.xlen = S.xlen;
+    a.nwin = P.nwin;
+    for (int k = 0; k < kWinMax; ++k) {
+        a.lo[k] = P.lo[k];
+        a.len[k] = P.len[k];
+        a.soff[k] = P.soff[k];
+    }
+    a.r_soff = P.r_soff;
+    a.d_soff = P.d_soff;
+    a.q_soff = P.q_soff;
+    a.c_soff = P.c_soff;
+    a.stage = P.stage;
+    a.al_r = P.al_r;
+    a.base0 = P.base0;
+    return a;
+}
+
+DictParam<true> win_param(const Sell& S) {
+    DictParam<true> dp;
+    for (int i = 0; i < 256; ++i) {
+        dp.e[i] = S.win.rec[i];
+        dp.dg[i] = 1.0;
+    }
+    return dp;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+bool use_win(const Sell& S, const SellOpArgs& o) {
+    if (!S.win.ok || S.format != Sell::kDict) return false;
+    if (o.op != kSpmv && o.op != kJacobi && o.op != kResid) return false;
+    return aligned16(o.x) && (o.op == kSpmv || aligned16(o.r)) && (o.op != kJacobi || aligned16(o.d));
+}
+
+// Replace the 8-byte l1 diagonal stream of a DICT Sell by a 1-byte code per
+// row into <= 256 distinct values (exact bits) passed with the dictionary.
+void try_diag_codes(const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
+    const int32_t* rl = S.rows.empty() ? nullptr : rows;
+    DBuf<ull> table(2 * kTableCap, s);
+    DBuf<unsigned> cnt(1, s);
+    DBuf<int> flags(2, s);
+    cnt.zero(s);
+    flags.zero(s);
+    k_table_init<<<kTableCap / 256, 256, 0, s>>>(table.get());
+    k_diag_insert<<<blocks_for(S.nrows, 256), 256, 0, s>>>(l1, rl, S.row0, S.nrows, table.get(), cnt.get(),
+                                                            flags.get());
+    PB_CHECK_LAUNCH();
+    int over = 0;
+    std::vector<ull> h(2 * kTableCap);
+    PB_CUDA(cudaMemcpyAsync(&over, flags.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaMemcpyAsync(h.data(), table.get(), 16 * kTableCap, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (over) return;
+    std::vector<std::pair<ull, int>> vals;  // (value bits, slot), ascending -> deterministic codes
+    for (int i = 0; i < kTableCap; ++i)
+        if (!(h[2 * i] == kEmptyLo && h[2 * i + 1] == 0)) vals.push_back({h[2 * i + 1], i});
+    if (vals.empty() || vals.size() > 256) return;
+    std::sort(vals.begin(), vals.end());
+    std::vector<int> slot_code(kTableCap, -1);
+    S.hdiag.assign(256, 1.0);
+    for (size_t c = 0; c < vals.size(); ++c) {
+        slot_code[vals[c].second] = static_cast<int>(c);
+        std::memcpy(&S.hdiag[c], &vals[c].first, 8);
+    }
+    DBuf<int> dsc(kTableCap, s);
+    PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
+    S.dcode.alloc(static_cast<size_t>(S.nslices * 32), s);
+    PB_CUDA(cudaMemsetAsync(S.dcode.get(), 0, S.nslices * 32, s));
+    k_diag_fill<<<blocks_for(S.nrows, 256), 256, 0, s>>>(l1, rl, S.row0, S.nrows, table.get(), dsc.get(),
+                                                          S.dcode.get(), flags.get() + 1);
+    PB_CHECK_LAUNCH();
+    int bad = 0;
+    PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (bad) {
+        S.dcode.reset();
+        S.hdiag.clear();
+    }
+}
+
+bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
     if (S.nrows == 0) return false;
     if (S.nslices * 32 >= (int64_t(1) << 31) / 8) return false;  // 32-bit code index range
     DBuf<ull> table(2 * kTableCap, s);
@@ -637,6 +839,8 @@ bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) 
     PB_CUDA(cudaStreamSynchronize(s));
     if (bad) fail(PAIRAMG_INTERNAL, "sell: dictionary encoding lost an entry");
     S.format = Sell::kDict;
+    if (l1 && env_flag("PAIRAMG_DIAG_CODE", false)) try_diag_codes(rows, S, l1, s);
+    if (S.rows.empty() && env_flag("PAIRAMG_WIN", false)) plan_windows(S, dcol, dval);
     return true;
 }
 
@@ -653,6 +857,63 @@ void max_row_len(const DevMatrix& M, const int32_t* rows, int64_t nrows, int64_t
     k_max_len<<<blocks_for(nrows, 256), 256, 0, s>>>(M.rp.get(), rows, nrows,
                                                      reinterpret_cast<unsigned long long*>(d_out));
     PB_CHECK_LAUNCH();
+}
+
+void reset_pat(Sell& S) {
+    S.pid.reset();
+    S.ptab.reset();
+    S.pmeta.reset();
+    S.pdiag.reset();
+    S.npat = 0;
+    S.maxlen = 0;
+    S.hptab.clear();
+    S.hpmeta.clear();
+    S.hpdiag.clear();
+    S.format = Sell::kPlain;
+}
+
+// PAT -> STEN when every pattern is an order-preserving subset of the
+// longest one with bitwise-equal records.
+bool try_sten(Sell& S) {
+    if (S.npat < 1) return false;
+    int mp = 0;
+    for (int p = 1; p < S.npat; ++p)
+        if (S.hpmeta[p].y > S.hpmeta[mp].y) mp = p;
+    const int L = S.hpmeta[mp].y;
+    if (L < 1 || L > kStenMax) return false;
+    const ulonglong2* mr = S.hptab.data() + S.hpmeta[mp].x;
+    std::vector<uint32_t> mask(S.npat, 0u);
+    for (int p = 0; p < S.npat; ++p) {
+        const ulonglong2* pr = S.hptab.data() + S.hpmeta[p].x;
+        int j = 0;
+        uint32_t present = 0;
+        for (int t = 0; t < S.hpmeta[p].y; ++t) {
+            while (j < L && !(mr[j].x == pr[t].x && mr[j].y == pr[t].y)) ++j;
+            if (j == L) return false;
+            present |= 1u << j;
+            ++j;
+        }
+        mask[p] = ~present & (L == 32 ? 0xFFFFFFFFu : ((1u << L) - 1u));
+    }
+    S.sten_L = L;
+    S.sten_off.assign(L, 0);
+    S.sten_val.assign(L, 0.0);
+    int64_t omin = 0, omax = 0;
+    for (int k = 0; k < L; ++k) {
+        const int64_t o = static_cast<int64_t>(mr[k].y);
+        S.sten_off[k] = static_cast<int>(o);
+        std::memcpy(&S.sten_val[k], &mr[k].x, 8);
+        omin = std::min(omin, o);
+        omax = std::max(omax, o);
+    }
+    S.sten_offmin = static_cast<int>(omin);
+    S.sten_offmax = static_cast<int>(omax);
+    S.sten_mask = mask;
+    S.ptab.reset();
+    S.pmeta.reset();
+    S.pdiag.reset();
+    S.format = Sell::kSten;
+    return true;
 }
 
 bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
@@ -713,6 +974,9 @@ bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double*
     }
     S.npat = static_cast<int>(pats.size());
     S.maxlen = maxlen;
+    S.hptab = rec;
+    S.hpmeta = meta;
+    S.hpdiag = pd;
     rec.resize(rec.size() + static_cast<size_t>((maxlen + 7) / 8) * 8, make_ulonglong2(0ULL, 0ULL));  // load padding
     S.ptab.alloc(std::max<size_t>(rec.size(), 1), s);
     S.pmeta.alloc(meta.size(), s);
@@ -731,15 +995,71 @@ bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double*
     PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
     PB_CUDA(cudaStreamSynchronize(s));
     if (bad) {  // hash collision or l1 mismatch: keep an exact format instead
-        S.pid.reset();
-        S.ptab.reset();
-        S.pmeta.reset();
-        S.pdiag.reset();
-        S.npat = 0;
+        reset_pat(S);
         return false;
     }
     S.format = Sell::kPat;
     return true;
+}
+
+StenArgs sten_args_of(const Sell& S) {
+    StenArgs a{};
+    a.pid = S.pid.get();
+    a.rows = S.rows.empty() ? nullptr : S.rows.get();
+    a.row0 = static_cast<int>(S.row0);
+    a.nrows = static_cast<int>(S.nrows);
+    a.xlen = static_cast<int>(S.xlen);
+    a.L = S.sten_L;
+    // blocks whose rows r all satisfy r + offmin >= 0 and r + offmax < xlen
+    // (first and last row grow with the block index: both tests are monotone)
+    const int64_t nb = (S.nrows + 255) / 256;
+    int64_t lo = 0, hi = 0;
+    if (S.rows.empty() && nb > 0) {
+        auto last = [&](int64_t b) { return S.row0 + std::min<int64_t>(256 * b + 255, S.nrows - 1); };
+        while (lo < nb && S.row0 + 256 * lo + S.sten_offmin < 0) ++lo;
+        hi = nb;
+        while (hi > lo && last(hi - 1) + S.sten_offmax > S.xlen - 1) --hi;
+    }
+    a.safe_lo = static_cast<int>(lo);
+    a.safe_hi = static_cast<int>(hi);
+    return a;
+}
+
+StenParam sten_param(const Sell& S) {
+    StenParam p{};
+    for (int k = 0; k < S.sten_L; ++k) {
+        p.off[k] = S.sten_off[k];
+        p.val[k] = S.sten_val[k];
+    }
+    for (int q = 0; q < 256; ++q) {
+        p.pmask[q] = q < S.npat ? S.sten_mask[q] : 0u;
+        p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
+    }
+    return p;
+}
+
+template <int OP, bool ROWS>
+void launch_sten(const Sell& S, const StenArgs& a, cudaStream_t s) {
+    const int grid = blocks_for(S.nrows, 256);
+    const StenParam p = sten_param(S);
+    if (S.sten_L == 7)
+        k_sten<OP, ROWS, 7><<<grid, 256, 0, s>>>(a, p);
+    else if (S.sten_L == 27)
+        k_sten<OP, ROWS, 27><<<grid, 256, 0, s>>>(a, p);
+    else
+        k_sten<OP, ROWS, 0><<<grid, 256, 0, s>>>(a, p);
+}
+
+template <bool ROWS>
+void launch_sten_dots(const Sell& S, const StenArgs& a, cudaStream_t s) {
+    const int grid = blocks_for(S.nrows, 256);
+    const StenParam p = sten_param(S);
+    if (S.sten_L == 7)
+        k_sten_dots<ROWS, 7><<<grid, 256, 0, s>>>(a, p);
+    else if (S.sten_L == 27)
+        k_sten_dots<ROWS, 27><<<grid, 256, 0, s>>>(a, p);
+    else
+        k_sten_dots<ROWS, 0><<<grid, 256, 0, s>>>(a, p);
 }
 
 PatArgs pat_args_of(const Sell& S) {
@@ -767,6 +1087,7 @@ SellArgs args_of(const Sell& S) {
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
     a.row0 = static_cast<int>(S.row0);
     a.nslices = S.nslices;
+    a.dcode = S.dcode.empty() ? nullptr : S.dcode.get();
     a.nrows = S.nrows;
     return a;
 }
@@ -774,6 +1095,7 @@ SellArgs args_of(const Sell& S) {
 DictParam<true> dict_param(const Sell& S) {
     DictParam<true> dp;
     for (int i = 0; i < 256; ++i) dp.e[i] = i < static_cast<int>(S.hdict.size()) ? S.hdict[i] : make_ulonglong2(0ULL, 0ULL);
+    for (int i = 0; i < 256; ++i) dp.dg[i] = i < static_cast<int>(S.hdiag.size()) ? S.hdiag[i] : 1.0;
     return dp;
 }
 
@@ -837,8 +1159,13 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
         }
         const int pref = env_int("PAIRAMG_SELL_PAT", -1);  // 1 force PAT, 0 never, -1 auto
         const bool want_pat = pref == 1 || (pref == -1 && maxlen > 16);
+        if (env_flag("PAIRAMG_SELL_STEN", true) && maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
+            if (try_sten(S)) return;
+            if (want_pat) return;
+            reset_pat(S);
+        }
         if (want_pat && try_pattern(M, rows, S, l1, s)) return;
-        if (try_dict(M, rows, S, s)) return;
+        if (try_dict(M, rows, S, l1, s)) return;
         if (pref != 0 && !want_pat && try_pattern(M, rows, S, l1, s)) return;
     }
     S.format = Sell::kPlain;
@@ -868,6 +1195,7 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
 }
 
 double sell_bytes(const Sell& S) {
+    if (S.format == Sell::kSten) return 1.0 * S.nrows + 12.0 * S.sten_L + 12.0 * S.npat;
     if (S.format == Sell::kPat) return 1.0 * S.nrows + 16.0 * S.ptab.size() + 16.0 * S.npat;
     if (S.format == Sell::kDict) return 4.0 * S.padded_nnz + 16.0 * S.ndict;
     return 12.0 * S.padded_nnz + 8.0 * (S.nslices + 1);
@@ -877,7 +1205,7 @@ double sell_op_bytes(const Sell& S, int op) {
     const double n = static_cast<double>(S.nrows), mat = sell_bytes(S);
     switch (op) {
         case kSpmv: return mat + 16.0 * n;                                             // x, y
-        case kJacobi: return mat + (S.format == Sell::kPat ? 24.0 : 32.0) * n;        // x, r, (d), y
+        case kJacobi: return mat + (S.format == Sell::kPat || S.format == Sell::kSten ? 24.0 : S.dcode.empty() ? 32.0 : 25.0) * n;  // x, r, (d), y
         case kResid: return mat + 24.0 * n;                                            // x, r, y
         default: return mat + 32.0 * n;                                                // spmv+dots: w, r, q, v
     }
@@ -885,6 +1213,28 @@ double sell_op_bytes(const Sell& S, int op) {
 
 void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
     if (!S.nslices) return;
+    if (S.format == Sell::kSten) {
+        StenArgs a = sten_args_of(S);
+        a.x = o.x;
+        a.y = o.y;
+        a.r = o.r;
+        a.omega = o.omega;
+        const bool rows = a.rows != nullptr;
+#define PB_STEN(OP)                          \
+    if (rows)                                \
+        launch_sten<OP, true>(S, a, s);      \
+    else                                     \
+        launch_sten<OP, false>(S, a, s);
+        switch (o.op) {
+            case kSpmv: PB_STEN(kSpmv) break;
+            case kJacobi: PB_STEN(kJacobi) break;
+            case kResid: PB_STEN(kResid) break;
+            default: fail(PAIRAMG_INTERNAL, "sell_apply: fused operators need PAIRAMG_SELL_STEN=0 PAIRAMG_SELL_PAT=0");
+        }
+#undef PB_STEN
+        PB_CHECK_LAUNCH();
+        return;
+    }
     if (S.format == Sell::kPat) {
         PatArgs a = pat_args_of(S);
         a.x = o.x;
@@ -908,6 +1258,22 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
         PB_CHECK_LAUNCH();
         return;
     }
+    if (use_win(S, o)) {
+        WinArgs w = win_args_of(S);
+        w.x = o.x;
+        w.y = o.y;
+        w.r = o.r;
+        w.d = o.d;
+        w.omega = o.omega;
+        const DictParam<true> dp = win_param(S);
+        switch (o.op) {
+            case kSpmv: k_win<kSpmv><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
+            case kJacobi: k_win<kJacobi><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
+            default: k_win<kResid><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
+        }
+        PB_CHECK_LAUNCH();
+        return;
+    }
     SellArgs a = args_of(S);
     a.x = o.x;
     a.y = o.y;
@@ -928,6 +1294,8 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
 }
 
 int sell_dots_grid(const Sell& S) {
+    if (S.format == Sell::kSten) return blocks_for(S.nrows, 256);
+    if (S.format == Sell::kDict && S.win.ok) return S.win.grid;
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
@@ -939,6 +1307,20 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
     const int grid = sell_dots_grid(S);
     if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
     const bool rows = !S.rows.empty();
+    if (S.format == Sell::kSten) {
+        StenArgs a = sten_args_of(S);
+        a.x = w;
+        a.y = v;
+        a.r = r;
+        a.q = q;
+        a.partials = partials;
+        if (rows)
+            launch_sten_dots<true>(S, a, s);
+        else
+            launch_sten_dots<false>(S, a, s);
+        PB_CHECK_LAUNCH();
+        return grid;
+    }
     if (S.format == Sell::kPat) {
         PatArgs p = pat_args_of(S);
         p.x = w;
@@ -950,6 +1332,17 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
             k_pat_spmv_dots<true><<<grid, kThreads, 0, s>>>(p);
         else
             k_pat_spmv_dots<false><<<grid, kThreads, 0, s>>>(p);
+        PB_CHECK_LAUNCH();
+        return grid;
+    }
+    if (S.format == Sell::kDict && S.win.ok && aligned16(w) && aligned16(r) && aligned16(q)) {
+        WinArgs wa = win_args_of(S);
+        wa.x = w;
+        wa.y = v;
+        wa.r = r;
+        wa.q = q;
+        wa.partials = partials;
+        k_win<-1><<<grid, kWinThreads, S.win.smem, s>>>(wa, win_param(S));
         PB_CHECK_LAUNCH();
         return grid;
     }

@@ -1,0 +1,143 @@
+// sell_sten.cuh -- STEN storage: every row is an order-preserving subset of
+// ONE main pattern (included by sell.cu, anonymous namespace).
+//
+// Layout: the main pattern's L <= 32 (column - row, value) records and, per
+// row pattern (<= 255, one byte per row as in PAT), the bit mask of main
+// records the row lacks plus its l1 diagonal -- all in the constant bank
+// (kernel parameter).  Per row only the pattern byte is streamed; the l1
+// diagonal stream disappears as in PAT.
+//
+// Why: in DICT/PAT every gather depends on a per-entry code or record load
+// (load -> lookup -> gather -> multiply), so a warp keeps one or two gathers
+// in flight and the sweeps are latency bound at ~45 % of HBM bandwidth.
+// Here a gather address is row + off[k] with off[k] uniform: all L gathers
+// and the row's own operands issue back to back before the first multiply,
+// and the multiplies take their value from uniform registers.  Warps whose
+// rows all carry the full pattern (the interior) skip the mask selects.
+//
+// Exactness: a row's sum runs over its own records in CSR order (the mask
+// only drops absent records; a dropped add leaves the sum untouched), each
+// record's value and column bitwise the CSR one -- the same dadd/dmul chain
+// as spmv_local.  Absent records still load x at row + off (clamped into
+// [0, xlen) in blocks that touch the vector ends) but never use it.
+
+constexpr int kStenMax = 32;
+
+struct StenParam {
+    int off[kStenMax];
+    double val[kStenMax];
+    uint32_t pmask[256];  // main records absent from the pattern (bit k = record k)
+    double pdiag[256];    // l1 diagonal of the pattern (bitwise = l1_diagonal)
+};
+
+struct StenArgs {
+    const uint8_t* pid;  // pattern id per row (indexed by row id)
+    const int32_t* rows;
+    int row0, nrows, xlen;
+    int L;
+    int safe_lo, safe_hi;  // blocks [safe_lo, safe_hi) gather in range without clamping (contiguous rows)
+    const double* x;
+    double* y;
+    const double* r;
+    double omega;
+    const double* q;
+    double* partials;
+};
+
+// Row sum over the main pattern; LL = compile-time record count (0 = generic,
+// runtime a.L <= kStenMax).  EDGE clamps the gather columns into [0, xlen).
+template <int LL, bool EDGE>
+__device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m) {
+    constexpr int N = LL ? LL : kStenMax;
+    double xv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (LL == 0 && k >= a.L) break;
+        int c = row + p.off[k];
+        if (EDGE) c = min(max(c, 0), a.xlen - 1);
+        xv[k] = __ldg(a.x + c);
+    }
+    double sum = 0.0;
+    if (__all_sync(0xffffffffu, m == 0u)) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (LL == 0 && k >= a.L) break;
+            sum = dadd(sum, dmul(p.val[k], xv[k]));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (LL == 0 && k >= a.L) break;
+            const double pr = dmul(p.val[k], xv[k]);
+            if (!((m >> k) & 1u)) sum = dadd(sum, pr);
+        }
+    }
+    return sum;
+}
+
+template <int LL>
+__device__ __forceinline__ double sten_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m, bool edge) {
+    return edge ? sten_row_sum<LL, true>(a, p, row, m) : sten_row_sum<LL, false>(a, p, row, m);
+}
+
+// One thread per row (32-bit indices: a Sell holds < 2^31 rows); rows past
+// nrows recompute the last row and do not store (every lane reaches the
+// warp vote).  The clamp test is per block (uniform).
+template <int OP, bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant__ StenParam p) {
+    const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
+    const bool valid = i < a.nrows;
+    const int ic = valid ? i : a.nrows - 1;
+    const int row = ROWS ? a.rows[ic] : a.row0 + ic;
+    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    const int q = a.pid[row];
+    double ri = 0.0, xi = 0.0;
+    if (OP != kSpmv) ri = a.r[row];
+    if (OP == kJacobi) xi = a.x[row];
+    const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge);
+    if (!valid) return;
+    if (OP == kSpmv)
+        a.y[row] = sum;
+    else if (OP == kResid)
+        a.y[row] = dsub(ri, sum);
+    else
+        a.y[row] = dadd(xi, ddiv(dmul(a.omega, dsub(ri, sum)), p.pdiag[q]));
+}
+
+// v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
+template <bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
+    const bool valid = i < a.nrows;
+    const int ic = valid ? i : a.nrows - 1;
+    const int row = ROWS ? a.rows[ic] : a.row0 + ic;
+    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    const int q = a.pid[row];
+    const double wi = a.x[row], rr = a.r[row], qq = a.q[row];
+    const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge);
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (valid) {
+        a.y[row] = sum;
+        sa = dmul(wi, rr);
+        sb = dmul(wi, sum);
+        sg = dmul(wi, qq);
+    }
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    __shared__ double red[3][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int k = 0; k < 8; ++k) acc = dadd(acc, red[threadIdx.x][k]);
+        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}

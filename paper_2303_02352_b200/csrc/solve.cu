@@ -412,7 +412,10 @@ static SellOpArgs jacobi_args(int op, const double* x, double* y, const double* 
     return o;
 }
 
-bool Solver::fusable(int k) { return fuse && !lvl(k).A.halo.has_traffic(); }
+bool Solver::fusable(int k) {
+    const Level& L = lvl(k);
+    return fuse && !L.A.halo.has_traffic() && (L.sell_all.format == Sell::kDict || L.sell_all.format == Sell::kPlain);
+}
 
 void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
                     bool l0) {

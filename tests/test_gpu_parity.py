@@ -84,9 +84,10 @@ def test_spmv_and_vcycle_bitexact(runtime, case):
 
 
 FORMATS = {  # solve-time storage of every level (csrc/sell.cu): all must be bit-identical
-    "pat": {"PAIRAMG_SELL_PAT": "1"},
-    "dict": {"PAIRAMG_SELL_PAT": "0"},
-    "plain": {"PAIRAMG_SELL_DICT": "0"},
+    "sten": {"PAIRAMG_SELL_STEN": "1"},
+    "pat": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "1"},
+    "dict": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0"},
+    "plain": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_DICT": "0"},
 }
 
 
@@ -96,6 +97,7 @@ def test_storage_formats_bitexact(runtime, case, fmt, monkeypatch):
     for k, v in FORMATS[fmt].items():
         monkeypatch.setenv(k, v)
     orc, s = build_pair(runtime, *case)
+    assert s.level_storage(0) == fmt
     rng = np.random.default_rng(11)
     for k in range(orc.num_levels):
         x = rng.standard_normal(orc.level_size(k)[0])
