@@ -910,8 +910,7 @@ bool try_sten(Sell& S) {
     S.sten_offmax = static_cast<int>(omax);
     S.sten_mask = mask;
     S.ptab.reset();
-    S.pmeta.reset();
-    S.pdiag.reset();
+    S.pmeta.reset();  // pdiag stays: the FCG update reads it (fused zero-start)
     S.format = Sell::kSten;
     return true;
 }
@@ -1022,6 +1021,8 @@ StenArgs sten_args_of(const Sell& S) {
     }
     a.safe_lo = static_cast<int>(lo);
     a.safe_hi = static_cast<int>(hi);
+    a.pf_blocks = env_int("PAIRAMG_PF_BLOCKS", 16 * kSmCount);
+    a.offmax = S.sten_offmax;
     return a;
 }
 

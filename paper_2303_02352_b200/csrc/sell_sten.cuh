@@ -36,6 +36,8 @@ struct StenArgs {
     int row0, nrows, xlen;
     int L;
     int safe_lo, safe_hi;  // blocks [safe_lo, safe_hi) gather in range without clamping (contiguous rows)
+    int pf_blocks;         // L2 prefetch distance in blocks (0 = off; contiguous rows only)
+    int offmax;
     const double* x;
     double* y;
     const double* r;
@@ -80,6 +82,26 @@ __device__ __forceinline__ double sten_sum(const StenArgs& a, const StenParam& p
     return edge ? sten_row_sum<LL, true>(a, p, row, m) : sten_row_sum<LL, false>(a, p, row, m);
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Streams the block pf_blocks ahead will touch first (its r rows, pattern
+// bytes and the x rows its largest offset reaches) into L2, so those first
+// touches overlap this block's latency instead of starting when it runs.
+template <int OP>
+__device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* own) {
+    if (a.pf_blocks <= 0 || threadIdx.x != 0) return;
+    const int b = static_cast<int>(blockIdx.x) + a.pf_blocks;
+    const int64_t first = static_cast<int64_t>(b) * 256;
+    if (first >= a.nrows) return;
+    const int64_t row = a.row0 + first;
+    const int64_t xr = (row + a.offmax) & ~int64_t(1);
+    if (xr + 256 <= a.xlen) bulk_prefetch_l2(a.x + xr, 2048);
+    if (OP != kSpmv && first + 256 <= a.nrows && !(row & 1)) bulk_prefetch_l2(own + row, 2048);
+    if (first + 256 <= a.nrows && !(row & 15)) bulk_prefetch_l2(a.pid + row, 256);
+}
+
 // One thread per row (32-bit indices: a Sell holds < 2^31 rows); rows past
 // nrows recompute the last row and do not store (every lane reaches the
 // warp vote).  The clamp test is per block (uniform).
@@ -90,6 +112,7 @@ __global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant_
     const int ic = valid ? i : a.nrows - 1;
     const int row = ROWS ? a.rows[ic] : a.row0 + ic;
     const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    if (!ROWS) sten_prefetch<OP>(a, a.r);
     const int q = a.pid[row];
     double ri = 0.0, xi = 0.0;
     if (OP != kSpmv) ri = a.r[row];
@@ -112,6 +135,7 @@ __global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_cons
     const int ic = valid ? i : a.nrows - 1;
     const int row = ROWS ? a.rows[ic] : a.row0 + ic;
     const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    if (!ROWS) sten_prefetch<-1>(a, a.r);
     const int q = a.pid[row];
     const double wi = a.x[row], rr = a.r[row], qq = a.q[row];
     const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge);

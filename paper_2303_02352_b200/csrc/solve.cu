@@ -44,10 +44,22 @@ __global__ void k_prolong(const int32_t* __restrict__ pcol, const double* __rest
 
 // FCG vector updates (Alg. 1 lines 16-19), op order shared with the oracle:
 //   d = w - c d ; q = v - c q ; u = u + a d ; r = r - a q ;  plus |r|^2 partials.
+// ZS: also forms the next V-cycle's level-0 zero-start sweep from the new
+// residual, x1 = (omega*r)/d (cycle.cpp:89-93), while r is in registers; d
+// is the pattern's l1 diagonal (STEN level 0: one byte per row) or the l1
+// array.
+template <bool ZS>
+__device__ __forceinline__ void zs_store(const ZeroStart& z, int64_t i, double rn) {
+    if (!ZS) return;
+    const double di = z.pid ? z.ptab[z.pid[i]] : z.l1[i];
+    z.x[i] = ddiv(dmul(z.omega, rn), di);
+}
+
+template <bool ZS>
 __global__ void __launch_bounds__(kRedThreads)
     k_update(const double* __restrict__ w, double* __restrict__ d, double* __restrict__ u,
              const double* __restrict__ v, double* __restrict__ q, double* __restrict__ r, int64_t n,
-             const FcgState* __restrict__ st, double* __restrict__ partials) {
+             const FcgState* __restrict__ st, double* __restrict__ partials, ZeroStart z) {
     const double c = st->c, a = st->a;
     double rr = 0.0;
     // 16-byte vector accesses (all vectors are 256-byte aligned), scalar tail
@@ -74,6 +86,8 @@ __global__ void __launch_bounds__(kRedThreads)
         q2[i] = qn;
         u2[i] = un;
         r2[i] = rn;
+        zs_store<ZS>(z, 2 * i, rn.x);
+        zs_store<ZS>(z, 2 * i + 1, rn.y);
         rr = dadd(rr, dmul(rn.x, rn.x));
         rr = dadd(rr, dmul(rn.y, rn.y));
     }
@@ -86,6 +100,7 @@ __global__ void __launch_bounds__(kRedThreads)
         u[i] = dadd(u[i], dmul(a, dn));
         const double rn = dsub(r[i], dmul(a, qn));
         r[i] = rn;
+        zs_store<ZS>(z, i, rn);
         rr = dadd(rr, dmul(rn, rn));
     }
     for (int o = 16; o; o >>= 1) rr = dadd(rr, __shfl_down_sync(0xffffffffu, rr, o));
@@ -426,7 +441,10 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
         return;
     }
     int sweep = 0;
-    if (zero_start && nu >= 2 && fusable(k)) {
+    if (zero_start && k == 0 && zs_pending_) {  // x1 already formed by the previous update / the solve prologue
+        zs_pending_ = false;
+        sweep = 1;
+    } else if (zero_start && nu >= 2 && fusable(k)) {
         // sweeps 1+2 in one pass: x1 = (omega*r)/d is formed at every gathered column
         apply(k, jacobi_args(kJacobiZero, nullptr, xc, rhs, L.l1.get(), omega), l0 ? 4 : -1);
         sweep = 2;
@@ -536,9 +554,33 @@ void Solver::reduce_norm_enqueue(bool init) {
     launches_ += 2;
 }
 
+// The level-0 zero-start sweep of every V-cycle is formed by the FCG update
+// that produced its right-hand side (and by the solve prologue for the first).
+bool Solver::zs_fused(const CycleConfig& cc, bool precflag) {
+    const int nu0 = h.nl() == 1 ? cc.coarsest_sweeps : cc.pre_sweeps;
+    return precflag && nu0 >= 1 && !fusable(0) && env_flag("PAIRAMG_ZS_FUSE", true);
+}
+
+ZeroStart Solver::zero_start_args(const CycleConfig& cc) {
+    Level& L0 = *h.levels[0];
+    ZeroStart z{};
+    z.x = L0.x.get();
+    z.omega = cc.relax_weight;
+    const Sell& S = L0.sell_all;
+    if (L0.A.halo.n_halo == 0 && S.format == Sell::kSten && S.nrows == L0.A.n) {
+        z.pid = S.pid.get();
+        z.ptab = S.pdiag.get();
+    } else {
+        z.l1 = L0.l1.get();
+    }
+    return z;
+}
+
 void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     Level& L0 = *h.levels[0];
     double* w = nullptr;
+    const bool zs = zs_fused(cc, precflag);
+    zs_pending_ = zs;
     if (precflag) {
         vcycle_enqueue(0, r_.get(), w, cc);
     } else {
@@ -576,8 +618,13 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     end_time(2);
     reduce_dots_enqueue();
     begin_time(3);
-    k_update<<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(), n_,
-                                                    state_.get(), partials_.get());
+    zs_pending_ = false;
+    if (zs)
+        k_update<true><<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
+                                                              n_, state_.get(), partials_.get(), zero_start_args(cc));
+    else
+        k_update<false><<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
+                                                               n_, state_.get(), partials_.get(), ZeroStart{});
     PB_CHECK_LAUNCH();
     end_time(3);
     launches_ += 1;
@@ -634,6 +681,11 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     PB_CHECK_LAUNCH();
     launches_ += 1;
     reduce_norm_enqueue(true);
+    if (zs_fused(cc, precflag) && n_) {
+        k_zero_start<<<blocks_for(n_, 256), 256, 0, s_>>>(r_.get(), L0.l1.get(), L0.x.get(), n_, cc.relax_weight);
+        PB_CHECK_LAUNCH();
+        launches_ += 1;
+    }
     timing = timing_save;
     PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
     PB_CUDA(cudaStreamSynchronize(s_));

@@ -10,6 +10,15 @@
 
 namespace pb {
 
+// Fused level-0 zero-start sweep written by the FCG update (solve.cu).
+struct ZeroStart {
+    double* x = nullptr;
+    const uint8_t* pid = nullptr;  // STEN level 0: pattern byte per row ...
+    const double* ptab = nullptr;  // ... and the per-pattern l1 diagonal
+    const double* l1 = nullptr;    // otherwise the l1 array
+    double omega = 1.0;
+};
+
 // Device-resident FCG scalars (Alg. 1 lines 11-15), read once per iteration.
 struct FcgState {
     double alpha, beta, gamma, rho;  // current dots / rho_i
@@ -63,6 +72,9 @@ private:
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
+    bool zs_fused(const CycleConfig& cc, bool precflag);
+    ZeroStart zero_start_args(const CycleConfig& cc);
+    bool zs_pending_ = false;  // level-0 x1 of the next V-cycle is already formed
     void reduce_dots_enqueue();
     void reduce_norm_enqueue(bool init_rr0);
     void ensure_vectors();
