@@ -219,7 +219,8 @@ def config_dict(args, world):
         "unknowns": nx * ny * nz, "stencil": args.stencil, "coarse_size_target": target,
         "aggregation_exponent": 3, "sweeps": "4/4/20 l1-Jacobi", "rtol": 1e-6, "parallelism": part,
         "step": "one full FCG solve to rtol (hierarchy prebuilt)",
-        "l2": "inputs larger than L2 (level-0 matrix alone is > 1 GB)",
+        "l2": "working set larger than L2 (no flush): every level-0 vector is 8*unknowns bytes (134 MB at 256^3 "
+              "vs 126 MB L2) and one FCG iteration streams several GB",
     }
 
 
@@ -314,6 +315,11 @@ def bench_ours(args, rank, world, local_rank):
     kt = [s.kernel_timing(k) for k in range(6)]
     peak, peak_src = measured_peaks()
     li0 = s.level_info(0)
+    fmt0 = s.level_storage(0)
+    sweep_kernel = {"sten": "k_sten<kJacobi> (STEN: one pattern byte per row, uniform offsets/values)",
+                    "pat": "k_pat<kJacobi> (PAT: one pattern byte per row)",
+                    "dict": "k_sell<kJacobi> (DICT: one code byte per entry)",
+                    "plain": "k_sell<kJacobi> (PLAIN SELL-32)"}[fmt0]
     survey_bytes = 12.0 * li0["local_nnz"] + 36.0 * li0["local_rows"]  # SURVEY 8d model: f64 values + int32 columns
     sweep = kt[0]
     sweep_ms = sweep["ms"] / max(sweep["launches"], 1)
@@ -375,8 +381,9 @@ def bench_ours(args, rank, world, local_rank):
         "setup_s": min(setup_times), "setup_breakdown": {k: sstats[k] for k in ("t_matching", "t_spmm", "t_spmm_comm")},
         "levels": sstats["levels"], "opc": sstats["opc"],
         "spmv_gbs": spmv_gbs, "spmv_frac_hbm": spmv_gbs / peak if spmv_gbs else None,
-        "roofline": {"bound": "hbm", "kernel": "level-0 l1-Jacobi sweep (k_sell<kJacobi> on the level's stored format)",
-                     "bytes_model": "stored-format bytes (1-byte DICT codes or PAT ids + x, r, d, y; gathers once)",
+        "roofline": {"bound": "hbm", "kernel": f"level-0 l1-Jacobi sweep, {sweep_kernel}", "storage": fmt0,
+                     "bytes_model": "algorithmic bytes of the stored format: pattern/code bytes + x, r, (l1 d unless "
+                                    "per pattern), y once per launch; gathered neighbours counted once",
                      "survey_model": {"bytes_per_launch": survey_bytes,
                                       "effective_gbs": survey_bytes / (sweep_ms * 1e-3) / 1e9 if sweep["launches"] else None,
                                       "note": "same launches against the SURVEY 8d 12*nnz+36*n model of an uncompressed "
