@@ -223,6 +223,25 @@ pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t 
                                       int64_t nz, int64_t row_begin, int64_t row_end,
                                       int64_t* d_row_ptr, int64_t* d_col, double* d_val);
 
+/* ---- MatrixMarket ingest / distribute (mm_io.cpp:26-110, csr.cpp:24-54,
+ *      dist.cpp:349-363) ---- */
+/* Parse a coordinate MatrixMarket file (real | integer | pattern; general |
+ * symmetric | skew-symmetric; symmetric storage expanded) into a host CSR with
+ * rows sorted by column; duplicates and malformed lines are
+ * PAIRAMG_PARSE_ERROR ("path:line: msg"), an unreadable file PAIRAMG_IO_ERROR. */
+typedef struct pairamg_mm pairamg_mm;
+pairamg_status pairamg_mm_open(const char* path, pairamg_mm** out, int64_t* nrows, int64_t* ncols,
+                               int64_t* nnz);
+/* Rows [row_begin, row_end) as a rank's DistMatrix block (distribute_matrix):
+ * nnz of the block, then local row_ptr (rows+1, from 0), global col, val. */
+pairamg_status pairamg_mm_rows(pairamg_mm* m, int64_t row_begin, int64_t row_end, int64_t* nnz_local);
+pairamg_status pairamg_mm_copy_rows(pairamg_mm* m, int64_t row_begin, int64_t row_end, int64_t* row_ptr,
+                                    int64_t* col, double* val);
+pairamg_status pairamg_mm_close(pairamg_mm* m);
+/* Write "coordinate real general" with %.17g values (write_matrix_market). */
+pairamg_status pairamg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                                const int64_t* col, const double* val);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,13 @@ def _lib(kind: str) -> C.CDLL:
     L.orc_build_weights.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp]
     L.orc_build_weights.restype = i64
     L.orc_match_graph.argtypes = [i64, vp, vp, vp, C.c_int, vp]
+    if hasattr(L, "orc_mm_load"):  # reference checker only
+        L.orc_mm_load.argtypes = [C.c_char_p]
+        L.orc_mm_load.restype = vp
+        L.orc_mm_info.argtypes = [vp, ip, ip, ip]
+        L.orc_mm_export.argtypes = [vp, vp, vp, vp]
+        L.orc_mm_free.argtypes = [vp]
+        L.orc_mm_write.argtypes = [C.c_char_p, i64, i64, vp, vp, vp]
     _loaded[kind] = L
     return L
 
@@ -138,6 +145,36 @@ def match_graph(kind, rp, col, w, mode=0):
     if L.orc_match_graph(len(rp) - 1, _p(rp), _p(col), _p(w), mode, _p(mate)) != 0:
         raise OracleError(L.orc_last_status(), L.orc_last_error().decode())
     return mate
+
+
+def mm_read(path: str):
+    """Reference read_matrix_market (mm_io.cpp:26-88): (nrows, ncols, row_ptr, col, val)."""
+    L = _lib("reference")
+    h = L.orc_mm_load(os.fsencode(path))
+    if not h:
+        raise OracleError(L.orc_last_status(), L.orc_last_error().decode())
+    try:
+        n, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        L.orc_mm_info(h, C.byref(n), C.byref(nc), C.byref(nz))
+        rp = np.empty(n.value + 1, np.int64)
+        ci = np.empty(nz.value, np.int64)
+        va = np.empty(nz.value, np.float64)
+        L.orc_mm_export(h, _p(rp), _p(ci), _p(va))
+    finally:
+        L.orc_mm_free(h)
+    return n.value, nc.value, rp, ci, va
+
+
+def mm_write(path: str, row_ptr, col, val, ncols=None):
+    """Reference write_matrix_market (mm_io.cpp:90-110)."""
+    L = _lib("reference")
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col, np.int64)
+    va = np.ascontiguousarray(val, np.float64)
+    n = len(rp) - 1
+    rc = L.orc_mm_write(os.fsencode(path), n, n if ncols is None else ncols, _p(rp), _p(ci), _p(va))
+    if rc:
+        raise OracleError(rc, L.orc_last_error().decode())
 
 
 class Oracle:

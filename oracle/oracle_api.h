@@ -102,6 +102,17 @@ int64_t orc_build_weights(int64_t n, const int64_t* rp, const int64_t* col, cons
 int orc_match_graph(int64_t n, const int64_t* rp, const int64_t* col, const double* w, int mode,
                     int64_t* mate);
 
+/* MatrixMarket (reference checker only: read_matrix_market, mm_io.cpp:26-88,
+ * through the reference's own CsrMatrix::from_triplets).  orc_mm_load returns
+ * NULL on error (orc_last_status / orc_last_error). */
+void* orc_mm_load(const char* path);
+void orc_mm_info(void* m, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+void orc_mm_export(void* m, int64_t* row_ptr, int64_t* col, double* val);
+void orc_mm_free(void* m);
+/* write_matrix_market (mm_io.cpp:90-110) of a CSR. */
+int orc_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int64_t* col,
+                 const double* val);
+
 /* y = A^k x (global vectors). */
 int orc_spmv(void* h, int level, const double* x, double* y);
 /* x = B r, one V-cycle from level 0 (global vectors). */

@@ -24,6 +24,7 @@
 #include "pairamg/amg.hpp"
 #include "pairamg/cycle.hpp"
 #include "pairamg/dist.hpp"
+#include "pairamg/mm_io.hpp"
 
 #include "oracle_api.h"
 
@@ -511,6 +512,40 @@ int orc_solve(void* h, const double* b, double* u, double* hist, int hist_cap, i
         if (hist)
             for (int i = 0; i < hist_cap && i < static_cast<int>(history.size()); ++i)
                 hist[i] = history[i];
+    });
+}
+
+
+void* orc_mm_load(const char* path) {
+    CsrMatrix* out = nullptr;
+    guarded([&] { out = new CsrMatrix(read_matrix_market(std::string(path))); });
+    return out;
+}
+
+void orc_mm_info(void* m, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    const CsrMatrix& A = *static_cast<CsrMatrix*>(m);
+    *nrows = A.nrows;
+    *ncols = A.ncols;
+    *nnz = static_cast<int64_t>(A.col_idx.size());
+}
+
+void orc_mm_export(void* m, int64_t* row_ptr, int64_t* col, double* val) {
+    const CsrMatrix& A = *static_cast<CsrMatrix*>(m);
+    std::memcpy(row_ptr, A.row_ptr.data(), 8 * A.row_ptr.size());
+    std::memcpy(col, A.col_idx.data(), 8 * A.col_idx.size());
+    std::memcpy(val, A.values.data(), 8 * A.values.size());
+}
+
+void orc_mm_free(void* m) { delete static_cast<CsrMatrix*>(m); }
+
+int orc_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int64_t* col,
+                 const double* val) {
+    return guarded([&] {
+        CsrMatrix A(nrows, ncols);
+        A.row_ptr.assign(row_ptr, row_ptr + nrows + 1);
+        A.col_idx.assign(col, col + row_ptr[nrows]);
+        A.values.assign(val, val + row_ptr[nrows]);
+        write_matrix_market(std::string(path), A);
     });
 }
 

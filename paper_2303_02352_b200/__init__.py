@@ -34,7 +34,8 @@ EXPORTS = [
     "pairamg_prolongator_export", "pairamg_num_matchings", "pairamg_matching_export",
     "pairamg_get_setup_stats", "pairamg_set_kernel_timing", "pairamg_kernel_timing", "pairamg_launch_count",
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
-    "pairamg_match_graph",
+    "pairamg_match_graph", "pairamg_mm_open", "pairamg_mm_rows", "pairamg_mm_copy_rows", "pairamg_mm_close",
+    "pairamg_mm_write",
 ]
 
 
@@ -141,6 +142,11 @@ def lib() -> C.CDLL:
         "pairamg_poisson_host": ([C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
         "pairamg_poisson_device": ([vp, C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
         "pairamg_match_graph": ([vp, i64, vp, vp, vp, vp], st),
+        "pairamg_mm_open": ([C.c_char_p, C.POINTER(vp), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
+        "pairamg_mm_rows": ([vp, i64, i64, C.POINTER(i64)], st),
+        "pairamg_mm_copy_rows": ([vp, i64, i64, vp, vp, vp], st),
+        "pairamg_mm_close": ([vp], st),
+        "pairamg_mm_write": ([C.c_char_p, i64, i64, vp, vp, vp], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -169,6 +175,36 @@ def unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().pairamg_comm_unique_id(buf))
     return bytes(buf)
+
+
+def read_matrix_market(path: str, row_begin: int = 0, row_end: int | None = None):
+    """MatrixMarket file -> (nrows, ncols, row_ptr, col, val) of rows
+    [row_begin, row_end) (read_matrix_market + distribute_matrix, mm_io.cpp:26-110,
+    dist.cpp:349-363): local row_ptr from 0, global ascending columns."""
+    L = lib()
+    h = C.c_void_p()
+    n, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(L.pairamg_mm_open(os.fsencode(path), C.byref(h), C.byref(n), C.byref(nc), C.byref(nz)))
+    try:
+        e = n.value if row_end is None else row_end
+        k = C.c_int64()
+        _check(L.pairamg_mm_rows(h, row_begin, e, C.byref(k)))
+        rp = np.empty(max(e - row_begin, 0) + 1, np.int64)
+        ci = np.empty(k.value, np.int64)
+        va = np.empty(k.value, np.float64)
+        _check(L.pairamg_mm_copy_rows(h, row_begin, e, _ptr(rp), _ptr(ci), _ptr(va)))
+    finally:
+        L.pairamg_mm_close(h)
+    return n.value, nc.value, rp, ci, va
+
+
+def write_matrix_market(path: str, row_ptr, col, val, ncols: int | None = None) -> None:
+    """coordinate real general, %.17g values (write_matrix_market, mm_io.cpp:90-110)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col, np.int64)
+    va = np.ascontiguousarray(val, np.float64)
+    n = len(rp) - 1
+    _check(lib().pairamg_mm_write(os.fsencode(path), n, n if ncols is None else ncols, _ptr(rp), _ptr(ci), _ptr(va)))
 
 
 def poisson(stencil: int, nx: int, ny: int, nz: int, row_begin: int = 0, row_end: int | None = None):

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 
+#include "mmio.cuh"
 #include "pairamg_b200.h"
 #include "solver.cuh"
 
@@ -550,6 +551,70 @@ pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t 
         if (m) k_poisson_fill<<<pb::blocks_for(m, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp, d_col, d_val);
         PB_CHECK_LAUNCH();
         PB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"
+
+// ---- MatrixMarket -----------------------------------------------------------
+
+struct pairamg_mm {
+    pb::HostCsr A;
+};
+
+namespace {
+void mm_block(pairamg_mm* m, int64_t b, int64_t e) {
+    if (!m) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null matrix handle");
+    if (b < 0 || e < b || e > m->A.nrows)
+        pb::fail(PAIRAMG_CONTRACT_VIOLATION, "distribute_matrix: row block outside the matrix");
+}
+}  // namespace
+
+extern "C" {
+
+pairamg_status pairamg_mm_open(const char* path, pairamg_mm** out, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    return guarded([&] {
+        if (!path || !out) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null path/out");
+        *out = nullptr;
+        auto m = std::make_unique<pairamg_mm>();
+        m->A = pb::read_matrix_market(path);
+        if (nrows) *nrows = m->A.nrows;
+        if (ncols) *ncols = m->A.ncols;
+        if (nnz) *nnz = static_cast<int64_t>(m->A.col.size());
+        *out = m.release();
+    });
+}
+
+pairamg_status pairamg_mm_rows(pairamg_mm* m, int64_t b, int64_t e, int64_t* nnz_local) {
+    return guarded([&] {
+        mm_block(m, b, e);
+        if (nnz_local) *nnz_local = m->A.row_ptr[static_cast<size_t>(e)] - m->A.row_ptr[static_cast<size_t>(b)];
+    });
+}
+
+pairamg_status pairamg_mm_copy_rows(pairamg_mm* m, int64_t b, int64_t e, int64_t* row_ptr, int64_t* col, double* val) {
+    return guarded([&] {
+        mm_block(m, b, e);
+        const int64_t base = m->A.row_ptr[static_cast<size_t>(b)];
+        const int64_t end = m->A.row_ptr[static_cast<size_t>(e)];
+        if (row_ptr)
+            for (int64_t i = 0; i <= e - b; ++i) row_ptr[i] = m->A.row_ptr[static_cast<size_t>(b + i)] - base;
+        if (col) std::memcpy(col, m->A.col.data() + base, 8 * static_cast<size_t>(end - base));
+        if (val) std::memcpy(val, m->A.val.data() + base, 8 * static_cast<size_t>(end - base));
+    });
+}
+
+pairamg_status pairamg_mm_close(pairamg_mm* m) {
+    delete m;
+    return PAIRAMG_OK;
+}
+
+pairamg_status pairamg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                                const int64_t* col, const double* val) {
+    return guarded([&] {
+        if (!path || nrows < 0 || ncols < 0 || (nrows > 0 && (!row_ptr || ((!col || !val) && row_ptr[nrows] > 0))))
+            pb::fail(PAIRAMG_INVALID_ARGUMENT, "mm_write: bad arguments");
+        pb::write_matrix_market(path, nrows, ncols, row_ptr, col, val);
     });
 }
 
