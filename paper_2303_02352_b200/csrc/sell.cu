@@ -1026,6 +1026,9 @@ StenArgs sten_args_of(const Sell& S) {
     return a;
 }
 
+// The fixed-length kernels take the row's own x from record L/2.
+bool sten_center(const Sell& S) { return S.sten_L > 0 && S.sten_off[static_cast<size_t>(S.sten_L / 2)] == 0; }
+
 StenParam sten_param(const Sell& S) {
     StenParam p{};
     for (int k = 0; k < S.sten_L; ++k) {
@@ -1043,9 +1046,9 @@ template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a, cudaStream_t s) {
     const int grid = blocks_for(S.nrows, 256);
     const StenParam p = sten_param(S);
-    if (S.sten_L == 7)
+    if (S.sten_L == 7 && sten_center(S))
         k_sten<OP, ROWS, 7><<<grid, 256, 0, s>>>(a, p);
-    else if (S.sten_L == 27)
+    else if (S.sten_L == 27 && sten_center(S))
         k_sten<OP, ROWS, 27><<<grid, 256, 0, s>>>(a, p);
     else
         k_sten<OP, ROWS, 0><<<grid, 256, 0, s>>>(a, p);
@@ -1055,9 +1058,9 @@ template <bool ROWS>
 void launch_sten_dots(const Sell& S, const StenArgs& a, cudaStream_t s) {
     const int grid = blocks_for(S.nrows, 256);
     const StenParam p = sten_param(S);
-    if (S.sten_L == 7)
+    if (S.sten_L == 7 && sten_center(S))
         k_sten_dots<ROWS, 7><<<grid, 256, 0, s>>>(a, p);
-    else if (S.sten_L == 27)
+    else if (S.sten_L == 27 && sten_center(S))
         k_sten_dots<ROWS, 27><<<grid, 256, 0, s>>>(a, p);
     else
         k_sten_dots<ROWS, 0><<<grid, 256, 0, s>>>(a, p);
