@@ -31,6 +31,9 @@ struct Level {
     DBuf<int64_t> rrp;   // R = P^T: local coarse rows -> local fine rows ascending
     DBuf<int32_t> rcol;
     DBuf<double> rval;
+    // solve-time byte codes of pval / rval (<= 256 distinct values each)
+    DBuf<uint8_t> pcode, rcode;
+    std::vector<double> ptab, rtab;
     // solve-time layout
     Sell sell_all;           // all rows (no halo)
     Sell sell_int, sell_bnd; // interior / boundary rows (halo present)

@@ -139,6 +139,9 @@ void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s);
 // diagonal bitwise), then DICT, then PLAIN.
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s,
                 bool allow_dict = true, const double* l1 = nullptr);
+// One byte per value into <= 256 distinct values (exact bits); false (and
+// nothing built) when there are more.
+bool build_value_codes(const double* v, int64_t n, DBuf<uint8_t>& code, std::vector<double>& table, cudaStream_t s);
 double sell_bytes(const Sell& S);               // stored matrix bytes of the format
 double sell_op_bytes(const Sell& S, int op);    // algorithmic bytes of one launch (op, or -1 = spmv+dots)
 // l1_diagonal_dist (cycle.cpp:55-75); throws singular_smoother.

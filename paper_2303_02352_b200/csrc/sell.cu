@@ -608,6 +608,26 @@ __global__ void k_diag_fill(const double* __restrict__ l1, const int32_t* __rest
     dcode[sr] = static_cast<uint8_t>(c);
 }
 
+// Generic value codes (transfer operators): key (0, value bits).
+__global__ void k_val_insert(const double* __restrict__ v, int64_t n, ull* table, unsigned* count, int* overflow) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n || *reinterpret_cast<volatile int*>(overflow)) return;
+    table_find(table, 0, static_cast<ull>(__double_as_longlong(v[i])), true, count, overflow);
+}
+
+__global__ void k_val_fill(const double* __restrict__ v, int64_t n, ull* table, const int* __restrict__ slot_code,
+                           uint8_t* __restrict__ code, int* bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int slot = table_find(table, 0, static_cast<ull>(__double_as_longlong(v[i])), false, nullptr, nullptr);
+    const int c = slot < 0 ? -1 : slot_code[slot];
+    if (c < 0) {
+        atomicExch(bad, 1);
+        return;
+    }
+    code[i] = static_cast<uint8_t>(c);
+}
+
 template <typename F>
 void cub_call(F&& f, cudaStream_t s) {
     size_t bytes = 0;
@@ -1124,6 +1144,51 @@ void launch_op(const Sell& S, const SellArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool build_value_codes(const double* v, int64_t n, DBuf<uint8_t>& code, std::vector<double>& table, cudaStream_t s) {
+    code.reset();
+    table.clear();
+    if (n <= 0) return false;
+    DBuf<ull> tab(2 * kTableCap, s);
+    DBuf<unsigned> cnt(1, s);
+    DBuf<int> flags(2, s);
+    cnt.zero(s);
+    flags.zero(s);
+    k_table_init<<<kTableCap / 256, 256, 0, s>>>(tab.get());
+    k_val_insert<<<blocks_for(n, 256), 256, 0, s>>>(v, n, tab.get(), cnt.get(), flags.get());
+    PB_CHECK_LAUNCH();
+    int over = 0;
+    std::vector<ull> h(2 * kTableCap);
+    PB_CUDA(cudaMemcpyAsync(&over, flags.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaMemcpyAsync(h.data(), tab.get(), 16 * kTableCap, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (over) return false;
+    std::vector<std::pair<ull, int>> vals;
+    for (int i = 0; i < kTableCap; ++i)
+        if (!(h[2 * i] == kEmptyLo && h[2 * i + 1] == 0)) vals.push_back({h[2 * i + 1], i});
+    if (vals.empty() || vals.size() > 256) return false;
+    std::sort(vals.begin(), vals.end());
+    std::vector<int> slot_code(kTableCap, -1);
+    table.assign(vals.size(), 0.0);
+    for (size_t c = 0; c < vals.size(); ++c) {
+        slot_code[vals[c].second] = static_cast<int>(c);
+        std::memcpy(&table[c], &vals[c].first, 8);
+    }
+    DBuf<int> dsc(kTableCap, s);
+    PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
+    code.alloc(static_cast<size_t>(n), s);
+    k_val_fill<<<blocks_for(n, 256), 256, 0, s>>>(v, n, tab.get(), dsc.get(), code.get(), flags.get() + 1);
+    PB_CHECK_LAUNCH();
+    int bad = 0;
+    PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (bad) {
+        code.reset();
+        table.clear();
+        return false;
+    }
+    return true;
+}
 
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict,
                 const double* l1) {

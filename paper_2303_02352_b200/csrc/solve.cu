@@ -42,6 +42,35 @@ __global__ void k_prolong(const int32_t* __restrict__ pcol, const double* __rest
     if (i < n) x[i] = dadd(x[i], dmul(pval[i], e[pcol[i]]));
 }
 
+// Same two operators with the transfer values as byte codes into a table of
+// <= 256 distinct values (kernel parameter): 7 fewer bytes per fine row.
+struct CodeTab {
+    double v[256];
+};
+
+__global__ void k_restrict_c(const int64_t* __restrict__ rrp, const int32_t* __restrict__ rcol,
+                             const uint8_t* __restrict__ rcode, const __grid_constant__ CodeTab t,
+                             const double* __restrict__ res, double* __restrict__ rc, int64_t nc) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double s = 0.0;
+    for (int64_t k = rrp[c]; k < rrp[c + 1]; ++k) s = dadd(s, dmul(t.v[rcode[k]], res[rcol[k]]));
+    rc[c] = s;
+}
+
+__global__ void k_prolong_c(const int32_t* __restrict__ pcol, const uint8_t* __restrict__ pcode,
+                            const __grid_constant__ CodeTab t, const double* __restrict__ e, double* __restrict__ x,
+                            int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = dadd(x[i], dmul(t.v[pcode[i]], e[pcol[i]]));
+}
+
+CodeTab code_tab(const std::vector<double>& v) {
+    CodeTab t{};
+    for (size_t i = 0; i < v.size() && i < 256; ++i) t.v[i] = v[i];
+    return t;
+}
+
 // FCG vector updates (Alg. 1 lines 16-19), op order shared with the oracle:
 //   d = w - c d ; q = v - c q ; u = u + a d ; r = r - a q ;  plus |r|^2 partials.
 // ZS: also forms the next V-cycle's level-0 zero-start sweep from the new
@@ -303,6 +332,15 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
     destroy_graph();
     ready = false;
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
+    if (env_flag("PAIRAMG_TRANSFER_CODES", true)) {
+        auto codes = [&](Level& L) {
+            if (L.pval.empty()) return;
+            build_value_codes(L.pval.get(), static_cast<int64_t>(L.pval.size()), L.pcode, L.ptab, s_);
+            build_value_codes(L.rval.get(), static_cast<int64_t>(L.rval.size()), L.rcode, L.rtab, s_);
+        };
+        for (int k = 1; k < h.nl(); ++k) codes(*h.levels[k]);
+        for (auto& R : h.rep) codes(*R);
+    }
     ensure_vectors();
     ready = true;
 }
@@ -485,8 +523,12 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     const bool gather = h.rep_level >= 0 && k + 1 == h.rep_level;
     Level& T = gather ? *h.levels[k + 1] : lvl(k + 1);
     Level& C = lvl(k + 1);
-    if (T.A.n) k_restrict<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rval.get(),
-                                                                    L.res.get(), T.rhs.get(), T.A.n);
+    if (T.A.n && !T.rcode.empty())
+        k_restrict_c<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rcode.get(),
+                                                             code_tab(T.rtab), L.res.get(), T.rhs.get(), T.A.n);
+    else if (T.A.n)
+        k_restrict<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rval.get(), L.res.get(),
+                                                           T.rhs.get(), T.A.n);
     PB_CHECK_LAUNCH();
     launches_ += 1;
     if (gather) {  // one padded allgather of the restricted rhs, then redundant coarse levels
@@ -508,7 +550,11 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         std::swap(xc, xo);
         --post;
     } else {
-        if (L.A.n) k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pval.get(), e, xc, L.A.n);
+        if (L.A.n && !T.pcode.empty())
+            k_prolong_c<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pcode.get(), code_tab(T.ptab), e, xc,
+                                                                L.A.n);
+        else if (L.A.n)
+            k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pval.get(), e, xc, L.A.n);
         PB_CHECK_LAUNCH();
         launches_ += 1;
     }
