@@ -698,7 +698,9 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     ktime[0].bytes_per_launch = op_bytes(kJacobi);            // x, r, (d) read; y written
     ktime[1].bytes_per_launch = op_bytes(kResid);             // x, r read; y written
     ktime[2].bytes_per_launch = op_bytes(-1);                 // w, r, q read; v written
-    ktime[3].bytes_per_launch = 80.0 * n0;                    // 6 vectors read, 4 written
+    // 6 vectors read, 4 written; + the fused zero-start: pattern byte (or l1) read, x1 written
+    const bool zs = zs_fused(cc, precflag);
+    ktime[3].bytes_per_launch = (80.0 + (zs ? (zero_start_args(cc).pid ? 9.0 : 16.0) : 0.0)) * n0;
     ktime[4].bytes_per_launch = mat + 24.0 * n0;              // r, d read; y written
     ktime[5].bytes_per_launch = mat + 44.0 * n0 + 8.0 * nc1;  // x, p, pcol, r, d read, e; y written
 
