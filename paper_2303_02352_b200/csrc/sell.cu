@@ -1021,7 +1021,7 @@ bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double*
     return true;
 }
 
-StenArgs sten_args_of(const Sell& S) {
+StenArgs sten_args_of(const Sell& S, int block_rows = 256) {
     StenArgs a{};
     a.pid = S.pid.get();
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
@@ -1031,17 +1031,17 @@ StenArgs sten_args_of(const Sell& S) {
     a.L = S.sten_L;
     // blocks whose rows r all satisfy r + offmin >= 0 and r + offmax < xlen
     // (first and last row grow with the block index: both tests are monotone)
-    const int64_t nb = (S.nrows + 255) / 256;
+    const int64_t B = block_rows, nb = (S.nrows + B - 1) / B;
     int64_t lo = 0, hi = 0;
     if (S.rows.empty() && nb > 0) {
-        auto last = [&](int64_t b) { return S.row0 + std::min<int64_t>(256 * b + 255, S.nrows - 1); };
-        while (lo < nb && S.row0 + 256 * lo + S.sten_offmin < 0) ++lo;
+        auto last = [&](int64_t b) { return S.row0 + std::min<int64_t>(B * b + B - 1, S.nrows - 1); };
+        while (lo < nb && S.row0 + B * lo + S.sten_offmin < 0) ++lo;
         hi = nb;
         while (hi > lo && last(hi - 1) + S.sten_offmax > S.xlen - 1) --hi;
     }
     a.safe_lo = static_cast<int>(lo);
     a.safe_hi = static_cast<int>(hi);
-    a.pf_blocks = env_int("PAIRAMG_PF_BLOCKS", 16 * kSmCount);
+    a.pf_blocks = env_int("PAIRAMG_PF_BLOCKS", 16 * kSmCount) * 256 / block_rows;
     a.offmax = S.sten_offmax;
     return a;
 }
@@ -1062,10 +1062,23 @@ StenParam sten_param(const Sell& S) {
     return p;
 }
 
+// Two rows per thread for the 7-record main pattern (k_sten2): +10% bandwidth.
+bool sten_rpt2(const Sell& S) { return S.sten_L == 7 && sten_center(S) && env_int("PAIRAMG_STEN_RPT", 2) == 2; }
+
 template <int OP, bool ROWS>
-void launch_sten(const Sell& S, const StenArgs& a, cudaStream_t s) {
-    const int grid = blocks_for(S.nrows, 256);
+void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
     const StenParam p = sten_param(S);
+    if (sten_rpt2(S)) {
+        StenArgs a = sten_args_of(S, 512);
+        a.x = a0.x;
+        a.y = a0.y;
+        a.r = a0.r;
+        a.omega = a0.omega;
+        k_sten2<OP, ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        return;
+    }
+    const StenArgs& a = a0;
+    const int grid = blocks_for(S.nrows, 256);
     if (S.sten_L == 7 && sten_center(S))
         k_sten<OP, ROWS, 7><<<grid, 256, 0, s>>>(a, p);
     else if (S.sten_L == 27 && sten_center(S))
@@ -1075,9 +1088,20 @@ void launch_sten(const Sell& S, const StenArgs& a, cudaStream_t s) {
 }
 
 template <bool ROWS>
-void launch_sten_dots(const Sell& S, const StenArgs& a, cudaStream_t s) {
-    const int grid = blocks_for(S.nrows, 256);
+void launch_sten_dots(const Sell& S, const StenArgs& a0, cudaStream_t s) {
     const StenParam p = sten_param(S);
+    if (sten_rpt2(S)) {
+        StenArgs a = sten_args_of(S, 512);
+        a.x = a0.x;
+        a.y = a0.y;
+        a.r = a0.r;
+        a.q = a0.q;
+        a.partials = a0.partials;
+        k_sten2_dots<ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        return;
+    }
+    const StenArgs& a = a0;
+    const int grid = blocks_for(S.nrows, 256);
     if (S.sten_L == 7 && sten_center(S))
         k_sten_dots<ROWS, 7><<<grid, 256, 0, s>>>(a, p);
     else if (S.sten_L == 27 && sten_center(S))
@@ -1363,7 +1387,7 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
 }
 
 int sell_dots_grid(const Sell& S) {
-    if (S.format == Sell::kSten) return blocks_for(S.nrows, 256);
+    if (S.format == Sell::kSten) return blocks_for(S.nrows, sten_rpt2(S) ? 512 : 256);
     if (S.format == Sell::kDict && S.win.ok) return S.win.grid;
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;

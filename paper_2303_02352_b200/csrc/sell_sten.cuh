@@ -94,17 +94,17 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
 // Streams the block pf_blocks ahead will touch first (its r rows, pattern
 // bytes and the x rows its largest offset reaches) into L2, so those first
 // touches overlap this block's latency instead of starting when it runs.
-template <int OP>
+template <int OP, int BR = 256>
 __device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* own) {
     if (a.pf_blocks <= 0 || threadIdx.x != 0) return;
     const int b = static_cast<int>(blockIdx.x) + a.pf_blocks;
-    const int64_t first = static_cast<int64_t>(b) * 256;
+    const int64_t first = static_cast<int64_t>(b) * BR;
     if (first >= a.nrows) return;
     const int64_t row = a.row0 + first;
     const int64_t xr = (row + a.offmax) & ~int64_t(1);
-    if (xr + 256 <= a.xlen) bulk_prefetch_l2(a.x + xr, 2048);
-    if (OP != kSpmv && first + 256 <= a.nrows && !(row & 1)) bulk_prefetch_l2(own + row, 2048);
-    if (first + 256 <= a.nrows && !(row & 15)) bulk_prefetch_l2(a.pid + row, 256);
+    if (xr + BR <= a.xlen) bulk_prefetch_l2(a.x + xr, 8 * BR);
+    if (OP != kSpmv && first + BR <= a.nrows && !(row & 1)) bulk_prefetch_l2(own + row, 8 * BR);
+    if (first + BR <= a.nrows && !(row & 15)) bulk_prefetch_l2(a.pid + row, BR);
 }
 
 // One thread per row (32-bit indices: a Sell holds < 2^31 rows); rows past
@@ -132,6 +132,79 @@ __global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant_
         const double t = dsub(ri, sum);  // omega = 1 (the paper's setting) multiplies exactly: skip it
         a.y[row] = dadd(xi, ddiv(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q]));
     }
+}
+
+// Two rows per thread (rows t and t + 256 of a 512-row block), every load of
+// both rows issued before the first multiply: twice the gathers in flight
+// per warp at a register cost that still leaves 40+ warps per SM (LL = 7).
+template <int LL, bool EDGE>
+__device__ __forceinline__ void sten_load(const StenArgs& a, const StenParam& p, int row, double (&xv)[LL]) {
+#pragma unroll
+    for (int k = 0; k < LL; ++k) {
+        int c = row + p.off[k];
+        if (EDGE) c = min(max(c, 0), a.xlen - 1);
+        xv[k] = __ldg(a.x + c);
+    }
+}
+
+template <int LL>
+__device__ __forceinline__ double sten_fold(const StenParam& p, const double (&xv)[LL], uint32_t m) {
+    double sum = 0.0;
+    if (__all_sync(0xffffffffu, m == 0u)) {
+#pragma unroll
+        for (int k = 0; k < LL; ++k) sum = dadd(sum, dmul(p.val[k], xv[k]));
+    } else {
+#pragma unroll
+        for (int k = 0; k < LL; ++k) {
+            const double pr = dmul(p.val[k], xv[k]);
+            if (!((m >> k) & 1u)) sum = dadd(sum, pr);
+        }
+    }
+    return sum;
+}
+
+template <int OP, int LL>
+__device__ __forceinline__ void sten_store(const StenArgs& a, const StenParam& p, int row, int q, double ri,
+                                           double xi, double sum) {
+    if (OP == kSpmv) {
+        a.y[row] = sum;
+    } else if (OP == kResid) {
+        a.y[row] = dsub(ri, sum);
+    } else {
+        const double t = dsub(ri, sum);
+        a.y[row] = dadd(xi, ddiv(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q]));
+    }
+}
+
+template <int OP, bool ROWS, int LL, bool EDGE>
+__device__ __forceinline__ void sten2_body(const StenArgs& a, const StenParam& p, int ia, int ib) {
+    const bool va = ia < a.nrows, vb = ib < a.nrows;
+    const int ra = ROWS ? a.rows[va ? ia : a.nrows - 1] : a.row0 + (va ? ia : a.nrows - 1);
+    const int rb = ROWS ? a.rows[vb ? ib : a.nrows - 1] : a.row0 + (vb ? ib : a.nrows - 1);
+    const int qa = a.pid[ra], qb = a.pid[rb];
+    double ria = 0.0, rib = 0.0;
+    if (OP != kSpmv) {
+        ria = a.r[ra];
+        rib = a.r[rb];
+    }
+    double xa[LL], xb[LL];
+    sten_load<LL, EDGE>(a, p, ra, xa);
+    sten_load<LL, EDGE>(a, p, rb, xb);
+    const double sa = sten_fold<LL>(p, xa, p.pmask[qa]);
+    const double sb = sten_fold<LL>(p, xb, p.pmask[qb]);
+    if (va) sten_store<OP, LL>(a, p, ra, qa, ria, xa[LL / 2], sa);
+    if (vb) sten_store<OP, LL>(a, p, rb, qb, rib, xb[LL / 2], sb);
+}
+
+template <int OP, bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant__ StenParam p) {
+    const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
+    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    if (!ROWS) sten_prefetch<OP, 512>(a, a.r);
+    if (edge)
+        sten2_body<OP, ROWS, LL, true>(a, p, ia, ia + 256);
+    else
+        sten2_body<OP, ROWS, LL, false>(a, p, ia, ia + 256);
 }
 
 // v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
@@ -173,3 +246,63 @@ __global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_cons
         a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
     }
 }
+
+// Two rows per thread (rows t and t + 256 of a 512-row block), as k_sten2.
+template <bool ROWS, int LL, bool EDGE>
+__device__ __forceinline__ void sten2_dots_body(const StenArgs& a, const StenParam& p, int ia, int ib, double& sa,
+                                                double& sb, double& sg) {
+    const bool va = ia < a.nrows, vb = ib < a.nrows;
+    const int ra = ROWS ? a.rows[va ? ia : a.nrows - 1] : a.row0 + (va ? ia : a.nrows - 1);
+    const int rb = ROWS ? a.rows[vb ? ib : a.nrows - 1] : a.row0 + (vb ? ib : a.nrows - 1);
+    const int qa = a.pid[ra], qb = a.pid[rb];
+    const double rra = a.r[ra], rrb = a.r[rb], qqa = a.q[ra], qqb = a.q[rb];
+    double xa[LL], xb[LL];
+    sten_load<LL, EDGE>(a, p, ra, xa);
+    sten_load<LL, EDGE>(a, p, rb, xb);
+    const double va_ = sten_fold<LL>(p, xa, p.pmask[qa]);
+    const double vb_ = sten_fold<LL>(p, xb, p.pmask[qb]);
+    const double wa = xa[LL / 2], wb = xb[LL / 2];
+    if (va) {
+        a.y[ra] = va_;
+        sa = dmul(wa, rra);
+        sb = dmul(wa, va_);
+        sg = dmul(wa, qqa);
+    }
+    if (vb) {
+        a.y[rb] = vb_;
+        sa = dadd(sa, dmul(wb, rrb));
+        sb = dadd(sb, dmul(wb, vb_));
+        sg = dadd(sg, dmul(wb, qqb));
+    }
+}
+
+template <bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
+    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
+    if (!ROWS) sten_prefetch<-1, 512>(a, a.r);
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (edge)
+        sten2_dots_body<ROWS, LL, true>(a, p, ia, ia + 256, sa, sb, sg);
+    else
+        sten2_dots_body<ROWS, LL, false>(a, p, ia, ia + 256, sa, sb, sg);
+    for (int o = 16; o; o >>= 1) {
+        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
+        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
+        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    }
+    __shared__ double red[3][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = sa;
+        red[1][warp] = sb;
+        red[2][warp] = sg;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double acc = 0.0;
+        for (int k = 0; k < 8; ++k) acc = dadd(acc, red[threadIdx.x][k]);
+        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
+    }
+}
+
