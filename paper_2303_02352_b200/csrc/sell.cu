@@ -1063,7 +1063,12 @@ StenParam sten_param(const Sell& S) {
 }
 
 // Two rows per thread for the 7-record main pattern (k_sten2): +10% bandwidth.
-bool sten_rpt2(const Sell& S) { return S.sten_L == 7 && sten_center(S) && env_int("PAIRAMG_STEN_RPT", 2) == 2; }
+// 27 records: only the SpMV+dots kernel gains (122 vs 132 us; sweeps lose).
+bool sten_rpt2(const Sell& S, bool dots = false) {
+    if (!sten_center(S)) return false;
+    if (S.sten_L == 7) return env_int("PAIRAMG_STEN_RPT", 2) == 2;
+    return S.sten_L == 27 && env_int("PAIRAMG_STEN_RPT27", dots ? 2 : 1) == 2;
+}
 
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
@@ -1074,7 +1079,10 @@ void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
         a.y = a0.y;
         a.r = a0.r;
         a.omega = a0.omega;
-        k_sten2<OP, ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        if (S.sten_L == 7)
+            k_sten2<OP, ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        else
+            k_sten2<OP, ROWS, 27><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
         return;
     }
     const StenArgs& a = a0;
@@ -1090,14 +1098,17 @@ void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
 template <bool ROWS>
 void launch_sten_dots(const Sell& S, const StenArgs& a0, cudaStream_t s) {
     const StenParam p = sten_param(S);
-    if (sten_rpt2(S)) {
+    if (sten_rpt2(S, true)) {
         StenArgs a = sten_args_of(S, 512);
         a.x = a0.x;
         a.y = a0.y;
         a.r = a0.r;
         a.q = a0.q;
         a.partials = a0.partials;
-        k_sten2_dots<ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        if (S.sten_L == 7)
+            k_sten2_dots<ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+        else
+            k_sten2_dots<ROWS, 27><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
         return;
     }
     const StenArgs& a = a0;
@@ -1387,7 +1398,7 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
 }
 
 int sell_dots_grid(const Sell& S) {
-    if (S.format == Sell::kSten) return blocks_for(S.nrows, sten_rpt2(S) ? 512 : 256);
+    if (S.format == Sell::kSten) return blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256);
     if (S.format == Sell::kDict && S.win.ok) return S.win.grid;
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;
