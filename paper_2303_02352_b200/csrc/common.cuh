@@ -108,6 +108,36 @@ private:
 // Exactly rounded FP64 (no contraction), matching the reference objects,
 // which contain no FMA.  The library is also
 // compiled with --fmad=false; these make the intent explicit at call sites.
+// Programmatic dependent launch: solve-path kernels are launched with
+// programmatic stream serialization (launch_k), so a kernel's CTAs can be
+// scheduled while its predecessor drains; every such kernel first lets its own
+// dependents launch, then waits until its predecessor grid has completed and
+// its writes are visible (griddepcontrol; no-ops without the attribute).
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline int pdl_mask() {
+    static const int m = env_int("PAIRAMG_PDL", 15);  // bits: 1 reductions, 2 row kernels, 4 transfers, 8 FCG update
+    return m;
+}
+
+template <int CLASS = 1, typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl_mask() & CLASS) ? 1 : 0;
+    PB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }

@@ -1080,19 +1080,19 @@ void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
         a.r = a0.r;
         a.omega = a0.omega;
         if (S.sten_L == 7)
-            k_sten2<OP, ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+            launch_k<2>(k_sten2<OP, ROWS, 7>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
         else
-            k_sten2<OP, ROWS, 27><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+            launch_k<2>(k_sten2<OP, ROWS, 27>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
         return;
     }
     const StenArgs& a = a0;
     const int grid = blocks_for(S.nrows, 256);
     if (S.sten_L == 7 && sten_center(S))
-        k_sten<OP, ROWS, 7><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten<OP, ROWS, 7>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
-        k_sten<OP, ROWS, 27><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten<OP, ROWS, 27>, grid, 256, 0, s, a, p);
     else
-        k_sten<OP, ROWS, 0><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten<OP, ROWS, 0>, grid, 256, 0, s, a, p);
 }
 
 template <bool ROWS>
@@ -1106,19 +1106,19 @@ void launch_sten_dots(const Sell& S, const StenArgs& a0, cudaStream_t s) {
         a.q = a0.q;
         a.partials = a0.partials;
         if (S.sten_L == 7)
-            k_sten2_dots<ROWS, 7><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+            launch_k<2>(k_sten2_dots<ROWS, 7>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
         else
-            k_sten2_dots<ROWS, 27><<<blocks_for(S.nrows, 512), 256, 0, s>>>(a, p);
+            launch_k<2>(k_sten2_dots<ROWS, 27>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
         return;
     }
     const StenArgs& a = a0;
     const int grid = blocks_for(S.nrows, 256);
     if (S.sten_L == 7 && sten_center(S))
-        k_sten_dots<ROWS, 7><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten_dots<ROWS, 7>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
-        k_sten_dots<ROWS, 27><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten_dots<ROWS, 27>, grid, 256, 0, s, a, p);
     else
-        k_sten_dots<ROWS, 0><<<grid, 256, 0, s>>>(a, p);
+        launch_k<2>(k_sten_dots<ROWS, 0>, grid, 256, 0, s, a, p);
 }
 
 PatArgs pat_args_of(const Sell& S) {

@@ -60,7 +60,7 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenPara
         if (LL == 0 && k >= a.L) break;
         int c = row + p.off[k];
         if (EDGE) c = min(max(c, 0), a.xlen - 1);
-        xv[k] = __ldg(a.x + c);
+        xv[k] = a.x[c];  // coherent load: this kernel may start before x's producer completes (PDL)
     }
     double sum = 0.0;
     if (__all_sync(0xffffffffu, m == 0u)) {
@@ -112,6 +112,7 @@ __device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* o
 // warp vote).  The clamp test is per block (uniform).
 template <int OP, bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
     const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
     const int ic = valid ? i : a.nrows - 1;
@@ -143,7 +144,7 @@ __device__ __forceinline__ void sten_load(const StenArgs& a, const StenParam& p,
     for (int k = 0; k < LL; ++k) {
         int c = row + p.off[k];
         if (EDGE) c = min(max(c, 0), a.xlen - 1);
-        xv[k] = __ldg(a.x + c);
+        xv[k] = a.x[c];  // coherent load: this kernel may start before x's producer completes (PDL)
     }
 }
 
@@ -198,6 +199,7 @@ __device__ __forceinline__ void sten2_body(const StenArgs& a, const StenParam& p
 
 template <int OP, bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
     const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
     const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
     if (!ROWS) sten_prefetch<OP, 512>(a, a.r);
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant
 // v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
 template <bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
     const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
     const int ic = valid ? i : a.nrows - 1;
@@ -278,6 +281,7 @@ __device__ __forceinline__ void sten2_dots_body(const StenArgs& a, const StenPar
 
 template <bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
     const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
     const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
     if (!ROWS) sten_prefetch<-1, 512>(a, a.r);

@@ -18,16 +18,18 @@ namespace {
 constexpr int kRedThreads = 256;
 
 // x = (omega*r)/d : the zero-start sweep (cycle.cpp:89-93)
-__global__ void k_zero_start(const double* __restrict__ r, const double* __restrict__ d,
-                             double* __restrict__ x, int64_t n, double omega) {
+__global__ void k_zero_start(const double* r, const double* d,
+                             double* x, int64_t n, double omega) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = ddiv(dmul(omega, r[i]), d[i]);
 }
 
 // restrict_to_coarse (cycle.cpp:104-115): rc_c = 0.0 + sum R_ci res_i, fine ascending
-__global__ void k_restrict(const int64_t* __restrict__ rrp, const int32_t* __restrict__ rcol,
-                           const double* __restrict__ rval, const double* __restrict__ res,
-                           double* __restrict__ rc, int64_t nc) {
+__global__ void k_restrict(const int64_t* rrp, const int32_t* rcol,
+                           const double* rval, const double* res,
+                           double* rc, int64_t nc) {
+    pdl_begin();
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     double s = 0.0;
@@ -36,8 +38,9 @@ __global__ void k_restrict(const int64_t* __restrict__ rrp, const int32_t* __res
 }
 
 // prolongate_add (cycle.cpp:117-124): x_i = x_i + p_i * e_agg(i)
-__global__ void k_prolong(const int32_t* __restrict__ pcol, const double* __restrict__ pval,
-                          const double* __restrict__ e, double* __restrict__ x, int64_t n) {
+__global__ void k_prolong(const int32_t* pcol, const double* pval,
+                          const double* e, double* x, int64_t n) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = dadd(x[i], dmul(pval[i], e[pcol[i]]));
 }
@@ -48,9 +51,10 @@ struct CodeTab {
     double v[256];
 };
 
-__global__ void k_restrict_c(const int64_t* __restrict__ rrp, const int32_t* __restrict__ rcol,
-                             const uint8_t* __restrict__ rcode, const __grid_constant__ CodeTab t,
-                             const double* __restrict__ res, double* __restrict__ rc, int64_t nc) {
+__global__ void k_restrict_c(const int64_t* rrp, const int32_t* rcol,
+                             const uint8_t* rcode, const __grid_constant__ CodeTab t,
+                             const double* res, double* rc, int64_t nc) {
+    pdl_begin();
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     double s = 0.0;
@@ -58,9 +62,10 @@ __global__ void k_restrict_c(const int64_t* __restrict__ rrp, const int32_t* __r
     rc[c] = s;
 }
 
-__global__ void k_prolong_c(const int32_t* __restrict__ pcol, const uint8_t* __restrict__ pcode,
-                            const __grid_constant__ CodeTab t, const double* __restrict__ e, double* __restrict__ x,
+__global__ void k_prolong_c(const int32_t* pcol, const uint8_t* pcode,
+                            const __grid_constant__ CodeTab t, const double* e, double* x,
                             int64_t n) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = dadd(x[i], dmul(t.v[pcode[i]], e[pcol[i]]));
 }
@@ -86,9 +91,10 @@ __device__ __forceinline__ void zs_store(const ZeroStart& z, int64_t i, double r
 
 template <bool ZS>
 __global__ void __launch_bounds__(kRedThreads)
-    k_update(const double* __restrict__ w, double* __restrict__ d, double* __restrict__ u,
-             const double* __restrict__ v, double* __restrict__ q, double* __restrict__ r, int64_t n,
-             const FcgState* __restrict__ st, double* __restrict__ partials, ZeroStart z) {
+    k_update(const double* w, double* d, double* u,
+             const double* v, double* q, double* r, int64_t n,
+             const FcgState* st, double* partials, ZeroStart z) {
+    pdl_begin();
     const double c = st->c, a = st->a;
     double rr = 0.0;
     // 16-byte vector accesses (all vectors are 256-byte aligned), scalar tail
@@ -145,7 +151,8 @@ __global__ void __launch_bounds__(kRedThreads)
 }
 
 __global__ void __launch_bounds__(kRedThreads)
-    k_norm_partials(const double* __restrict__ r, int64_t n, double* __restrict__ partials) {
+    k_norm_partials(const double* r, int64_t n, double* partials) {
+    pdl_begin();
     double rr = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -164,7 +171,8 @@ __global__ void __launch_bounds__(kRedThreads)
 
 // Fixed-order reduction of G partial K-tuples into out[K] (one block).
 __global__ void __launch_bounds__(kRedThreads)
-    k_reduce(const double* __restrict__ partials, int G, int K, double* __restrict__ out) {
+    k_reduce(const double* partials, int G, int K, double* out) {
+    pdl_begin();
     __shared__ double red[kRedThreads];
     for (int k = 0; k < K; ++k) {
         double s = 0.0;
@@ -185,7 +193,8 @@ constexpr int kStage = 256;
 // First stage for large partial counts: block b reduces the contiguous chunk
 // [b*G/gridDim, (b+1)*G/gridDim) of K-tuples in a fixed order.
 __global__ void __launch_bounds__(kRedThreads)
-    k_reduce_chunks(const double* __restrict__ partials, int G, int K, double* __restrict__ out) {
+    k_reduce_chunks(const double* partials, int G, int K, double* out) {
+    pdl_begin();
     __shared__ double red[kRedThreads];
     const int64_t g0 = static_cast<int64_t>(G) * blockIdx.x / gridDim.x;
     const int64_t g1 = static_cast<int64_t>(G) * (blockIdx.x + 1) / gridDim.x;
@@ -205,7 +214,8 @@ __global__ void __launch_bounds__(kRedThreads)
 
 // Cross-rank sums in rank order (runtime.cpp:388-396), then the FCG scalar
 // recurrences (Alg. 1 lines 4-5, 14; breakdown check SPEC.md:478).
-__global__ void k_fcg_scalars(const double* __restrict__ g, int p, FcgState* __restrict__ st) {
+__global__ void k_fcg_scalars(const double* g, int p, FcgState* st) {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double al = 0.0, be = 0.0, ga = 0.0;
     for (int r = 0; r < p; ++r) {
@@ -232,8 +242,9 @@ __global__ void k_fcg_scalars(const double* __restrict__ g, int p, FcgState* __r
 
 // Device-side stopping test of the graph loop (same operations as the host
 // loop: rel = sqrt(rr)/sqrt(rr0); stop on rel < rtol, max_iters or breakdown).
-__global__ void k_loop_ctl(const FcgState* __restrict__ st, double rtol, int max_iters, double* __restrict__ hist,
+__global__ void k_loop_ctl(const FcgState* st, double rtol, int max_iters, double* hist,
                            cudaGraphConditionalHandle h) {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double rel = ddiv(__dsqrt_rn(st->rr), __dsqrt_rn(st->rr0));
     if (st->it <= max_iters) hist[st->it] = rel;
@@ -241,7 +252,8 @@ __global__ void k_loop_ctl(const FcgState* __restrict__ st, double rtol, int max
     cudaGraphSetConditional(h, stop ? 0u : 1u);
 }
 
-__global__ void k_norm_final(const double* __restrict__ g, int p, FcgState* __restrict__ st, int init) {
+__global__ void k_norm_final(const double* g, int p, FcgState* st, int init) {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double rr = 0.0;
     for (int r = 0; r < p; ++r) rr = dadd(rr, g[r]);
@@ -315,7 +327,7 @@ void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol
     const int64_t l0 = launches_;
     PB_CUDA(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     iteration_enqueue(cc, precflag);
-    k_loop_ctl<<<1, 32, 0, s_>>>(state_.get(), rtol, max_iters, hist_.get(), handle);
+    launch_k(k_loop_ctl, 1, 32, 0, s_, state_.get(), rtol, max_iters, hist_.get(), handle);
     PB_CHECK_LAUNCH();
     PB_CUDA(cudaStreamEndCapture(s_, &body));
     launches_ = l0;
@@ -488,7 +500,7 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
         sweep = 2;
     } else if (zero_start) {
         begin_time(-1);
-        if (n) k_zero_start<<<blocks_for(n, 256), 256, 0, s_>>>(rhs, L.l1.get(), xc, n, omega);
+        if (n) launch_k<4>(k_zero_start, blocks_for(n, 256), 256, 0, s_, rhs, L.l1.get(), xc, n, omega);
         PB_CHECK_LAUNCH();
         launches_ += 1;
         sweep = 1;
@@ -524,10 +536,10 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     Level& T = gather ? *h.levels[k + 1] : lvl(k + 1);
     Level& C = lvl(k + 1);
     if (T.A.n && !T.rcode.empty())
-        k_restrict_c<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rcode.get(),
+        launch_k<4>(k_restrict_c, blocks_for(T.A.n, 256), 256, 0, s_, T.rrp.get(), T.rcol.get(), T.rcode.get(),
                                                              code_tab(T.rtab), L.res.get(), T.rhs.get(), T.A.n);
     else if (T.A.n)
-        k_restrict<<<blocks_for(T.A.n, 256), 256, 0, s_>>>(T.rrp.get(), T.rcol.get(), T.rval.get(), L.res.get(),
+        launch_k<4>(k_restrict, blocks_for(T.A.n, 256), 256, 0, s_, T.rrp.get(), T.rcol.get(), T.rval.get(), L.res.get(),
                                                            T.rhs.get(), T.A.n);
     PB_CHECK_LAUNCH();
     launches_ += 1;
@@ -551,10 +563,10 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         --post;
     } else {
         if (L.A.n && !T.pcode.empty())
-            k_prolong_c<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pcode.get(), code_tab(T.ptab), e, xc,
+            launch_k<4>(k_prolong_c, blocks_for(L.A.n, 256), 256, 0, s_, T.pcol.get(), T.pcode.get(), code_tab(T.ptab), e, xc,
                                                                 L.A.n);
         else if (L.A.n)
-            k_prolong<<<blocks_for(L.A.n, 256), 256, 0, s_>>>(T.pcol.get(), T.pval.get(), e, xc, L.A.n);
+            launch_k<4>(k_prolong, blocks_for(L.A.n, 256), 256, 0, s_, T.pcol.get(), T.pval.get(), e, xc, L.A.n);
         PB_CHECK_LAUNCH();
         launches_ += 1;
     }
@@ -568,12 +580,12 @@ void Solver::reduce_dots_enqueue() {
     Level& L0 = *h.levels[0];
     const int G = dots_grid_;  // partial triples written by the SpMV+dots launches
     if (G > kStage) {  // two fixed-order stages: kStage blocks over contiguous chunks, then one block
-        k_reduce_chunks<<<kStage, kRedThreads, 0, s_>>>(partials_.get(), G, 3, stage_.get());
+        launch_k(k_reduce_chunks, kStage, kRedThreads, 0, s_, partials_.get(), G, 3, stage_.get());
         PB_CHECK_LAUNCH();
-        k_reduce<<<1, kRedThreads, 0, s_>>>(stage_.get(), kStage, 3, local_.get());
+        launch_k(k_reduce, 1, kRedThreads, 0, s_, stage_.get(), kStage, 3, local_.get());
         launches_ += 1;
     } else {
-        k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), G, 3, local_.get());
+        launch_k(k_reduce, 1, kRedThreads, 0, s_, partials_.get(), G, 3, local_.get());
     }
     PB_CHECK_LAUNCH();
     const double* g = local_.get();
@@ -581,21 +593,21 @@ void Solver::reduce_dots_enqueue() {
         rt.allgather_f64(local_.get(), gathered_.get(), 3, s_);
         g = gathered_.get();
     }
-    k_fcg_scalars<<<1, 32, 0, s_>>>(g, p, state_.get());
+    launch_k(k_fcg_scalars, 1, 32, 0, s_, g, p, state_.get());
     PB_CHECK_LAUNCH();
     launches_ += 2;
 }
 
 void Solver::reduce_norm_enqueue(bool init) {
     const int p = rt.nranks();
-    k_reduce<<<1, kRedThreads, 0, s_>>>(partials_.get(), red_grid(n_), 1, local_.get() + 3);
+    launch_k(k_reduce, 1, kRedThreads, 0, s_, partials_.get(), red_grid(n_), 1, local_.get() + 3);
     PB_CHECK_LAUNCH();
     const double* g = local_.get() + 3;
     if (p > 1) {
         rt.allgather_f64(local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
         g = gathered_.get() + 3 * p;
     }
-    k_norm_final<<<1, 32, 0, s_>>>(g, p, state_.get(), init ? 1 : 0);
+    launch_k(k_norm_final, 1, 32, 0, s_, g, p, state_.get(), init ? 1 : 0);
     PB_CHECK_LAUNCH();
     launches_ += 2;
 }
@@ -666,10 +678,10 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     begin_time(3);
     zs_pending_ = false;
     if (zs)
-        k_update<true><<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
+        launch_k<8>(k_update<true>, red_grid(n_), kRedThreads, 0, s_, w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
                                                               n_, state_.get(), partials_.get(), zero_start_args(cc));
     else
-        k_update<false><<<red_grid(n_), kRedThreads, 0, s_>>>(w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
+        launch_k<8>(k_update<false>, red_grid(n_), kRedThreads, 0, s_, w, d_.get(), u_.get(), v_.get(), q_.get(), r_.get(),
                                                                n_, state_.get(), partials_.get(), ZeroStart{});
     PB_CHECK_LAUNCH();
     end_time(3);
@@ -725,12 +737,12 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
         o.r = d_b;
         apply(0, o, -1);
     }
-    k_norm_partials<<<red_grid(n_), kRedThreads, 0, s_>>>(r_.get(), n_, partials_.get());
+    launch_k(k_norm_partials, red_grid(n_), kRedThreads, 0, s_, r_.get(), n_, partials_.get());
     PB_CHECK_LAUNCH();
     launches_ += 1;
     reduce_norm_enqueue(true);
     if (zs_fused(cc, precflag) && n_) {
-        k_zero_start<<<blocks_for(n_, 256), 256, 0, s_>>>(r_.get(), L0.l1.get(), L0.x.get(), n_, cc.relax_weight);
+        launch_k<4>(k_zero_start, blocks_for(n_, 256), 256, 0, s_, r_.get(), L0.l1.get(), L0.x.get(), n_, cc.relax_weight);
         PB_CHECK_LAUNCH();
         launches_ += 1;
     }
