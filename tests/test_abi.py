@@ -92,3 +92,15 @@ def test_product_does_not_use_oracle():
 
     out = subprocess.run(["ldd", pb.LIB_PATH], capture_output=True, text=True).stdout
     assert "pairamg_oracle" not in out and "pairamg_ref" not in out
+
+
+def test_no_load_ahead_of_grid_dependency_wait(lib):
+    """Kernels launched with programmatic dependent launch may start while
+    their predecessor still writes: no global load may precede the
+    griddepcontrol.wait (SASS ACQBULK) -- ptxas hoists ld.global.nc loads."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "check_pdl_sass.py")], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
