@@ -892,27 +892,66 @@ void reset_pat(Sell& S) {
     S.format = Sell::kPlain;
 }
 
-// PAT -> STEN when every pattern is an order-preserving subset of the
-// longest one with bitwise-equal records.
+// PAT -> STEN: the main pattern is a common supersequence of all row patterns
+// (records compared bitwise), built from the longest pattern by merging in
+// every pattern that is not already a subsequence (shortest common
+// supersequence of the two, LCS dynamic programme); <= kStenMax records.
+// Slab-partition boundary rows, whose halo neighbour sits at a different
+// local offset on each face, nest this way.
 bool try_sten(Sell& S) {
     if (S.npat < 1) return false;
-    int mp = 0;
-    for (int p = 1; p < S.npat; ++p)
-        if (S.hpmeta[p].y > S.hpmeta[mp].y) mp = p;
-    const int L = S.hpmeta[mp].y;
-    if (L < 1 || L > kStenMax) return false;
-    const ulonglong2* mr = S.hptab.data() + S.hpmeta[mp].x;
-    std::vector<uint32_t> mask(S.npat, 0u);
-    for (int p = 0; p < S.npat; ++p) {
-        const ulonglong2* pr = S.hptab.data() + S.hpmeta[p].x;
-        int j = 0;
-        uint32_t present = 0;
-        for (int t = 0; t < S.hpmeta[p].y; ++t) {
-            while (j < L && !(mr[j].x == pr[t].x && mr[j].y == pr[t].y)) ++j;
-            if (j == L) return false;
-            present |= 1u << j;
+    auto eq = [](const ulonglong2& a, const ulonglong2& b) { return a.x == b.x && a.y == b.y; };
+    auto pat = [&](int p) {
+        return std::vector<ulonglong2>(S.hptab.begin() + S.hpmeta[p].x, S.hptab.begin() + S.hpmeta[p].x + S.hpmeta[p].y);
+    };
+    auto subseq = [&](const std::vector<ulonglong2>& P, const std::vector<ulonglong2>& M, uint32_t* present) {
+        size_t j = 0;
+        uint32_t pr = 0;
+        for (const auto& r : P) {
+            while (j < M.size() && !eq(M[j], r)) ++j;
+            if (j == M.size()) return false;
+            pr |= 1u << j;
             ++j;
         }
+        if (present) *present = pr;
+        return true;
+    };
+    std::vector<int> order(S.npat);
+    for (int p = 0; p < S.npat; ++p) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return S.hpmeta[a].y > S.hpmeta[b].y; });
+    std::vector<ulonglong2> M = pat(order[0]);
+    for (int p : order) {
+        const std::vector<ulonglong2> P = pat(p);
+        if (subseq(P, M, nullptr)) continue;
+        const size_t a = M.size(), b = P.size();
+        std::vector<std::vector<int>> lcs(a + 1, std::vector<int>(b + 1, 0));
+        for (size_t i = a; i-- > 0;)
+            for (size_t j = b; j-- > 0;)
+                lcs[i][j] = eq(M[i], P[j]) ? lcs[i + 1][j + 1] + 1 : std::max(lcs[i + 1][j], lcs[i][j + 1]);
+        std::vector<ulonglong2> U;
+        size_t i = 0, j = 0;
+        while (i < a && j < b) {
+            if (eq(M[i], P[j])) {
+                U.push_back(M[i++]);
+                ++j;
+            } else if (lcs[i + 1][j] >= lcs[i][j + 1]) {
+                U.push_back(M[i++]);
+            } else {
+                U.push_back(P[j++]);
+            }
+        }
+        while (i < a) U.push_back(M[i++]);
+        while (j < b) U.push_back(P[j++]);
+        if (U.size() > static_cast<size_t>(kStenMax)) return false;
+        M.swap(U);
+    }
+    const int L = static_cast<int>(M.size());
+    if (L < 1 || L > kStenMax) return false;
+    const ulonglong2* mr = M.data();
+    std::vector<uint32_t> mask(S.npat, 0u);
+    for (int p = 0; p < S.npat; ++p) {
+        uint32_t present = 0;
+        if (!subseq(pat(p), M, &present)) return false;
         mask[p] = ~present & (L == 32 ? 0xFFFFFFFFu : ((1u << L) - 1u));
     }
     S.sten_L = L;

@@ -934,7 +934,10 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         if (L.A.halo.n_halo > 0) {
             build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, env_flag("PAIRAMG_SELL_DICT", true),
                        L.l1.get());
-            build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s, /*allow_dict=*/false);
+            // boundary rows: STEN too when the faces' halo offsets nest into
+            // one main pattern (slab partitions), else PAT/DICT/PLAIN
+            build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s,
+                       env_flag("PAIRAMG_SELL_DICT", true) && env_flag("PAIRAMG_BND_FORMATS", true), L.l1.get());
             // whole level incl. halo columns, for the exchange-then-compute
             // schedule (slab partitions keep constant halo column offsets,
             // so DICT/PAT usually still apply)
