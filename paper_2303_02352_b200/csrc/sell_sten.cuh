@@ -53,32 +53,46 @@ struct StenArgs {
 template <int LL, bool EDGE>
 __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m,
                                                double& own) {
-    constexpr int N = LL ? LL : kStenMax;
-    double xv[N];
+    if constexpr (LL == 0) {
+        // generic length: batches of 8 loads (registers, no local-memory array)
+        double sum = 0.0;
+        for (int k0 = 0; k0 < a.L; k0 += 8) {
+            double xv[8];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        if (LL == 0 && k >= a.L) break;
-        int c = row + p.off[k];
-        if (EDGE) c = min(max(c, 0), a.xlen - 1);
-        xv[k] = a.x[c];  // coherent load: this kernel may start before x's producer completes (PDL)
-    }
-    double sum = 0.0;
-    if (__all_sync(0xffffffffu, m == 0u)) {
+            for (int j = 0; j < 8; ++j) {
+                int c = row + (k0 + j < a.L ? p.off[k0 + j] : 0);
+                if (EDGE) c = min(max(c, 0), a.xlen - 1);
+                xv[j] = a.x[c];
+            }
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            if (LL == 0 && k >= a.L) break;
-            sum = dadd(sum, dmul(p.val[k], xv[k]));
+            for (int j = 0; j < 8; ++j) {
+                const int k = k0 + j;
+                if (k < a.L && !((m >> k) & 1u)) sum = dadd(sum, dmul(p.val[k], xv[j]));
+            }
         }
+        return sum;
     } else {
+        double xv[LL];
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            if (LL == 0 && k >= a.L) break;
-            const double pr = dmul(p.val[k], xv[k]);
-            if (!((m >> k) & 1u)) sum = dadd(sum, pr);
+        for (int k = 0; k < LL; ++k) {
+            int c = row + p.off[k];
+            if (EDGE) c = min(max(c, 0), a.xlen - 1);
+            xv[k] = a.x[c];  // coherent load: this kernel may start before x's producer completes (PDL)
         }
+        double sum = 0.0;
+        if (__all_sync(0xffffffffu, m == 0u)) {
+#pragma unroll
+            for (int k = 0; k < LL; ++k) sum = dadd(sum, dmul(p.val[k], xv[k]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < LL; ++k) {
+                const double pr = dmul(p.val[k], xv[k]);
+                if (!((m >> k) & 1u)) sum = dadd(sum, pr);
+            }
+        }
+        own = xv[LL / 2];
+        return sum;
     }
-    if (LL > 0) own = xv[LL > 0 ? LL / 2 : 0];
-    return sum;
 }
 
 template <int LL>

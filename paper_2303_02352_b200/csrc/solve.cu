@@ -369,8 +369,10 @@ void Solver::ensure_vectors() {
     q_.alloc(static_cast<size_t>(n_), s_);
     // partial triples of the SpMV+dots launches (interior + boundary, one
     // block per 8 slices) and of the grid-stride reductions
-    const int64_t dots_blocks = L0.A.halo.n_halo > 0 ? int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd)
-                                                     : int64_t(sell_dots_grid(L0.sell_all));
+    // (overlapped schedule: interior + boundary partials; exchange-then-compute: sell_all)
+    int64_t dots_blocks = sell_dots_grid(L0.sell_all);
+    if (L0.A.halo.n_halo > 0)
+        dots_blocks = std::max<int64_t>(dots_blocks, int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd));
     max_blocks_ = static_cast<int>(std::max<int64_t>(dots_blocks, kSmCount * 8));
     partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
     stage_.alloc(static_cast<size_t>(3 * kStage), s_);

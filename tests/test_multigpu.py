@@ -13,14 +13,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_parity(world):
+@pytest.mark.parametrize("world,overlap", [(2, 1), (2, 0), (4, 1)])
+def test_distributed_parity(world, overlap):
+    """overlap=0: exchange-then-compute over the whole level (one Sell with halo columns)."""
     if gpu_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + 10 * world + overlap),
            os.path.join(ROOT, "tests", "mp_parity.py")]
-    r = subprocess.run(["timeout", "-k", "10", "300", *cmd], capture_output=True, text=True, timeout=400, cwd=ROOT)
+    env = dict(os.environ, PAIRAMG_OVERLAP=str(overlap))
+    r = subprocess.run(["timeout", "-k", "10", "300", *cmd], capture_output=True, text=True, timeout=400, cwd=ROOT,
+                       env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("MP_PARITY_OK") == 5, out[-4000:]
