@@ -278,6 +278,7 @@ int red_grid(int64_t n) {
 Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
     fuse = env_flag("PAIRAMG_FUSE", false);
     overlap = env_flag("PAIRAMG_OVERLAP", true);
+    bnd_on_comm = env_flag("PAIRAMG_BND_ON_COMM", true);
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
@@ -449,13 +450,24 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
     if (L.A.halo.has_traffic()) {
         if (o.op == kJacobiZero || o.op == kJacobiProl)
             fail(PAIRAMG_INTERNAL, "fused sweeps need a level without halo traffic");
+        // The boundary rows run on the (high-priority) communication stream
+        // right behind the halo receive, concurrently with the interior rows:
+        // the compute stream only joins at the end, no second launch on it.
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
         halo_exchange(rt, L.A.halo, o.x, const_cast<double*>(o.x) + L.A.n, rt.comm_stream());
+        if (L.A.halo.n_halo > 0 && bnd_on_comm) {
+            sell_apply(L.sell_bnd, o, rt.comm_stream());
+            launches_ += 1;
+        }
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += L.A.halo.send_off.back() ? 1 : 0;
     }
-    if (L.A.halo.n_halo > 0) {
+    if (L.A.halo.n_halo > 0 && bnd_on_comm) {
+        sell_apply(L.sell_int, o, s_);
+        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        launches_ += 1;
+    } else if (L.A.halo.n_halo > 0) {
         sell_apply(L.sell_int, o, s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         sell_apply(L.sell_bnd, o, s_);
@@ -654,6 +666,19 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         halo_exchange(rt, L0.A.halo, w, w + L0.A.n, s_);
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
+    } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
+        const int g1 = sell_dots_grid(L0.sell_int);
+        PB_CUDA(cudaEventRecord(ev_fork_, s_));
+        PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
+        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, rt.comm_stream());
+        const int g2 = sell_spmv_dots(L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get() + 3 * g1,
+                                      max_blocks_ - g1, rt.comm_stream());
+        PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
+        const int g1b = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), g1, s_);
+        if (g1b != g1) fail(PAIRAMG_INTERNAL, "spmv+dots: interior partial count changed");
+        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+        dots_grid_ = g1 + g2;
+        launches_ += 3;
     } else if (L0.A.halo.has_traffic()) {  // halo of w in flight while the interior rows run
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
@@ -661,7 +686,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }
-    if (L0.A.halo.has_traffic() && !overlap) {
+    if ((L0.A.halo.has_traffic() && !overlap) || (L0.A.halo.n_halo > 0 && bnd_on_comm)) {
         // done above
     } else if (L0.A.halo.n_halo > 0) {
         const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);

@@ -59,6 +59,7 @@ public:
     bool fuse = true;     // fused zero-start / prolongation sweeps on halo-free levels
     bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
     bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
+    bool bnd_on_comm = true;  // halo boundary rows computed on the comm stream behind the receive
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
