@@ -159,5 +159,8 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s);
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
                    double* partials, int max_blocks, cudaStream_t s);
 int sell_dots_grid(const Sell& S);
+// The coarsest level's zero start + nu-1 l1-Jacobi sweeps in one cluster
+// launch (halo-free STEN, <= 16384 rows); false when not applicable.
+bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, double omega, cudaStream_t s);
 
 }  // namespace pb

@@ -29,6 +29,7 @@
 // The two fused operators trade stored bytes for per-entry recomputation; on
 // B200 they measured slower than the separate kernels and are
 // off by default (PAIRAMG_FUSE=1 enables them).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1434,6 +1435,39 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
         case kJacobiProl: launch_op<kJacobiProl>(S, a, s); break;
         default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
     }
+}
+
+bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, double omega, cudaStream_t s) {
+    // <= 8 records: with 27 the remote (DSMEM) gathers outweigh the saved
+    // launches (measured 1.28 vs 1.25 ms/iter at 27-point 192^3)
+    if (S.format != Sell::kSten || !S.rows.empty() || S.row0 != 0 || S.nrows != S.xlen || nu < 1 ||
+        S.nrows > int64_t(kCoarseCta) * kCoarseRows || S.sten_L > env_int("PAIRAMG_COARSE_CLUSTER_L", 8))
+        return false;
+    const int R = static_cast<int>((S.nrows + kCoarseCta - 1) / kCoarseCta);
+    StenArgs a = sten_args_of(S);
+    a.r = rhs;
+    a.omega = omega;
+    const StenParam p = sten_param(S);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCoarseCta);
+    cfg.blockDim = dim3(kCoarseThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCoarseCta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl_mask() & 2) ? 2 : 1;
+    if (S.sten_L == 7)
+        PB_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_solve<7>, a, p, x, nu, R));
+    else if (S.sten_L == 27)
+        PB_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_solve<27>, a, p, x, nu, R));
+    else
+        PB_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_solve<0>, a, p, x, nu, R));
+    return true;
 }
 
 int sell_dots_grid(const Sell& S) {

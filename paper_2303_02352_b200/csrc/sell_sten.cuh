@@ -324,3 +324,77 @@ __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_con
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// The coarsest level's whole smoothing (zero start + nu-1 l1-Jacobi sweeps,
+// cycle.cpp:126-133) in ONE launch of one thread-block cluster: every CTA
+// owns R consecutive rows, keeps its slice of the iterate in shared memory
+// (ping-pong), gathers neighbours from the owning CTA's shared memory
+// (distributed shared memory) and the cluster barrier separates the sweeps.
+// Replaces nu launch-bound kernels (19 x ~3.7 us at 256^3) by one.  Row sums
+// in CSR order with the same dadd/dmul chain: bitwise the sweep kernels.
+constexpr int kCoarseCta = 8;          // portable cluster size
+constexpr int kCoarseThreads = 1024;
+constexpr int kCoarseRows = 2048;      // rows per CTA (2 per thread)
+
+template <int LL>
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, const __grid_constant__ StenParam p,
+                                                                 double* out, int nu, int R) {
+    namespace cg = cooperative_groups;
+    pdl_begin();
+    __shared__ double xs[2][kCoarseRows];
+    cg::cluster_group cl = cg::this_cluster();
+    const int me = static_cast<int>(cl.block_rank());
+    const int n = a.nrows;
+    const int L = LL ? LL : a.L;
+    int rowv[2];
+    double rv[2], dv[2];
+    uint32_t mv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = static_cast<int>(threadIdx.x) + h * kCoarseThreads;
+        const int row = me * R + t;
+        rowv[h] = (t < R && row < n) ? row : -1;
+        if (rowv[h] >= 0) {
+            const int q = a.pid[row];
+            rv[h] = a.r[row];
+            dv[h] = p.pdiag[q];
+            mv[h] = p.pmask[q];
+            xs[0][t] = ddiv(a.omega == 1.0 ? rv[h] : dmul(a.omega, rv[h]), dv[h]);  // zero start
+        }
+    }
+    cl.sync();
+    for (int sweep = 1; sweep < nu; ++sweep) {
+        const int cur = (sweep - 1) & 1, nxt = sweep & 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (rowv[h] < 0) continue;
+            const int row = rowv[h];
+            double sum = 0.0;
+            for (int k0 = 0; k0 < L; k0 += 8) {  // 8 independent DSMEM loads in flight, then the CSR-order sum
+                double xv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int k = k0 + j;
+                    int c = row + (k < L ? p.off[k] : 0);
+                    c = min(max(c, 0), n - 1);
+                    const int owner = c / R, loc = c - owner * R;
+                    xv[j] = *cl.map_shared_rank(&xs[cur][loc], owner);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int k = k0 + j;
+                    if (k < L && !((mv[h] >> k) & 1u)) sum = dadd(sum, dmul(p.val[k], xv[j]));
+                }
+            }
+            const int t = row - me * R;
+            const double t1 = dsub(rv[h], sum);
+            xs[nxt][t] = dadd(xs[cur][t], ddiv(a.omega == 1.0 ? t1 : dmul(a.omega, t1), dv[h]));
+        }
+        cl.sync();
+    }
+    const int fin = (nu - 1) & 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        if (rowv[h] >= 0) out[rowv[h]] = xs[fin][rowv[h] - me * R];
+}

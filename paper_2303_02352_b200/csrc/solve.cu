@@ -70,6 +70,27 @@ __global__ void k_prolong_c(const int32_t* pcol, const uint8_t* pcode,
     if (i < n) x[i] = dadd(x[i], dmul(t.v[pcode[i]], e[pcol[i]]));
 }
 
+// Four rows per thread with 16-byte loads/stores (x, pcol) and one 4-byte
+// pattern load: the four coarse gathers are independent and in flight
+// together (the one-row kernel is a load -> gather -> store latency chain).
+__global__ void __launch_bounds__(256) k_prolong_c4(const int4* pcol, const uint32_t* pcode,
+                                                     const __grid_constant__ CodeTab t, const double* e, double2* x,
+                                                     int64_t n4) {
+    pdl_begin();
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    const int4 c = pcol[i];
+    const uint32_t k = pcode[i];
+    const double e0 = e[c.x], e1 = e[c.y], e2 = e[c.z], e3 = e[c.w];
+    double2 a = x[2 * i], b = x[2 * i + 1];
+    a.x = dadd(a.x, dmul(t.v[k & 0xFF], e0));
+    a.y = dadd(a.y, dmul(t.v[(k >> 8) & 0xFF], e1));
+    b.x = dadd(b.x, dmul(t.v[(k >> 16) & 0xFF], e2));
+    b.y = dadd(b.y, dmul(t.v[k >> 24], e3));
+    x[2 * i] = a;
+    x[2 * i + 1] = b;
+}
+
 CodeTab code_tab(const std::vector<double>& v) {
     CodeTab t{};
     for (size_t i = 0; i < v.size() && i < 256; ++i) t.v[i] = v[i];
@@ -531,7 +552,12 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     double* xo = L.xt.get();
     const bool l0 = k == 0;
     if (k == h.nl() - 1) {
-        smooth(k, true, cc.coarsest_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+        if (!L.A.halo.has_traffic() && !(k == 0 && zs_pending_) &&
+            sell_coarse_solve(L.sell_all, rhs, xc, cc.coarsest_sweeps, cc.relax_weight, s_)) {
+            launches_ += 1;
+        } else {
+            smooth(k, true, cc.coarsest_sweeps, rhs, xc, xo, cc.relax_weight, l0);
+        }
         out = xc;
         return;
     }
@@ -576,7 +602,18 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         std::swap(xc, xo);
         --post;
     } else {
-        if (L.A.n && !T.pcode.empty())
+        const bool v4 = L.A.n >= 4 && (reinterpret_cast<uintptr_t>(xc) & 15) == 0;  // 16-byte aligned buffers
+        if (L.A.n && !T.pcode.empty() && v4) {
+            const int64_t n4 = L.A.n / 4;  // the < 4 tail rows by the scalar kernel
+            launch_k<4>(k_prolong_c4, blocks_for(n4, 256), 256, 0, s_, reinterpret_cast<const int4*>(T.pcol.get()),
+                        reinterpret_cast<const uint32_t*>(T.pcode.get()), code_tab(T.ptab), e,
+                        reinterpret_cast<double2*>(xc), n4);
+            if (L.A.n % 4) {
+                launch_k<4>(k_prolong_c, 1, 32, 0, s_, T.pcol.get() + 4 * n4, T.pcode.get() + 4 * n4, code_tab(T.ptab),
+                            e, xc + 4 * n4, L.A.n - 4 * n4);
+                launches_ += 1;
+            }
+        } else if (L.A.n && !T.pcode.empty())
             launch_k<4>(k_prolong_c, blocks_for(L.A.n, 256), 256, 0, s_, T.pcol.get(), T.pcode.get(), code_tab(T.ptab), e, xc,
                                                                 L.A.n);
         else if (L.A.n)
