@@ -1105,7 +1105,7 @@ StenParam sten_param(const Sell& S) {
 // Two rows per thread for the 7-record main pattern (k_sten2): +10% bandwidth.
 // 27 records: only the SpMV+dots kernel gains (122 vs 132 us; sweeps lose).
 bool sten_rpt2(const Sell& S, bool dots = false) {
-    if (!sten_center(S)) return false;
+    if (!sten_center(S) || S.nrows < env_int("PAIRAMG_STEN_RPT_MIN_ROWS", 0)) return false;
     if (S.sten_L == 7) return env_int("PAIRAMG_STEN_RPT", 2) == 2;
     return S.sten_L == 27 && env_int("PAIRAMG_STEN_RPT27", dots ? 2 : 1) == 2;
 }
