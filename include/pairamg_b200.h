@@ -238,6 +238,16 @@ pairamg_status pairamg_mm_rows(pairamg_mm* m, int64_t row_begin, int64_t row_end
 pairamg_status pairamg_mm_copy_rows(pairamg_mm* m, int64_t row_begin, int64_t row_end, int64_t* row_ptr,
                                     int64_t* col, double* val);
 pairamg_status pairamg_mm_close(pairamg_mm* m);
+/* General sparse product C = A*B on rt's GPU (spgemm_local, csr.cpp:206-272;
+ * SURVEY 8f row 4): A is a_nrows x a_ncols, B is a_ncols x b_ncols, host CSR
+ * arrays; per output entry the products a_ik*b_kj are summed in encounter
+ * order (A row, then B row), the first assigned -- bitwise the reference.
+ * The result is a host-CSR handle read with pairamg_mm_rows/copy_rows and
+ * freed with pairamg_mm_close. */
+pairamg_status pairamg_spgemm(pairamg_runtime* rt, int64_t a_nrows, int64_t a_ncols, const int64_t* a_row_ptr,
+                              const int64_t* a_col, const double* a_val, int64_t b_ncols,
+                              const int64_t* b_row_ptr, const int64_t* b_col, const double* b_val,
+                              pairamg_mm** out, int64_t* nnz);
 /* Write "coordinate real general" with %.17g values (write_matrix_market). */
 pairamg_status pairamg_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
                                 const int64_t* col, const double* val);

@@ -113,6 +113,8 @@ def _lib(kind: str) -> C.CDLL:
         L.orc_mm_export.argtypes = [vp, vp, vp, vp]
         L.orc_mm_free.argtypes = [vp]
         L.orc_mm_write.argtypes = [C.c_char_p, i64, i64, vp, vp, vp]
+        L.orc_spgemm.argtypes = [i64, i64, vp, vp, vp, i64, vp, vp, vp]
+        L.orc_spgemm.restype = vp
     _loaded[kind] = L
     return L
 
@@ -163,6 +165,28 @@ def mm_read(path: str):
     finally:
         L.orc_mm_free(h)
     return n.value, nc.value, rp, ci, va
+
+
+def spgemm(A, B):
+    """Reference spgemm_local (csr.cpp:206-279). A, B = (row_ptr, col, val, ncols)."""
+    L = _lib("reference")
+    arp, acol, aval, am = A
+    brp, bcol, bval, bm = B
+    arp, acol, brp, bcol = (np.ascontiguousarray(x, np.int64) for x in (arp, acol, brp, bcol))
+    aval, bval = (np.ascontiguousarray(x, np.float64) for x in (aval, bval))
+    h = L.orc_spgemm(len(arp) - 1, am, _p(arp), _p(acol), _p(aval), bm, _p(brp), _p(bcol), _p(bval))
+    if not h:
+        raise OracleError(L.orc_last_status(), L.orc_last_error().decode())
+    try:
+        n, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        L.orc_mm_info(h, C.byref(n), C.byref(nc), C.byref(nz))
+        rp = np.empty(n.value + 1, np.int64)
+        ci = np.empty(nz.value, np.int64)
+        va = np.empty(nz.value, np.float64)
+        L.orc_mm_export(h, _p(rp), _p(ci), _p(va))
+    finally:
+        L.orc_mm_free(h)
+    return rp, ci, va
 
 
 def mm_write(path: str, row_ptr, col, val, ncols=None):

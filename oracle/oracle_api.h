@@ -109,6 +109,10 @@ void* orc_mm_load(const char* path);
 void orc_mm_info(void* m, int64_t* nrows, int64_t* ncols, int64_t* nnz);
 void orc_mm_export(void* m, int64_t* row_ptr, int64_t* col, double* val);
 void orc_mm_free(void* m);
+/* spgemm_local(A, B) (csr.cpp:206-279) -> a CsrMatrix handle read with
+ * orc_mm_info / orc_mm_export / orc_mm_free; NULL on error. */
+void* orc_spgemm(int64_t an, int64_t am, const int64_t* a_rp, const int64_t* a_col, const double* a_val, int64_t bm,
+                 const int64_t* b_rp, const int64_t* b_col, const double* b_val);
 /* write_matrix_market (mm_io.cpp:90-110) of a CSR. */
 int orc_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int64_t* col,
                  const double* val);

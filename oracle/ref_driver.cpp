@@ -538,6 +538,22 @@ void orc_mm_export(void* m, int64_t* row_ptr, int64_t* col, double* val) {
 
 void orc_mm_free(void* m) { delete static_cast<CsrMatrix*>(m); }
 
+void* orc_spgemm(int64_t an, int64_t am, const int64_t* a_rp, const int64_t* a_col, const double* a_val, int64_t bm,
+                 const int64_t* b_rp, const int64_t* b_col, const double* b_val) {
+    CsrMatrix* out = nullptr;
+    guarded([&] {
+        CsrMatrix A(an, am), B(am, bm);
+        A.row_ptr.assign(a_rp, a_rp + an + 1);
+        A.col_idx.assign(a_col, a_col + a_rp[an]);
+        A.values.assign(a_val, a_val + a_rp[an]);
+        B.row_ptr.assign(b_rp, b_rp + am + 1);
+        B.col_idx.assign(b_col, b_col + b_rp[am]);
+        B.values.assign(b_val, b_val + b_rp[am]);
+        out = new CsrMatrix(spgemm_local(A, B));
+    });
+    return out;
+}
+
 int orc_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int64_t* col,
                  const double* val) {
     return guarded([&] {

@@ -35,7 +35,7 @@ EXPORTS = [
     "pairamg_get_setup_stats", "pairamg_set_kernel_timing", "pairamg_kernel_timing", "pairamg_launch_count",
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
     "pairamg_match_graph", "pairamg_mm_open", "pairamg_mm_rows", "pairamg_mm_copy_rows", "pairamg_mm_close",
-    "pairamg_mm_write",
+    "pairamg_mm_write", "pairamg_spgemm",
 ]
 
 
@@ -147,6 +147,7 @@ def lib() -> C.CDLL:
         "pairamg_mm_copy_rows": ([vp, i64, i64, vp, vp, vp], st),
         "pairamg_mm_close": ([vp], st),
         "pairamg_mm_write": ([C.c_char_p, i64, i64, vp, vp, vp], st),
+        "pairamg_spgemm": ([vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, C.POINTER(vp), C.POINTER(i64)], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -196,6 +197,30 @@ def read_matrix_market(path: str, row_begin: int = 0, row_end: int | None = None
     finally:
         L.pairamg_mm_close(h)
     return n.value, nc.value, rp, ci, va
+
+
+def spgemm(rt: "Runtime", A, B):
+    """C = A*B on rt's GPU in the reference's summation order (spgemm_local,
+    csr.cpp:206-272).  A, B = (row_ptr, col, val, ncols) host arrays;
+    returns (row_ptr, col, val)."""
+    L = lib()
+    arp, acol, aval, am = A
+    brp, bcol, bval, bm = B
+    arp, acol, brp, bcol = (np.ascontiguousarray(x, np.int64) for x in (arp, acol, brp, bcol))
+    aval, bval = (np.ascontiguousarray(x, np.float64) for x in (aval, bval))
+    h = C.c_void_p()
+    nz = C.c_int64()
+    _check(L.pairamg_spgemm(rt.h, len(arp) - 1, am, _ptr(arp), _ptr(acol), _ptr(aval), bm, _ptr(brp), _ptr(bcol),
+                            _ptr(bval), C.byref(h), C.byref(nz)))
+    try:
+        n = len(arp) - 1
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(nz.value, np.int64)
+        va = np.empty(nz.value, np.float64)
+        _check(L.pairamg_mm_copy_rows(h, 0, n, _ptr(rp), _ptr(ci), _ptr(va)))
+    finally:
+        L.pairamg_mm_close(h)
+    return rp, ci, va
 
 
 def write_matrix_market(path: str, row_ptr, col, val, ncols: int | None = None) -> None:

@@ -9,6 +9,7 @@
 
 #include "mmio.cuh"
 #include "pairamg_b200.h"
+#include "spgemm.cuh"
 #include "solver.cuh"
 
 struct pairamg_runtime {
@@ -601,6 +602,20 @@ pairamg_status pairamg_mm_copy_rows(pairamg_mm* m, int64_t b, int64_t e, int64_t
             for (int64_t i = 0; i <= e - b; ++i) row_ptr[i] = m->A.row_ptr[static_cast<size_t>(b + i)] - base;
         if (col) std::memcpy(col, m->A.col.data() + base, 8 * static_cast<size_t>(end - base));
         if (val) std::memcpy(val, m->A.val.data() + base, 8 * static_cast<size_t>(end - base));
+    });
+}
+
+pairamg_status pairamg_spgemm(pairamg_runtime* rt, int64_t an, int64_t am, const int64_t* a_rp, const int64_t* a_col,
+                              const double* a_val, int64_t bm, const int64_t* b_rp, const int64_t* b_col,
+                              const double* b_val, pairamg_mm** out, int64_t* nnz) {
+    return guarded([&] {
+        if (!rt || !rt->rt || !out || !a_rp || !b_rp) pb::fail(PAIRAMG_INVALID_ARGUMENT, "spgemm: null argument");
+        *out = nullptr;
+        PB_CUDA(cudaSetDevice(rt->rt->device()));
+        auto m = std::make_unique<pairamg_mm>();
+        m->A = pb::spgemm(an, am, a_rp, a_col, a_val, bm, b_rp, b_col, b_val, rt->rt->stream());
+        if (nnz) *nnz = static_cast<int64_t>(m->A.col.size());
+        *out = m.release();
     });
 }
 
