@@ -22,7 +22,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libpairamg_b200.so")
-SOURCES = ["runtime.cu", "sparse.cu", "sell.cu", "setup.cu", "solve.cu", "mmio.cu", "spgemm.cu", "capi.cu"]
+SOURCES = ["runtime.cu", "sparse.cu", "sell.cu", "setup.cu", "solve.cu", "mmio.cu", "spgemm.cu", "p2p.cu", "capi.cu"]
 
 
 def nvcc() -> str:

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "matrix.cuh"
+#include "p2p.cuh"
 
 namespace pb {
 
@@ -40,6 +41,8 @@ struct Level {
     // V-cycle work vectors
     DBuf<double> x, xt;      // n + n_halo (ping-pong iterates)
     DBuf<double> rhs, res;   // n
+    P2PHalo p2p;             // NVLink direct-store halo exchange (multi-rank)
+    ~Level() { p2p_destroy(p2p); }
 };
 
 struct SetupStats {  // SetupStats (amg.hpp:40-47)

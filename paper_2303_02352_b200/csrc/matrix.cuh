@@ -121,6 +121,7 @@ struct SellOpArgs {
     const int32_t* pcol = nullptr;  // kJacobiProl: prolongator of the coarser level
     const double* pval = nullptr;
     const double* e = nullptr;      // kJacobiProl: coarse correction
+    int max_grid = 0;               // STEN: cap on CTAs (grid-stride), 0 = one CTA per row block
 };
 
 // ---- sparse.cu ----
@@ -156,9 +157,10 @@ void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_
 void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s);
 // v = A w plus per-block partials of (w.r, w.v, w.q) (FCG lines 10-13).
 // Returns the number of partial triples written.
+// cap > 0: at most cap CTAs (STEN grid-strides; leaves SM slots to concurrent kernels).
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
-                   double* partials, int max_blocks, cudaStream_t s);
-int sell_dots_grid(const Sell& S);
+                   double* partials, int max_blocks, cudaStream_t s, int cap = 0);
+int sell_dots_grid(const Sell& S, int cap = 0);
 // The coarsest level's zero start + nu-1 l1-Jacobi sweeps in one cluster
 // launch (halo-free STEN, <= 16384 rows); false when not applicable.
 bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, double omega, cudaStream_t s);

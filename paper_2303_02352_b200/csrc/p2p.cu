@@ -1,0 +1,211 @@
+// p2p.cu -- NVLink halo exchange by direct stores (see p2p.cuh).
+#include <cstring>
+
+#include "p2p.cuh"
+
+namespace pb {
+
+namespace {
+
+constexpr int kMaxPeers = 8;
+constexpr int kPullBlocks = 32;
+
+struct PushArgs {
+    int npeers;
+    int64_t off[kMaxPeers + 1];  // send_off
+    double* dst[kMaxPeers];      // peer staging + my offset
+    int64_t stride[kMaxPeers];   // peer parity stride
+    unsigned long long* flag[kMaxPeers];
+};
+
+struct PullArgs {
+    int nrecv;
+    int from[kMaxPeers];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Every rank pushes its boundary values into each neighbour's staging slot of
+// parity (exchange count & 1); the last CTA raises the neighbours' flags.
+__global__ void __launch_bounds__(256) k_p2p_push(const double* x, const int32_t* send_idx, int64_t nsend,
+                                                   const __grid_constant__ PushArgs pa, unsigned long long* ctr) {
+    const unsigned long long e = ctr[0];
+    const int64_t par = static_cast<int64_t>(e & 1ull);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsend;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int p = 0;
+        while (p + 1 < pa.npeers && i >= pa.off[p + 1]) ++p;
+        pa.dst[p][par * pa.stride[p] + (i - pa.off[p])] = x[send_idx[i]];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1ull) == gridDim.x - 1) {
+        ctr[1] = 0;
+        __threadfence_system();
+        for (int p = 0; p < pa.npeers; ++p) st_release_sys(pa.flag[p], e + 1);
+    }
+}
+
+// Wait for every sender's flag of this exchange, then copy the staging slot
+// into the halo slots; the last CTA advances the exchange count.
+__global__ void __launch_bounds__(256) k_p2p_pull(const double* staging, const unsigned long long* flags, int64_t n_halo,
+                                                   const __grid_constant__ PullArgs pl, double* x_halo,
+                                                   unsigned long long* ctr) {
+    const unsigned long long e = ctr[0];
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < pl.nrecv; ++k) {
+            long long spins = 0;
+            while (ld_acquire_sys(flags + pl.from[k]) < e + 1) {
+                __nanosleep(64);
+                if (++spins == (1ll << 28)) {  // a lost flag must fail loudly, not hang the solve
+                    printf("pairamg: p2p halo flag wait timed out\n");
+                    __trap();
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const double* src = staging + static_cast<int64_t>(e & 1ull) * n_halo;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_halo;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x_halo[j] = __ldcv(src + j);  // written by a peer GPU: bypass L1
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&ctr[2], 1ull) == gridDim.x - 1) {
+        ctr[2] = 0;
+        ctr[0] = e + 1;
+    }
+}
+
+struct Blob {
+    cudaIpcMemHandle_t staging, flags;
+    int64_t n_halo;
+    int32_t nrecv;
+    int32_t recv_rank[kMaxPeers];
+    int64_t recv_off[kMaxPeers];
+};
+
+}  // namespace
+
+void p2p_destroy(P2PHalo& P) {
+    for (void* p : P.opened) cudaIpcCloseMemHandle(p);
+    P.opened.clear();
+    if (P.staging) cudaFree(P.staging);
+    if (P.flags) cudaFree(P.flags);
+    P.staging = nullptr;
+    P.flags = nullptr;
+    P.ok = false;
+}
+
+void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s) {
+    p2p_destroy(P);
+    if (rt.nranks() == 1) return;
+    Blob mine;
+    std::memset(&mine, 0, sizeof mine);
+    bool local_ok = H.recv_peers.size() <= static_cast<size_t>(kMaxPeers) &&
+                    H.send_peers.size() <= static_cast<size_t>(kMaxPeers);
+    P.n_halo = H.n_halo;
+    if (local_ok) {
+        local_ok = cudaMalloc(&P.staging, 16 * static_cast<size_t>(std::max<int64_t>(H.n_halo, 1))) == cudaSuccess &&
+                   cudaMalloc(&P.flags, 8 * static_cast<size_t>(rt.nranks())) == cudaSuccess &&
+                   cudaMemset(P.flags, 0, 8 * static_cast<size_t>(rt.nranks())) == cudaSuccess &&
+                   cudaIpcGetMemHandle(&mine.staging, P.staging) == cudaSuccess &&
+                   cudaIpcGetMemHandle(&mine.flags, P.flags) == cudaSuccess;
+        cudaGetLastError();
+    }
+    mine.n_halo = local_ok ? H.n_halo : -1;  // -1: this rank cannot take part
+    mine.nrecv = static_cast<int32_t>(std::min<size_t>(H.recv_peers.size(), kMaxPeers));
+    for (int i = 0; i < mine.nrecv; ++i) {
+        mine.recv_rank[i] = H.recv_peers[static_cast<size_t>(i)];
+        mine.recv_off[i] = H.recv_off[static_cast<size_t>(i)];
+    }
+    const std::vector<uint8_t> all = rt.allgather_bytes(&mine, sizeof(Blob));
+    std::vector<Blob> blobs(static_cast<size_t>(rt.nranks()));
+    std::memcpy(blobs.data(), all.data(), all.size());
+    bool ok = true;
+    for (const Blob& b : blobs) ok = ok && b.n_halo >= 0;
+    if (ok) {
+        for (size_t i = 0; i < H.send_peers.size(); ++i) {
+            const Blob& q = blobs[static_cast<size_t>(H.send_peers[i])];
+            int64_t off = -1;
+            for (int k = 0; k < q.nrecv; ++k)
+                if (q.recv_rank[k] == rt.rank()) off = q.recv_off[k];
+            void* st = nullptr;
+            void* fl = nullptr;
+            if (off < 0 || cudaIpcOpenMemHandle(&st, q.staging, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                ok = false;
+                cudaGetLastError();
+                break;
+            }
+            P.opened.push_back(st);
+            if (cudaIpcOpenMemHandle(&fl, q.flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                ok = false;
+                cudaGetLastError();
+                break;
+            }
+            P.opened.push_back(fl);
+            P.peer_staging.push_back(static_cast<double*>(st) + off);
+            P.peer_stride.push_back(q.n_halo);
+            P.peer_flag.push_back(static_cast<unsigned long long*>(fl) + rt.rank());
+        }
+    }
+    // every rank must agree, else all fall back to NCCL together
+    const bool all_ok = rt.allreduce_sum_i64(ok ? 1 : 0) == rt.nranks();
+    if (!all_ok) {
+        p2p_destroy(P);
+        P.peer_staging.clear();
+        P.peer_stride.clear();
+        P.peer_flag.clear();
+        return;
+    }
+    P.ctr.alloc(3, s);
+    P.ctr.zero(s);
+    PB_CUDA(cudaStreamSynchronize(s));
+    P.ok = true;
+}
+
+void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s) {
+    const int64_t nsend = H.send_off.empty() ? 0 : H.send_off.back();
+    PushArgs pa{};
+    pa.npeers = static_cast<int>(H.send_peers.size());
+    for (int i = 0; i <= pa.npeers; ++i) pa.off[i] = H.send_off[static_cast<size_t>(i)];
+    for (int i = 0; i < pa.npeers; ++i) {
+        pa.dst[i] = P.peer_staging[static_cast<size_t>(i)];
+        pa.stride[i] = P.peer_stride[static_cast<size_t>(i)];
+        pa.flag[i] = P.peer_flag[static_cast<size_t>(i)];
+    }
+    PullArgs pl{};
+    pl.nrecv = static_cast<int>(H.recv_peers.size());
+    for (int i = 0; i < pl.nrecv; ++i) pl.from[i] = H.recv_peers[static_cast<size_t>(i)];
+    // a rank with nothing to send still runs the push (it raises no flag) so
+    // the exchange counters of all ranks advance together
+    // highest scheduling priority on the launch itself: a stream's priority is
+    // not carried into the nodes of a captured graph
+    static int prio = [] {
+        int lo = 0, hi = 0;
+        PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        return env_flag("PAIRAMG_P2P_PRIO", true) ? hi : lo;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((nsend + 255) / 256, 2 * kSmCount))));
+    PB_CUDA(cudaLaunchKernelEx(&cfg, k_p2p_push, x_owned, static_cast<const int32_t*>(H.send_idx.get()), nsend, pa,
+                               P.ctr.get()));
+    cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((H.n_halo + 255) / 256, kPullBlocks))));
+    PB_CUDA(cudaLaunchKernelEx(&cfg, k_p2p_pull, static_cast<const double*>(P.staging),
+                               static_cast<const unsigned long long*>(P.flags), H.n_halo, pl, x_halo, P.ctr.get()));
+}
+
+}  // namespace pb

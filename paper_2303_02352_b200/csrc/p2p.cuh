@@ -1,0 +1,45 @@
+// p2p.cuh -- halo exchange by direct NVLink stores into the neighbours'
+// memory (CUDA IPC), replacing NCCL send/recv on the solve path.
+//
+// Measured on the B200 pair: a 512 KB NCCL send/recv takes ~51 us alone and
+// ~255 us next to an HBM-bound kernel, so at level 0 of a 256^3 slab the
+// exchange finished only after the interior rows (halo trace).
+// Here the sender's pack kernel stores its boundary values straight into the
+// receiver's staging buffer (one per level, double-buffered by exchange
+// parity) and raises a per-sender flag with a system-scope release; the
+// receiver's unpack kernel waits for the flag, copies staging -> halo slots.
+// Parity double-buffering needs no acknowledgement: a sender can be at most
+// one exchange ahead (its next exchange needs the receiver's data of this
+// one).  Both kernels run on the communication stream.
+#pragma once
+
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace pb {
+
+struct P2PHalo {
+    bool ok = false;
+    int64_t n_halo = 0;
+    double* staging = nullptr;                 // 2 * n_halo (cudaMalloc, IPC-exported)
+    unsigned long long* flags = nullptr;       // nranks slots (cudaMalloc, IPC-exported); slot = sender
+    std::vector<double*> peer_staging;         // per send peer: its staging + my offset (parity 0)
+    std::vector<int64_t> peer_stride;          // per send peer: its n_halo (parity stride)
+    std::vector<unsigned long long*> peer_flag;  // per send peer: its flags[my rank]
+    std::vector<void*> opened;                 // IPC mappings to close
+    DBuf<unsigned long long> ctr;              // [0] exchanges done, [1] push blocks done, [2] pull blocks done
+    DBuf<double*> d_peer_staging;              // device copies of the per-peer tables
+    DBuf<int64_t> d_peer_stride;
+    DBuf<unsigned long long*> d_peer_flag;
+    DBuf<int> d_recv_from;                     // recv peer ranks (flags to wait for)
+};
+
+// Collective over the ranks sharing the level; leaves P.ok = false (NCCL
+// path stays) when IPC is unavailable.
+void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s);
+void p2p_destroy(P2PHalo& P);
+// x_halo <- the owners' x (push from every rank, then pull), on stream s.
+void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s);
+
+}  // namespace pb

@@ -52,6 +52,21 @@ std::vector<int64_t> Runtime::allgather_i64(int64_t x) {
     return out;
 }
 
+std::vector<uint8_t> Runtime::allgather_bytes(const void* data, size_t n) {
+    std::vector<uint8_t> out(static_cast<size_t>(nranks_) * n);
+    if (nranks_ == 1) {
+        std::memcpy(out.data(), data, n);
+        return out;
+    }
+    stats_.allgathers += 1;
+    DBuf<uint8_t> d(static_cast<size_t>(nranks_ + 1) * n, stream_);
+    PB_CUDA(cudaMemcpyAsync(d.get() + nranks_ * n, data, n, cudaMemcpyHostToDevice, stream_));
+    PB_NCCL(ncclAllGather(d.get() + nranks_ * n, d.get(), n, ncclUint8, comm_, stream_));
+    PB_CUDA(cudaMemcpyAsync(out.data(), d.get(), static_cast<size_t>(nranks_) * n, cudaMemcpyDeviceToHost, stream_));
+    PB_CUDA(cudaStreamSynchronize(stream_));
+    return out;
+}
+
 int64_t Runtime::allreduce_sum_i64(int64_t x) {
     if (nranks_ == 1) return x;
     stats_.allreduces += 1;

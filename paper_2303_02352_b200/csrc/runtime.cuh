@@ -51,6 +51,8 @@ public:
 
     // Host-level collectives (setup path; synchronize the compute stream).
     std::vector<int64_t> allgather_i64(int64_t x);
+    // nranks * n bytes: every rank's blob in rank order.
+    std::vector<uint8_t> allgather_bytes(const void* data, size_t n);
     int64_t allreduce_sum_i64(int64_t x);
     // alltoallv of int64 id lists (setup only): chunks[d] goes to rank d; the
     // result holds what every source rank sent to us, in rank order.

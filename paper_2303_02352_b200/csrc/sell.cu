@@ -1081,6 +1081,7 @@ StenArgs sten_args_of(const Sell& S, int block_rows = 256) {
     }
     a.safe_lo = static_cast<int>(lo);
     a.safe_hi = static_cast<int>(hi);
+    a.nblk = static_cast<int>((S.nrows + block_rows - 1) / block_rows);
     a.pf_blocks = env_int("PAIRAMG_PF_BLOCKS", 16 * kSmCount) * 256 / block_rows;
     a.offmax = S.sten_offmax;
     return a;
@@ -1110,8 +1111,11 @@ bool sten_rpt2(const Sell& S, bool dots = false) {
     return S.sten_L == 27 && env_int("PAIRAMG_STEN_RPT27", dots ? 2 : 1) == 2;
 }
 
+inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nblk; }
+
+// cap > 0: at most `cap` CTAs, grid-striding over the logical blocks.
 template <int OP, bool ROWS>
-void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
+void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
     if (sten_rpt2(S)) {
         StenArgs a = sten_args_of(S, 512);
@@ -1119,14 +1123,15 @@ void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
         a.y = a0.y;
         a.r = a0.r;
         a.omega = a0.omega;
+        const int grid = capped(a.nblk, cap);
         if (S.sten_L == 7)
-            launch_k<2>(k_sten2<OP, ROWS, 7>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
+            launch_k<2>(k_sten2<OP, ROWS, 7>, grid, 256, 0, s, a, p);
         else
-            launch_k<2>(k_sten2<OP, ROWS, 27>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
+            launch_k<2>(k_sten2<OP, ROWS, 27>, grid, 256, 0, s, a, p);
         return;
     }
     const StenArgs& a = a0;
-    const int grid = blocks_for(S.nrows, 256);
+    const int grid = capped(a.nblk, cap);
     if (S.sten_L == 7 && sten_center(S))
         launch_k<2>(k_sten<OP, ROWS, 7>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
@@ -1136,7 +1141,7 @@ void launch_sten(const Sell& S, const StenArgs& a0, cudaStream_t s) {
 }
 
 template <bool ROWS>
-void launch_sten_dots(const Sell& S, const StenArgs& a0, cudaStream_t s) {
+int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
     if (sten_rpt2(S, true)) {
         StenArgs a = sten_args_of(S, 512);
@@ -1145,20 +1150,22 @@ void launch_sten_dots(const Sell& S, const StenArgs& a0, cudaStream_t s) {
         a.r = a0.r;
         a.q = a0.q;
         a.partials = a0.partials;
+        const int grid = capped(a.nblk, cap);
         if (S.sten_L == 7)
-            launch_k<2>(k_sten2_dots<ROWS, 7>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
+            launch_k<2>(k_sten2_dots<ROWS, 7>, grid, 256, 0, s, a, p);
         else
-            launch_k<2>(k_sten2_dots<ROWS, 27>, blocks_for(S.nrows, 512), 256, 0, s, a, p);
-        return;
+            launch_k<2>(k_sten2_dots<ROWS, 27>, grid, 256, 0, s, a, p);
+        return grid;
     }
     const StenArgs& a = a0;
-    const int grid = blocks_for(S.nrows, 256);
+    const int grid = capped(a.nblk, cap);
     if (S.sten_L == 7 && sten_center(S))
         launch_k<2>(k_sten_dots<ROWS, 7>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
         launch_k<2>(k_sten_dots<ROWS, 27>, grid, 256, 0, s, a, p);
     else
         launch_k<2>(k_sten_dots<ROWS, 0>, grid, 256, 0, s, a, p);
+    return grid;
 }
 
 PatArgs pat_args_of(const Sell& S) {
@@ -1366,9 +1373,9 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
         const bool rows = a.rows != nullptr;
 #define PB_STEN(OP)                          \
     if (rows)                                \
-        launch_sten<OP, true>(S, a, s);      \
+        launch_sten<OP, true>(S, a, o.max_grid, s);  \
     else                                     \
-        launch_sten<OP, false>(S, a, s);
+        launch_sten<OP, false>(S, a, o.max_grid, s);
         switch (o.op) {
             case kSpmv: PB_STEN(kSpmv) break;
             case kJacobi: PB_STEN(kJacobi) break;
@@ -1470,8 +1477,8 @@ bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, doub
     return true;
 }
 
-int sell_dots_grid(const Sell& S) {
-    if (S.format == Sell::kSten) return blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256);
+int sell_dots_grid(const Sell& S, int cap) {
+    if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256), cap);
     if (S.format == Sell::kDict && S.win.ok) return S.win.grid;
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;
@@ -1479,9 +1486,9 @@ int sell_dots_grid(const Sell& S) {
 }
 
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q, double* partials,
-                   int max_blocks, cudaStream_t s) {
+                   int max_blocks, cudaStream_t s, int cap) {
     if (!S.nrows) return 0;
-    const int grid = sell_dots_grid(S);
+    const int grid = sell_dots_grid(S, cap);
     if (grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: partial buffer too small");
     const bool rows = !S.rows.empty();
     if (S.format == Sell::kSten) {
@@ -1491,11 +1498,9 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
         a.r = r;
         a.q = q;
         a.partials = partials;
-        if (rows)
-            launch_sten_dots<true>(S, a, s);
-        else
-            launch_sten_dots<false>(S, a, s);
+        const int g = rows ? launch_sten_dots<true>(S, a, cap, s) : launch_sten_dots<false>(S, a, cap, s);
         PB_CHECK_LAUNCH();
+        if (g != grid) fail(PAIRAMG_INTERNAL, "sell_spmv_dots: grid mismatch");
         return grid;
     }
     if (S.format == Sell::kPat) {

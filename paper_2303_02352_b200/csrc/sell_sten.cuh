@@ -37,6 +37,7 @@ struct StenArgs {
     int L;
     int safe_lo, safe_hi;  // blocks [safe_lo, safe_hi) gather in range without clamping (contiguous rows)
     int pf_blocks;         // L2 prefetch distance in blocks (0 = off; contiguous rows only)
+    int nblk;              // logical row blocks; the grid may be smaller (grid-stride loop)
     int offmax;
     const double* x;
     double* y;
@@ -109,9 +110,9 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
 // bytes and the x rows its largest offset reaches) into L2, so those first
 // touches overlap this block's latency instead of starting when it runs.
 template <int OP, int BR = 256>
-__device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* own) {
+__device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* own, int blk) {
     if (a.pf_blocks <= 0 || threadIdx.x != 0) return;
-    const int b = static_cast<int>(blockIdx.x) + a.pf_blocks;
+    const int b = blk + a.pf_blocks;
     const int64_t first = static_cast<int64_t>(b) * BR;
     if (first >= a.nrows) return;
     const int64_t row = a.row0 + first;
@@ -125,14 +126,13 @@ __device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* o
 // nrows recompute the last row and do not store (every lane reaches the
 // warp vote).  The clamp test is per block (uniform).
 template <int OP, bool ROWS, int LL>
-__global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant__ StenParam p) {
-    pdl_begin();
-    const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
+__device__ __forceinline__ void sten1_block(const StenArgs& a, const StenParam& p, int blk) {
+    const int i = blk * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
     const int ic = valid ? i : a.nrows - 1;
     const int row = ROWS ? a.rows[ic] : a.row0 + ic;
-    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
-    if (!ROWS) sten_prefetch<OP>(a, a.r);
+    const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+    if (!ROWS) sten_prefetch<OP>(a, a.r, blk);
     const int q = a.pid[row];
     double ri = 0.0, xi = 0.0;
     if (OP != kSpmv) ri = a.r[row];
@@ -147,6 +147,15 @@ __global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant_
         const double t = dsub(ri, sum);  // omega = 1 (the paper's setting) multiplies exactly: skip it
         a.y[row] = dadd(xi, ddiv(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q]));
     }
+}
+
+// Grid-stride over the logical blocks: a capped grid leaves SM slots free for
+// concurrent communication kernels (halo levels).
+template <int OP, bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
+    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+        sten1_block<OP, ROWS, LL>(a, p, blk);
 }
 
 // Two rows per thread (rows t and t + 256 of a 512-row block), every load of
@@ -214,36 +223,41 @@ __device__ __forceinline__ void sten2_body(const StenArgs& a, const StenParam& p
 template <int OP, bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
-    const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
-    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
-    if (!ROWS) sten_prefetch<OP, 512>(a, a.r);
-    if (edge)
-        sten2_body<OP, ROWS, LL, true>(a, p, ia, ia + 256);
-    else
-        sten2_body<OP, ROWS, LL, false>(a, p, ia, ia + 256);
+    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x)) {
+        const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+        const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+        if (!ROWS) sten_prefetch<OP, 512>(a, a.r, blk);
+        if (edge)
+            sten2_body<OP, ROWS, LL, true>(a, p, ia, ia + 256);
+        else
+            sten2_body<OP, ROWS, LL, false>(a, p, ia, ia + 256);
+    }
 }
 
 // v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
 template <bool ROWS, int LL>
-__global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_constant__ StenParam p) {
-    pdl_begin();
-    const int i = static_cast<int>(blockIdx.x) * 256 + static_cast<int>(threadIdx.x);
+__device__ __forceinline__ void sten1_dots_block(const StenArgs& a, const StenParam& p, int blk, double& sa, double& sb,
+                                                 double& sg) {
+    const int i = blk * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
     const int ic = valid ? i : a.nrows - 1;
     const int row = ROWS ? a.rows[ic] : a.row0 + ic;
-    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
-    if (!ROWS) sten_prefetch<-1>(a, a.r);
+    const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+    if (!ROWS) sten_prefetch<-1>(a, a.r, blk);
     const int q = a.pid[row];
     double wi = LL == 0 ? a.x[row] : 0.0;
     const double rr = a.r[row], qq = a.q[row];
     const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge, wi);
-    double sa = 0.0, sb = 0.0, sg = 0.0;
     if (valid) {
         a.y[row] = sum;
-        sa = dmul(wi, rr);
-        sb = dmul(wi, sum);
-        sg = dmul(wi, qq);
+        sa = dadd(sa, dmul(wi, rr));
+        sb = dadd(sb, dmul(wi, sum));
+        sg = dadd(sg, dmul(wi, qq));
     }
+}
+
+// Block sum of the dot triple in a fixed order -> partials[blockIdx.x] (3 doubles).
+__device__ __forceinline__ void dots_block_store(double sa, double sb, double sg, double* partials) {
     for (int o = 16; o; o >>= 1) {
         sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
         sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
@@ -260,8 +274,18 @@ __global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_cons
     if (threadIdx.x < 3) {
         double acc = 0.0;
         for (int k = 0; k < 8; ++k) acc = dadd(acc, red[threadIdx.x][k]);
-        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
+        partials[blockIdx.x * 3 + threadIdx.x] = acc;
     }
+}
+
+// v = A w + per-CTA partials of (w.r, w.v, w.q) (fixed order -> deterministic).
+template <bool ROWS, int LL>
+__global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+        sten1_dots_block<ROWS, LL>(a, p, blk, sa, sb, sg);
+    dots_block_store(sa, sb, sg, a.partials);
 }
 
 // Two rows per thread (rows t and t + 256 of a 512-row block), as k_sten2.
@@ -281,9 +305,9 @@ __device__ __forceinline__ void sten2_dots_body(const StenArgs& a, const StenPar
     const double wa = xa[LL / 2], wb = xb[LL / 2];
     if (va) {
         a.y[ra] = va_;
-        sa = dmul(wa, rra);
-        sb = dmul(wa, va_);
-        sg = dmul(wa, qqa);
+        sa = dadd(sa, dmul(wa, rra));
+        sb = dadd(sb, dmul(wa, va_));
+        sg = dadd(sg, dmul(wa, qqa));
     }
     if (vb) {
         a.y[rb] = vb_;
@@ -296,32 +320,17 @@ __device__ __forceinline__ void sten2_dots_body(const StenArgs& a, const StenPar
 template <bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
-    const int ia = static_cast<int>(blockIdx.x) * 512 + static_cast<int>(threadIdx.x);
-    const bool edge = ROWS || static_cast<int>(blockIdx.x) < a.safe_lo || static_cast<int>(blockIdx.x) >= a.safe_hi;
-    if (!ROWS) sten_prefetch<-1, 512>(a, a.r);
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    if (edge)
-        sten2_dots_body<ROWS, LL, true>(a, p, ia, ia + 256, sa, sb, sg);
-    else
-        sten2_dots_body<ROWS, LL, false>(a, p, ia, ia + 256, sa, sb, sg);
-    for (int o = 16; o; o >>= 1) {
-        sa = dadd(sa, __shfl_down_sync(0xffffffffu, sa, o));
-        sb = dadd(sb, __shfl_down_sync(0xffffffffu, sb, o));
-        sg = dadd(sg, __shfl_down_sync(0xffffffffu, sg, o));
+    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x)) {
+        const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+        const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+        if (!ROWS) sten_prefetch<-1, 512>(a, a.r, blk);
+        if (edge)
+            sten2_dots_body<ROWS, LL, true>(a, p, ia, ia + 256, sa, sb, sg);
+        else
+            sten2_dots_body<ROWS, LL, false>(a, p, ia, ia + 256, sa, sb, sg);
     }
-    __shared__ double red[3][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        red[0][warp] = sa;
-        red[1][warp] = sb;
-        red[2][warp] = sg;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        double acc = 0.0;
-        for (int k = 0; k < 8; ++k) acc = dadd(acc, red[threadIdx.x][k]);
-        a.partials[blockIdx.x * 3 + threadIdx.x] = acc;
-    }
+    dots_block_store(sa, sb, sg, a.partials);
 }
 
 

@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cstdio>
+
 #include "solver.cuh"
 
 namespace pb {
@@ -300,6 +302,7 @@ Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
     fuse = env_flag("PAIRAMG_FUSE", false);
     overlap = env_flag("PAIRAMG_OVERLAP", true);
     bnd_on_comm = env_flag("PAIRAMG_BND_ON_COMM", true);
+    halo_grid_ = kSmCount * env_int("PAIRAMG_HALO_CTAS_PER_SM", 4);
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
@@ -366,6 +369,10 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
     destroy_graph();
     ready = false;
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
+    if (rt.nranks() > 1 && env_flag("PAIRAMG_P2P", true)) {  // collective: every rank, every distributed level
+        const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
+        for (int k = 0; k < nd; ++k) p2p_setup(rt, h.levels[static_cast<size_t>(k)]->A.halo, h.levels[static_cast<size_t>(k)]->p2p, s_);
+    }
     if (env_flag("PAIRAMG_TRANSFER_CODES", true)) {
         auto codes = [&](Level& L) {
             if (L.pval.empty()) return;
@@ -441,8 +448,27 @@ void Solver::end_time(int kc) {
     tcount_[kc] = idx + 1;
 }
 
+void Solver::hrec(cudaEvent_t e, cudaStream_t st) {
+    if (capturing(st))
+        PB_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else
+        PB_CUDA(cudaEventRecord(e, st));
+}
+
 void Solver::collect_times() {
     if (!timing) return;
+    if (hcount_ > 0) {  // PAIRAMG_HALO_TRACE summary (rank, averages in us from the compute-stream start)
+        double acc[4] = {0, 0, 0, 0};
+        for (int i = 0; i < hcount_; ++i)
+            for (int j = 1; j < 5; ++j) {
+                float ms = 0.f;
+                PB_CUDA(cudaEventElapsedTime(&ms, htrace_[static_cast<size_t>(i)][0], htrace_[static_cast<size_t>(i)][j]));
+                acc[j - 1] += ms * 1e3 / hcount_;
+            }
+        std::fprintf(stderr, "halo trace rank %d (%d sweeps): comm start %.1f  exchange done %.1f  boundary done %.1f  interior done %.1f us\n",
+                     rt.rank(), hcount_, acc[0], acc[1], acc[2], acc[3]);
+        hcount_ = 0;
+    }
     for (int kc = 0; kc < kNumClasses; ++kc)
         for (int i = 0; i < tcount_[kc]; ++i) {
             float ms = 0.f;
@@ -458,15 +484,36 @@ Level& Solver::lvl(int k) {
 
 void Solver::apply(int k, const SellOpArgs& o, int kc) { apply_on(lvl(k), o, kc); }
 
+// Halo of x (owned -> slots [n, n + n_halo)): NVLink direct stores when the
+// level's P2P plan is up, else NCCL send/recv.
+void Solver::exchange(Level& L, const double* x, cudaStream_t st) {
+    double* halo = const_cast<double*>(x) + L.A.n;
+    if (L.p2p.ok)
+        p2p_exchange(L.A.halo, L.p2p, x, halo, st);
+    else
+        halo_exchange(rt, L.A.halo, x, halo, st);
+}
+
 void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
     begin_time(kc);
     if (L.A.halo.has_traffic() && !overlap) {
         // exchange first (on the compute stream), then one kernel over all rows
-        halo_exchange(rt, L.A.halo, o.x, const_cast<double*>(o.x) + L.A.n, s_);
+        exchange(L, o.x, s_);
         sell_apply(L.sell_all, o, s_);
         launches_ += 1 + (L.A.halo.send_off.back() ? 1 : 0);
         end_time(kc);
         return;
+    }
+    const bool trace = timing && kc == 0 && L.A.halo.n_halo > 0 && bnd_on_comm && env_flag("PAIRAMG_HALO_TRACE", false);
+    std::array<cudaEvent_t, 5>* tr = nullptr;
+    if (trace) {
+        while (static_cast<int>(htrace_.size()) <= hcount_) {
+            std::array<cudaEvent_t, 5> ev;
+            for (auto& e : ev) PB_CUDA(cudaEventCreate(&e));
+            htrace_.push_back(ev);
+        }
+        tr = &htrace_[static_cast<size_t>(hcount_++)];
+        hrec((*tr)[0], s_);
     }
     if (L.A.halo.has_traffic()) {
         if (o.op == kJacobiZero || o.op == kJacobiProl)
@@ -476,16 +523,25 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         // the compute stream only joins at the end, no second launch on it.
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
-        halo_exchange(rt, L.A.halo, o.x, const_cast<double*>(o.x) + L.A.n, rt.comm_stream());
+        if (tr) hrec((*tr)[1], rt.comm_stream());
+        exchange(L, o.x, rt.comm_stream());
+        if (tr) hrec((*tr)[2], rt.comm_stream());
         if (L.A.halo.n_halo > 0 && bnd_on_comm) {
             sell_apply(L.sell_bnd, o, rt.comm_stream());
             launches_ += 1;
         }
+        if (tr) hrec((*tr)[3], rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += L.A.halo.send_off.back() ? 1 : 0;
     }
     if (L.A.halo.n_halo > 0 && bnd_on_comm) {
-        sell_apply(L.sell_int, o, s_);
+        // capped grid: the interior kernel leaves SM slots to the pack/NCCL/
+        // boundary kernels (else they only run once every interior CTA has
+        // been dispatched; measured: halo done at 91 us of an 89 us interior)
+        SellOpArgs oi = o;
+        oi.max_grid = halo_grid_;
+        sell_apply(L.sell_int, oi, s_);
+        if (tr) hrec((*tr)[4], s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         launches_ += 1;
     } else if (L.A.halo.n_halo > 0) {
@@ -700,18 +756,19 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     // v = A w and the dot triple (Alg. 1 lines 10-13)
     begin_time(2);
     if (L0.A.halo.has_traffic() && !overlap) {
-        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, s_);
+        exchange(L0, w, s_);
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
     } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
-        const int g1 = sell_dots_grid(L0.sell_int);
+        const int g1 = sell_dots_grid(L0.sell_int, halo_grid_);
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
-        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, rt.comm_stream());
+        exchange(L0, w, rt.comm_stream());
         const int g2 = sell_spmv_dots(L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get() + 3 * g1,
                                       max_blocks_ - g1, rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
-        const int g1b = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), g1, s_);
+        const int g1b = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), g1, s_,
+                                       halo_grid_);
         if (g1b != g1) fail(PAIRAMG_INTERNAL, "spmv+dots: interior partial count changed");
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         dots_grid_ = g1 + g2;
@@ -719,7 +776,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     } else if (L0.A.halo.has_traffic()) {  // halo of w in flight while the interior rows run
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
-        halo_exchange(rt, L0.A.halo, w, w + L0.A.n, rt.comm_stream());
+        exchange(L0, w, rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }

@@ -60,6 +60,7 @@ public:
     bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
     bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
     bool bnd_on_comm = true;  // halo boundary rows computed on the comm stream behind the receive
+    int halo_grid_ = 0;       // CTA cap of interior kernels on halo levels (0 = uncapped)
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
@@ -69,6 +70,7 @@ private:
                 bool time_l0);
     void apply(int k, const SellOpArgs& o, int kclass);
     void apply_on(Level& L, const SellOpArgs& o, int kclass);
+    void exchange(Level& L, const double* x, cudaStream_t st);
     bool fusable(int k);
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
@@ -113,6 +115,11 @@ private:
     std::array<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>, kNumClasses> tev_{};
     std::array<int, kNumClasses> tcount_{};
     std::array<int, kNumClasses> topen_{};
+    // PAIRAMG_HALO_TRACE (timing mode): per level-0 halo sweep, events at
+    // {compute start, comm start, exchange done, boundary done, interior done}
+    std::vector<std::array<cudaEvent_t, 5>> htrace_;
+    int hcount_ = 0;
+    void hrec(cudaEvent_t e, cudaStream_t st);
     int64_t launches_ = 0;
 };
 
