@@ -118,6 +118,10 @@ __device__ __forceinline__ void pdl_begin() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Kernels whose blocks may wait on another GPU must not let their dependents
+// launch early (waiting dependent CTAs would hold SM slots).
+__device__ __forceinline__ void pdl_wait_only() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 inline int pdl_mask() {
     static const int m = env_int("PAIRAMG_PDL", 15);  // bits: 1 reductions, 2 row kernels, 4 transfers, 8 FCG update
     return m;

@@ -161,6 +161,24 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s);
 int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, const double* q,
                    double* partials, int max_blocks, cudaStream_t s, int cap = 0);
 int sell_dots_grid(const Sell& S, int cap = 0);
+// Halo delivered by NVLink direct stores (p2p.cu): where the boundary rows of
+// a split launch find it and how they learn it has arrived.
+struct HaloSrc {
+    const unsigned long long* flags = nullptr;  // flag slot per sender rank
+    int nfrom = 0;
+    int from[8] = {};
+    const double* staging = nullptr;            // parity stride nhalo
+    int64_t nhalo = 0;
+    unsigned long long* ctr = nullptr;          // [0] exchanges done, [3] boundary blocks done
+};
+// Interior (contiguous STEN) + boundary (STEN) rows in one launch; the
+// boundary blocks wait for the neighbours' pushes of this exchange.
+bool sell_split_ok(const Sell& interior, const Sell& boundary);
+void sell_apply_split(const Sell& interior, const Sell& boundary, const SellOpArgs& o, const HaloSrc& hs,
+                      cudaStream_t s);
+int sell_split_dots_grid(const Sell& interior, const Sell& boundary);
+int sell_spmv_dots_split(const Sell& interior, const Sell& boundary, const double* w, double* v, const double* r,
+                         const double* q, double* partials, int max_blocks, const HaloSrc& hs, cudaStream_t s);
 // The coarsest level's zero start + nu-1 l1-Jacobi sweeps in one cluster
 // launch (halo-free STEN, <= 16384 rows); false when not applicable.
 bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, double omega, cudaStream_t s);

@@ -164,13 +164,23 @@ void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s) {
         P.peer_flag.clear();
         return;
     }
-    P.ctr.alloc(3, s);
+    P.ctr.alloc(4, s);
     P.ctr.zero(s);
     PB_CUDA(cudaStreamSynchronize(s));
     P.ok = true;
 }
 
-void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s) {
+namespace {
+int p2p_prio() {
+    static int prio = [] {
+        int lo = 0, hi = 0;
+        PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        return env_flag("PAIRAMG_P2P_PRIO", true) ? hi : lo;
+    }();
+    return prio;
+}
+
+void launch_push(const HaloPlan& H, P2PHalo& P, const double* x_owned, cudaStream_t s) {
     const int64_t nsend = H.send_off.empty() ? 0 : H.send_off.back();
     PushArgs pa{};
     pa.npeers = static_cast<int>(H.send_peers.size());
@@ -180,22 +190,13 @@ void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* 
         pa.stride[i] = P.peer_stride[static_cast<size_t>(i)];
         pa.flag[i] = P.peer_flag[static_cast<size_t>(i)];
     }
-    PullArgs pl{};
-    pl.nrecv = static_cast<int>(H.recv_peers.size());
-    for (int i = 0; i < pl.nrecv; ++i) pl.from[i] = H.recv_peers[static_cast<size_t>(i)];
-    // a rank with nothing to send still runs the push (it raises no flag) so
-    // the exchange counters of all ranks advance together
-    // highest scheduling priority on the launch itself: a stream's priority is
-    // not carried into the nodes of a captured graph
-    static int prio = [] {
-        int lo = 0, hi = 0;
-        PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        return env_flag("PAIRAMG_P2P_PRIO", true) ? hi : lo;
-    }();
+    // highest scheduling priority on the launch itself (a stream's priority
+    // is not carried into the nodes of a captured graph); a rank with nothing
+    // to send still runs it so every rank's exchange counter advances alike
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributePriority;
-    at[0].val.priority = prio;
+    at[0].val.priority = p2p_prio();
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cfg.blockDim = dim3(256);
@@ -203,6 +204,35 @@ void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* 
     cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((nsend + 255) / 256, 2 * kSmCount))));
     PB_CUDA(cudaLaunchKernelEx(&cfg, k_p2p_push, x_owned, static_cast<const int32_t*>(H.send_idx.get()), nsend, pa,
                                P.ctr.get()));
+}
+}  // namespace
+
+void p2p_push(const HaloPlan& H, P2PHalo& P, const double* x_owned, cudaStream_t s) { launch_push(H, P, x_owned, s); }
+
+HaloSrc p2p_halo_src(const HaloPlan& H, P2PHalo& P) {
+    HaloSrc hs;
+    hs.flags = P.flags;
+    hs.nfrom = static_cast<int>(std::min<size_t>(H.recv_peers.size(), 8));
+    for (int i = 0; i < hs.nfrom; ++i) hs.from[i] = H.recv_peers[static_cast<size_t>(i)];
+    hs.staging = P.staging;
+    hs.nhalo = H.n_halo;
+    hs.ctr = P.ctr.get();
+    return hs;
+}
+
+void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s) {
+    launch_push(H, P, x_owned, s);
+    PullArgs pl{};
+    pl.nrecv = static_cast<int>(H.recv_peers.size());
+    for (int i = 0; i < pl.nrecv; ++i) pl.from[i] = H.recv_peers[static_cast<size_t>(i)];
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = p2p_prio();
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
     cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((H.n_halo + 255) / 256, kPullBlocks))));
     PB_CUDA(cudaLaunchKernelEx(&cfg, k_p2p_pull, static_cast<const double*>(P.staging),
                                static_cast<const unsigned long long*>(P.flags), H.n_halo, pl, x_halo, P.ctr.get()));

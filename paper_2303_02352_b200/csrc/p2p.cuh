@@ -28,7 +28,7 @@ struct P2PHalo {
     std::vector<int64_t> peer_stride;          // per send peer: its n_halo (parity stride)
     std::vector<unsigned long long*> peer_flag;  // per send peer: its flags[my rank]
     std::vector<void*> opened;                 // IPC mappings to close
-    DBuf<unsigned long long> ctr;              // [0] exchanges done, [1] push blocks done, [2] pull blocks done
+    DBuf<unsigned long long> ctr;              // [0] exchanges done, [1] push / [2] pull / [3] split blocks done
     DBuf<double*> d_peer_staging;              // device copies of the per-peer tables
     DBuf<int64_t> d_peer_stride;
     DBuf<unsigned long long*> d_peer_flag;
@@ -41,5 +41,9 @@ void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s);
 void p2p_destroy(P2PHalo& P);
 // x_halo <- the owners' x (push from every rank, then pull), on stream s.
 void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s);
+// Push only: the consumer is a split launch reading the staging slot itself
+// (sell_apply_split / sell_spmv_dots_split with p2p_halo_src).
+void p2p_push(const HaloPlan& H, P2PHalo& P, const double* x_owned, cudaStream_t s);
+HaloSrc p2p_halo_src(const HaloPlan& H, P2PHalo& P);
 
 }  // namespace pb

@@ -1477,6 +1477,108 @@ bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, doub
     return true;
 }
 
+bool sell_split_ok(const Sell& I, const Sell& B) {
+    return I.format == Sell::kSten && B.format == Sell::kSten && I.rows.empty() && I.nrows > 0 && B.nrows > 0 &&
+           env_flag("PAIRAMG_HALO_SPLIT", true);
+}
+
+namespace {
+struct SplitPlan {
+    StenArgs a;
+    HaloSplit h;
+    int la;
+    bool r2;
+    int grid;
+};
+
+SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs) {
+    SplitPlan P{};
+    P.la = (I.sten_L == 7 || I.sten_L == 27) && sten_center(I) ? I.sten_L : 0;
+    P.r2 = P.la != 0 && sten_rpt2(I, dots);
+    P.a = sten_args_of(I, P.r2 ? 512 : 256);
+    P.h.pa = sten_param(I);
+    P.h.pb = sten_param(B);
+    P.h.b = sten_args_of(B);
+    P.h.nblk_a = P.a.nblk;
+    P.h.nblk_b = P.h.b.nblk;
+    P.grid = P.h.nblk_a + P.h.nblk_b;
+    if (hs) {
+        P.h.flags = hs->flags;
+        P.h.nfrom = hs->nfrom;
+        for (int i = 0; i < 8; ++i) P.h.from[i] = hs->from[i];
+        P.h.staging = hs->staging;
+        P.h.nhalo = hs->nhalo;
+        P.h.ctr = hs->ctr;
+        P.h.b.nown = static_cast<int>(I.xlen - hs->nhalo);
+    }
+    return P;
+}
+}  // namespace
+
+void sell_apply_split(const Sell& I, const Sell& B, const SellOpArgs& o, const HaloSrc& hs, cudaStream_t s) {
+    SplitPlan P = split_plan(I, B, false, &hs);
+    for (StenArgs* a : {&P.a, &P.h.b}) {
+        a->x = o.x;
+        a->y = o.y;
+        a->r = o.r;
+        a->omega = o.omega;
+    }
+    const bool br = !B.rows.empty();
+#define PB_SPLIT2(OP, BR)                                                                                 \
+    if (P.la == 7 && P.r2) launch_k<2>(k_sten_split<OP, 7, true, BR>, P.grid, 256, 0, s, P.a, P.h);        \
+    else if (P.la == 7) launch_k<2>(k_sten_split<OP, 7, false, BR>, P.grid, 256, 0, s, P.a, P.h);         \
+    else if (P.la == 27 && P.r2) launch_k<2>(k_sten_split<OP, 27, true, BR>, P.grid, 256, 0, s, P.a, P.h);  \
+    else if (P.la == 27) launch_k<2>(k_sten_split<OP, 27, false, BR>, P.grid, 256, 0, s, P.a, P.h);       \
+    else launch_k<2>(k_sten_split<OP, 0, false, BR>, P.grid, 256, 0, s, P.a, P.h);
+#define PB_SPLIT(OP)      \
+    if (br) {             \
+        PB_SPLIT2(OP, true)  \
+    } else {              \
+        PB_SPLIT2(OP, false) \
+    }
+    switch (o.op) {
+        case kSpmv: PB_SPLIT(kSpmv) break;
+        case kJacobi: PB_SPLIT(kJacobi) break;
+        case kResid: PB_SPLIT(kResid) break;
+        default: fail(PAIRAMG_INTERNAL, "sell_apply_split: bad op");
+    }
+#undef PB_SPLIT
+#undef PB_SPLIT2
+}
+
+int sell_split_dots_grid(const Sell& I, const Sell& B) { return split_plan(I, B, true, nullptr).grid; }
+
+int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* v, const double* r, const double* q,
+                         double* partials, int max_blocks, const HaloSrc& hs, cudaStream_t s) {
+    SplitPlan P = split_plan(I, B, true, &hs);
+    if (P.grid > max_blocks) fail(PAIRAMG_INTERNAL, "sell_spmv_dots_split: partial buffer too small");
+    for (StenArgs* a : {&P.a, &P.h.b}) {
+        a->x = w;
+        a->y = v;
+        a->r = r;
+        a->q = q;
+        a->partials = partials;
+    }
+    const bool br = !B.rows.empty();
+    auto go = [&](auto kt, auto kf) {
+        if (br)
+            launch_k<2>(kt, P.grid, 256, 0, s, P.a, P.h);
+        else
+            launch_k<2>(kf, P.grid, 256, 0, s, P.a, P.h);
+    };
+    if (P.la == 7 && P.r2)
+        go(k_sten_split_dots<7, true, true>, k_sten_split_dots<7, true, false>);
+    else if (P.la == 7)
+        go(k_sten_split_dots<7, false, true>, k_sten_split_dots<7, false, false>);
+    else if (P.la == 27 && P.r2)
+        go(k_sten_split_dots<27, true, true>, k_sten_split_dots<27, true, false>);
+    else if (P.la == 27)
+        go(k_sten_split_dots<27, false, true>, k_sten_split_dots<27, false, false>);
+    else
+        go(k_sten_split_dots<0, false, true>, k_sten_split_dots<0, false, false>);
+    return P.grid;
+}
+
 int sell_dots_grid(const Sell& S, int cap) {
     if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256), cap);
     if (S.format == Sell::kDict && S.win.ok) return S.win.grid;

@@ -45,13 +45,15 @@ struct StenArgs {
     double omega;
     const double* q;
     double* partials;
+    const double* hsrc;  // boundary rows of a split launch: columns >= nown read hsrc[c - nown]
+    int nown;
 };
 
 // Row sum over the main pattern; LL = compile-time record count (0 = generic,
 // runtime a.L <= kStenMax).  EDGE clamps the gather columns into [0, xlen).
 // With LL > 0 the launcher guarantees record LL/2 is the diagonal (offset
 // 0, sorted symmetric stencil), so its gather doubles as the row's own x.
-template <int LL, bool EDGE>
+template <int LL, bool EDGE, bool HALO = false>
 __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m,
                                                double& own) {
     if constexpr (LL == 0) {
@@ -63,7 +65,7 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenPara
             for (int j = 0; j < 8; ++j) {
                 int c = row + (k0 + j < a.L ? p.off[k0 + j] : 0);
                 if (EDGE) c = min(max(c, 0), a.xlen - 1);
-                xv[j] = a.x[c];
+                xv[j] = (HALO && c >= a.nown) ? __ldcv(a.hsrc + (c - a.nown)) : a.x[c];
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -96,10 +98,10 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenPara
     }
 }
 
-template <int LL>
+template <int LL, bool HALO = false>
 __device__ __forceinline__ double sten_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m, bool edge,
                                            double& own) {
-    return edge ? sten_row_sum<LL, true>(a, p, row, m, own) : sten_row_sum<LL, false>(a, p, row, m, own);
+    return edge ? sten_row_sum<LL, true, HALO>(a, p, row, m, own) : sten_row_sum<LL, false, HALO>(a, p, row, m, own);
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
@@ -125,7 +127,7 @@ __device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* o
 // One thread per row (32-bit indices: a Sell holds < 2^31 rows); rows past
 // nrows recompute the last row and do not store (every lane reaches the
 // warp vote).  The clamp test is per block (uniform).
-template <int OP, bool ROWS, int LL>
+template <int OP, bool ROWS, int LL, bool HALO = false>
 __device__ __forceinline__ void sten1_block(const StenArgs& a, const StenParam& p, int blk) {
     const int i = blk * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
@@ -137,7 +139,7 @@ __device__ __forceinline__ void sten1_block(const StenArgs& a, const StenParam& 
     double ri = 0.0, xi = 0.0;
     if (OP != kSpmv) ri = a.r[row];
     if (OP == kJacobi && LL == 0) xi = a.x[row];
-    const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge, xi);
+    const double sum = sten_sum<LL, HALO>(a, p, row, p.pmask[q], edge, xi);
     if (!valid) return;
     if (OP == kSpmv) {
         a.y[row] = sum;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant
 }
 
 // v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
-template <bool ROWS, int LL>
+template <bool ROWS, int LL, bool HALO = false>
 __device__ __forceinline__ void sten1_dots_block(const StenArgs& a, const StenParam& p, int blk, double& sa, double& sb,
                                                  double& sg) {
     const int i = blk * 256 + static_cast<int>(threadIdx.x);
@@ -247,7 +249,7 @@ __device__ __forceinline__ void sten1_dots_block(const StenArgs& a, const StenPa
     const int q = a.pid[row];
     double wi = LL == 0 ? a.x[row] : 0.0;
     const double rr = a.r[row], qq = a.q[row];
-    const double sum = sten_sum<LL>(a, p, row, p.pmask[q], edge, wi);
+    const double sum = sten_sum<LL, HALO>(a, p, row, p.pmask[q], edge, wi);
     if (valid) {
         a.y[row] = sum;
         sa = dadd(sa, dmul(wi, rr));
@@ -407,3 +409,108 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
     for (int h = 0; h < 2; ++h)
         if (rowv[h] >= 0) out[rowv[h]] = xs[fin][rowv[h] - me * R];
 }
+
+// ---------------------------------------------------------------------------
+// Interior + halo-boundary rows of a halo level in ONE launch, with the halo
+// delivered by NVLink direct stores (p2p.cu).  Order on the compute stream:
+// push (this rank's boundary values into the neighbours' staging), then this
+// kernel.  Boundary blocks (the lowest block ids, dispatched first) wait
+// until every neighbour's flag shows this exchange, then gather
+// halo columns straight from the staging slot of its parity.  A neighbour's
+// push for exchange k is issued before its own kernel k, so a waiting block
+// only waits on work that is already enqueued ahead of everything on the
+// other GPU: no deadlock, whatever holds SM slots here.  The last boundary
+// block advances the exchange counter (read by the next push).
+struct HaloSplit {
+    StenParam pa, pb;          // interior / boundary main patterns
+    StenArgs b;                // boundary rows (list, or range on an end rank)
+    int nblk_a, nblk_b;
+    const unsigned long long* flags;  // this rank's flag slots (indexed by sender)
+    int nfrom;
+    int from[8];
+    const double* staging;     // this rank's staging, parity stride nhalo
+    int64_t nhalo;
+    unsigned long long* ctr;   // [0] exchanges done, [3] boundary blocks done
+};
+
+__device__ __forceinline__ const double* halo_wait_p2p(const HaloSplit& h) {
+    const unsigned long long e = h.ctr[0];
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < h.nfrom; ++k) {
+            long long spins = 0;
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(h.flags + h.from[k]) : "memory");
+                if (v < e + 1) __nanosleep(64);
+                if (++spins == (1ll << 28)) {
+                    printf("pairamg: halo flag wait timed out\n");
+                    __trap();
+                }
+            } while (v < e + 1);
+        }
+    }
+    __syncthreads();
+    return h.staging + static_cast<int64_t>(e & 1ull) * h.nhalo;
+}
+
+__device__ __forceinline__ void halo_done_p2p(const HaloSplit& h) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&h.ctr[3], 1ull) == static_cast<unsigned long long>(h.nblk_b) - 1) {
+        h.ctr[3] = 0;
+        h.ctr[0] = h.ctr[0] + 1;
+    }
+}
+
+template <int OP, int LLA, bool R2, bool BROWS>
+__global__ void __launch_bounds__(256) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
+    pdl_wait_only();  // no early dependents: the boundary blocks wait on another GPU
+    // boundary blocks first: dispatched at once, their short wait for the
+    // neighbours' pushes and their slower generic rows overlap the interior
+    const int blk = static_cast<int>(blockIdx.x) - h.nblk_b;
+    if (blk >= 0) {
+        if constexpr (R2) {
+            const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+            const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
+            sten_prefetch<OP, 512>(a, a.r, blk);
+            if (edge)
+                sten2_body<OP, false, LLA, true>(a, h.pa, ia, ia + 256);
+            else
+                sten2_body<OP, false, LLA, false>(a, h.pa, ia, ia + 256);
+        } else {
+            sten1_block<OP, false, LLA>(a, h.pa, blk);
+        }
+        return;
+    }
+    StenArgs b = h.b;
+    b.hsrc = halo_wait_p2p(h);
+    sten1_block<OP, BROWS, 0, true>(b, h.pb, static_cast<int>(blockIdx.x));
+    halo_done_p2p(h);
+}
+
+template <int LLA, bool R2, bool BROWS>
+__global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
+    pdl_wait_only();
+    const int blk = static_cast<int>(blockIdx.x) - h.nblk_b;  // boundary blocks first
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (blk >= 0) {
+        if constexpr (R2) {
+            const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+            const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
+            sten_prefetch<-1, 512>(a, a.r, blk);
+            if (edge)
+                sten2_dots_body<false, LLA, true>(a, h.pa, ia, ia + 256, sa, sb, sg);
+            else
+                sten2_dots_body<false, LLA, false>(a, h.pa, ia, ia + 256, sa, sb, sg);
+        } else {
+            sten1_dots_block<false, LLA>(a, h.pa, blk, sa, sb, sg);
+        }
+        dots_block_store(sa, sb, sg, a.partials);
+        return;
+    }
+    StenArgs b = h.b;
+    b.hsrc = halo_wait_p2p(h);
+    sten1_dots_block<BROWS, 0, true>(b, h.pb, static_cast<int>(blockIdx.x), sa, sb, sg);
+    dots_block_store(sa, sb, sg, a.partials);
+    halo_done_p2p(h);
+}
+

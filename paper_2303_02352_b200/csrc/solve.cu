@@ -402,6 +402,8 @@ void Solver::ensure_vectors() {
     int64_t dots_blocks = sell_dots_grid(L0.sell_all);
     if (L0.A.halo.n_halo > 0)
         dots_blocks = std::max<int64_t>(dots_blocks, int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd));
+        if (sell_split_ok(L0.sell_int, L0.sell_bnd))
+            dots_blocks = std::max<int64_t>(dots_blocks, sell_split_dots_grid(L0.sell_int, L0.sell_bnd));
     max_blocks_ = static_cast<int>(std::max<int64_t>(dots_blocks, kSmCount * 8));
     partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
     stage_.alloc(static_cast<size_t>(3 * kStage), s_);
@@ -514,6 +516,16 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         }
         tr = &htrace_[static_cast<size_t>(hcount_++)];
         hrec((*tr)[0], s_);
+    }
+    if (L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.sell_bnd) &&
+        (o.op == kSpmv || o.op == kJacobi || o.op == kResid)) {
+        // push this rank's boundary values into the neighbours, then one
+        // launch whose boundary blocks wait for theirs (no comm stream)
+        p2p_push(L.A.halo, L.p2p, o.x, s_);
+        sell_apply_split(L.sell_int, L.sell_bnd, o, p2p_halo_src(L.A.halo, L.p2p), s_);
+        launches_ += 2;
+        end_time(kc);
+        return;
     }
     if (L.A.halo.has_traffic()) {
         if (o.op == kJacobiZero || o.op == kJacobiProl)
@@ -759,6 +771,11 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         exchange(L0, w, s_);
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
+    } else if (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.sell_bnd)) {
+        p2p_push(L0.A.halo, L0.p2p, w, s_);
+        dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get(),
+                                          max_blocks_, p2p_halo_src(L0.A.halo, L0.p2p), s_);
+        launches_ += 2;
     } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
         const int g1 = sell_dots_grid(L0.sell_int, halo_grid_);
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
@@ -780,7 +797,8 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }
-    if ((L0.A.halo.has_traffic() && !overlap) || (L0.A.halo.n_halo > 0 && bnd_on_comm)) {
+    if ((L0.A.halo.has_traffic() && !overlap) || (L0.A.halo.n_halo > 0 && bnd_on_comm) ||
+        (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.sell_bnd))) {
         // done above
     } else if (L0.A.halo.n_halo > 0) {
         const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
