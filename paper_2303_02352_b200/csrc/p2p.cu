@@ -238,4 +238,111 @@ void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* 
                                static_cast<const unsigned long long*>(P.flags), H.n_halo, pl, x_halo, P.ctr.get()));
 }
 
+// ---- small allgather ------------------------------------------------------
+
+namespace {
+__global__ void k_p2p_allgather(const double* send, double* recv, int K, int nranks, int rank, double* const* peer_mail,
+                                unsigned long long* const* peer_flags, const double* my_mail,
+                                const unsigned long long* my_flags, int kmax, unsigned long long* ctr) {
+    pdl_wait_only();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long e = ctr[0];
+    const int64_t par = static_cast<int64_t>(e & 1ull) * nranks * kmax;
+    for (int r = 0; r < nranks; ++r)
+        for (int k = 0; k < K; ++k) peer_mail[r][par + rank * kmax + k] = send[k];
+    __threadfence_system();
+    for (int r = 0; r < nranks; ++r) st_release_sys(peer_flags[r] + rank, e + 1);
+    for (int r = 0; r < nranks; ++r) {
+        long long spins = 0;
+        while (ld_acquire_sys(my_flags + r) < e + 1) {
+            __nanosleep(32);
+            if (++spins == (1ll << 28)) {
+                printf("pairamg: p2p allgather flag wait timed out\n");
+                __trap();
+            }
+        }
+    }
+    for (int r = 0; r < nranks; ++r)
+        for (int k = 0; k < K; ++k) recv[r * K + k] = __ldcv(my_mail + par + r * kmax + k);
+    ctr[0] = e + 1;
+}
+}  // namespace
+
+P2PGather::~P2PGather() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    if (mail) cudaFree(mail);
+    if (flags) cudaFree(flags);
+}
+
+void p2p_gather_setup(Runtime& rt, P2PGather& G, int kmax, cudaStream_t s) {
+    if (rt.nranks() == 1 || G.mail) return;  // set up once per solver (re-setups keep it)
+    G.ok = false;
+    G.nranks = rt.nranks();
+    G.rank = rt.rank();
+    G.kmax = kmax;
+    struct GBlob {
+        cudaIpcMemHandle_t mail, flags;
+        int32_t ok;
+    } mine;
+    std::memset(&mine, 0, sizeof mine);
+    const size_t mbytes = 8 * 2 * static_cast<size_t>(G.nranks) * kmax;
+    mine.ok = cudaMalloc(&G.mail, mbytes) == cudaSuccess && cudaMalloc(&G.flags, 8 * G.nranks) == cudaSuccess &&
+              cudaMemset(G.flags, 0, 8 * G.nranks) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.mail, G.mail) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.flags, G.flags) == cudaSuccess;
+    cudaGetLastError();
+    const std::vector<uint8_t> all = rt.allgather_bytes(&mine, sizeof mine);
+    std::vector<GBlob> blobs(static_cast<size_t>(G.nranks));
+    std::memcpy(blobs.data(), all.data(), all.size());
+    bool ok = true;
+    for (const GBlob& b : blobs) ok = ok && b.ok;
+    for (int r = 0; ok && r < G.nranks; ++r) {
+        if (r == G.rank) {
+            G.peer_mail.push_back(G.mail);
+            G.peer_flags.push_back(G.flags);
+            continue;
+        }
+        void* m = nullptr;
+        void* f = nullptr;
+        if (cudaIpcOpenMemHandle(&m, blobs[static_cast<size_t>(r)].mail, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&f, blobs[static_cast<size_t>(r)].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+        }
+        G.opened.push_back(m);
+        G.opened.push_back(f);
+        G.peer_mail.push_back(static_cast<double*>(m));
+        G.peer_flags.push_back(static_cast<unsigned long long*>(f));
+    }
+    if (rt.allreduce_sum_i64(ok ? 1 : 0) != G.nranks) return;  // all or none
+    G.ctr.alloc(1, s);
+    G.ctr.zero(s);
+    G.d_peer_mail.alloc(static_cast<size_t>(G.nranks), s);
+    G.d_peer_flags.alloc(static_cast<size_t>(G.nranks), s);
+    PB_CUDA(cudaMemcpyAsync(G.d_peer_mail.get(), G.peer_mail.data(), 8 * G.nranks, cudaMemcpyHostToDevice, s));
+    PB_CUDA(cudaMemcpyAsync(G.d_peer_flags.get(), G.peer_flags.data(), 8 * G.nranks, cudaMemcpyHostToDevice, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    G.ok = true;
+}
+
+void p2p_allgather(P2PGather& G, const double* send, double* recv, int K, cudaStream_t s) {
+    if (!G.ok || K > G.kmax) fail(PAIRAMG_INTERNAL, "p2p_allgather: not set up");
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = p2p_prio();
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = s;
+    PB_CUDA(cudaLaunchKernelEx(&cfg, k_p2p_allgather, send, recv, K, G.nranks, G.rank,
+                               static_cast<double* const*>(G.d_peer_mail.get()),
+                               static_cast<unsigned long long* const*>(G.d_peer_flags.get()),
+                               static_cast<const double*>(G.mail), static_cast<const unsigned long long*>(G.flags),
+                               G.kmax, G.ctr.get()));
+}
+
 }  // namespace pb
+

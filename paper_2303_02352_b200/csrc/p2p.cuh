@@ -46,4 +46,26 @@ void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* 
 void p2p_push(const HaloPlan& H, P2PHalo& P, const double* x_owned, cudaStream_t s);
 HaloSrc p2p_halo_src(const HaloPlan& H, P2PHalo& P);
 
+// Small allgather (the FCG dot partials) by NVLink stores: every rank writes
+// its K doubles into every rank's mailbox (parity double-buffered), raises
+// its flag there, waits for all flags, copies the mailbox out in rank order.
+struct P2PGather {
+    bool ok = false;
+    int nranks = 0, rank = 0, kmax = 0;
+    double* mail = nullptr;                      // 2 * nranks * kmax (IPC-exported)
+    unsigned long long* flags = nullptr;         // nranks (IPC-exported)
+    std::vector<double*> peer_mail;              // per rank (own: local pointer)
+    std::vector<unsigned long long*> peer_flags;
+    std::vector<void*> opened;
+    DBuf<unsigned long long> ctr;                // [0] gathers done
+    DBuf<double*> d_peer_mail;
+    DBuf<unsigned long long*> d_peer_flags;
+    ~P2PGather();
+};
+
+void p2p_gather_setup(Runtime& rt, P2PGather& G, int kmax, cudaStream_t s);
+// recv[r*K + k] = rank r's send[k], on stream s (device-side, graph-capturable).
+void p2p_allgather(P2PGather& G, const double* send, double* recv, int K, cudaStream_t s);
+
 }  // namespace pb
+

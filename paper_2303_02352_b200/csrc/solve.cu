@@ -369,6 +369,8 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
     destroy_graph();
     ready = false;
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
+    if (rt.nranks() > 1 && env_flag("PAIRAMG_P2P", true) && env_flag("PAIRAMG_P2P_DOTS", true))
+        p2p_gather_setup(rt, dots_gather_, 4, s_);  // collective
     if (rt.nranks() > 1 && env_flag("PAIRAMG_P2P", true)) {  // collective: every rank, every distributed level
         const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
         for (int k = 0; k < nd; ++k) p2p_setup(rt, h.levels[static_cast<size_t>(k)]->A.halo, h.levels[static_cast<size_t>(k)]->p2p, s_);
@@ -709,7 +711,10 @@ void Solver::reduce_dots_enqueue() {
     PB_CHECK_LAUNCH();
     const double* g = local_.get();
     if (p > 1) {
-        rt.allgather_f64(local_.get(), gathered_.get(), 3, s_);
+        if (dots_gather_.ok)
+            p2p_allgather(dots_gather_, local_.get(), gathered_.get(), 3, s_);
+        else
+            rt.allgather_f64(local_.get(), gathered_.get(), 3, s_);
         g = gathered_.get();
     }
     launch_k(k_fcg_scalars, 1, 32, 0, s_, g, p, state_.get());
@@ -723,7 +728,10 @@ void Solver::reduce_norm_enqueue(bool init) {
     PB_CHECK_LAUNCH();
     const double* g = local_.get() + 3;
     if (p > 1) {
-        rt.allgather_f64(local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
+        if (dots_gather_.ok)
+            p2p_allgather(dots_gather_, local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
+        else
+            rt.allgather_f64(local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
         g = gathered_.get() + 3 * p;
     }
     launch_k(k_norm_final, 1, 32, 0, s_, g, p, state_.get(), init ? 1 : 0);

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "amg.cuh"
+#include "p2p.cuh"
 
 namespace pb {
 
@@ -61,6 +62,7 @@ public:
     bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
     bool bnd_on_comm = true;  // halo boundary rows computed on the comm stream behind the receive
     int halo_grid_ = 0;       // CTA cap of interior kernels on halo levels (0 = uncapped)
+    P2PGather dots_gather_;   // NVLink allgather of the per-iteration dot partials
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
