@@ -1117,20 +1117,6 @@ inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nb
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
-    const int rpt = env_int("PAIRAMG_STEN_RPT", 2);
-    if (S.sten_L == 7 && sten_center(S) && (rpt == 3 || rpt == 4)) {  // experimental: more rows per thread
-        StenArgs a = sten_args_of(S, 256 * rpt);
-        a.x = a0.x;
-        a.y = a0.y;
-        a.r = a0.r;
-        a.omega = a0.omega;
-        const int grid = capped(a.nblk, cap);
-        if (rpt == 3)
-            launch_k<2>(k_stenR<OP, ROWS, 7, 3>, grid, 256, 0, s, a, p);
-        else
-            launch_k<2>(k_stenR<OP, ROWS, 7, 4>, grid, 256, 0, s, a, p);
-        return;
-    }
     if (sten_rpt2(S)) {
         StenArgs a = sten_args_of(S, 512);
         a.x = a0.x;

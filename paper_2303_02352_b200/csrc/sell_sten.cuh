@@ -222,43 +222,6 @@ __device__ __forceinline__ void sten2_body(const StenArgs& a, const StenParam& p
     if (vb) sten_store<OP, LL>(a, p, rb, qb, rib, xb[LL / 2], sb);
 }
 
-// R rows per thread (rows t, t + 256, ... of a 256R-row block), all loads
-// issued before the first multiply.
-template <int OP, bool ROWS, int LL, bool EDGE, int R>
-__device__ __forceinline__ void stenR_body(const StenArgs& a, const StenParam& p, int i0) {
-    int rw[R], q[R];
-    bool v[R];
-    double ri[R], xv[R][LL];
-#pragma unroll
-    for (int h = 0; h < R; ++h) {
-        const int i = i0 + 256 * h;
-        v[h] = i < a.nrows;
-        rw[h] = ROWS ? a.rows[v[h] ? i : a.nrows - 1] : a.row0 + (v[h] ? i : a.nrows - 1);
-        q[h] = a.pid[rw[h]];
-        ri[h] = OP != kSpmv ? a.r[rw[h]] : 0.0;
-        sten_load<LL, EDGE>(a, p, rw[h], xv[h]);
-    }
-#pragma unroll
-    for (int h = 0; h < R; ++h) {
-        const double sm = sten_fold<LL>(p, xv[h], p.pmask[q[h]]);
-        if (v[h]) sten_store<OP, LL>(a, p, rw[h], q[h], ri[h], xv[h][LL / 2], sm);
-    }
-}
-
-template <int OP, bool ROWS, int LL, int R>
-__global__ void __launch_bounds__(256) k_stenR(StenArgs a, const __grid_constant__ StenParam p) {
-    pdl_begin();
-    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x)) {
-        const int i0 = blk * 256 * R + static_cast<int>(threadIdx.x);
-        const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
-        if (!ROWS) sten_prefetch<OP, 256 * R>(a, a.r, blk);
-        if (edge)
-            stenR_body<OP, ROWS, LL, true, R>(a, p, i0);
-        else
-            stenR_body<OP, ROWS, LL, false, R>(a, p, i0);
-    }
-}
-
 template <int OP, bool ROWS, int LL>
 __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
