@@ -1124,20 +1124,22 @@ void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
         a.r = a0.r;
         a.omega = a0.omega;
         const int grid = capped(a.nblk, cap);
+        const bool gs = grid < a.nblk;
         if (S.sten_L == 7)
-            launch_k<2>(k_sten2<OP, ROWS, 7>, grid, 256, 0, s, a, p);
+            launch_k<2>(gs ? k_sten2<OP, ROWS, 7, true> : k_sten2<OP, ROWS, 7, false>, grid, 256, 0, s, a, p);
         else
-            launch_k<2>(k_sten2<OP, ROWS, 27>, grid, 256, 0, s, a, p);
+            launch_k<2>(gs ? k_sten2<OP, ROWS, 27, true> : k_sten2<OP, ROWS, 27, false>, grid, 256, 0, s, a, p);
         return;
     }
     const StenArgs& a = a0;
     const int grid = capped(a.nblk, cap);
+    const bool gs = grid < a.nblk;
     if (S.sten_L == 7 && sten_center(S))
-        launch_k<2>(k_sten<OP, ROWS, 7>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten<OP, ROWS, 7, true> : k_sten<OP, ROWS, 7, false>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
-        launch_k<2>(k_sten<OP, ROWS, 27>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten<OP, ROWS, 27, true> : k_sten<OP, ROWS, 27, false>, grid, 256, 0, s, a, p);
     else
-        launch_k<2>(k_sten<OP, ROWS, 0>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten<OP, ROWS, 0, true> : k_sten<OP, ROWS, 0, false>, grid, 256, 0, s, a, p);
 }
 
 template <bool ROWS>
@@ -1151,20 +1153,22 @@ int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s)
         a.q = a0.q;
         a.partials = a0.partials;
         const int grid = capped(a.nblk, cap);
+        const bool gs = grid < a.nblk;
         if (S.sten_L == 7)
-            launch_k<2>(k_sten2_dots<ROWS, 7>, grid, 256, 0, s, a, p);
+            launch_k<2>(gs ? k_sten2_dots<ROWS, 7, true> : k_sten2_dots<ROWS, 7, false>, grid, 256, 0, s, a, p);
         else
-            launch_k<2>(k_sten2_dots<ROWS, 27>, grid, 256, 0, s, a, p);
+            launch_k<2>(gs ? k_sten2_dots<ROWS, 27, true> : k_sten2_dots<ROWS, 27, false>, grid, 256, 0, s, a, p);
         return grid;
     }
     const StenArgs& a = a0;
     const int grid = capped(a.nblk, cap);
+    const bool gs = grid < a.nblk;
     if (S.sten_L == 7 && sten_center(S))
-        launch_k<2>(k_sten_dots<ROWS, 7>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten_dots<ROWS, 7, true> : k_sten_dots<ROWS, 7, false>, grid, 256, 0, s, a, p);
     else if (S.sten_L == 27 && sten_center(S))
-        launch_k<2>(k_sten_dots<ROWS, 27>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten_dots<ROWS, 27, true> : k_sten_dots<ROWS, 27, false>, grid, 256, 0, s, a, p);
     else
-        launch_k<2>(k_sten_dots<ROWS, 0>, grid, 256, 0, s, a, p);
+        launch_k<2>(gs ? k_sten_dots<ROWS, 0, true> : k_sten_dots<ROWS, 0, false>, grid, 256, 0, s, a, p);
     return grid;
 }
 

@@ -153,11 +153,17 @@ __device__ __forceinline__ void sten1_block(const StenArgs& a, const StenParam& 
 
 // Grid-stride over the logical blocks: a capped grid leaves SM slots free for
 // concurrent communication kernels (halo levels).
-template <int OP, bool ROWS, int LL>
+// GS: grid-stride over the logical blocks (a capped grid leaves SM slots to
+// concurrent kernels); the one-block-per-CTA form keeps fewer registers.
+template <int OP, bool ROWS, int LL, bool GS = false>
 __global__ void __launch_bounds__(256) k_sten(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
-    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
-        sten1_block<OP, ROWS, LL>(a, p, blk);
+    if constexpr (GS) {
+        for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+            sten1_block<OP, ROWS, LL>(a, p, blk);
+    } else {
+        sten1_block<OP, ROWS, LL>(a, p, static_cast<int>(blockIdx.x));
+    }
 }
 
 // Two rows per thread (rows t and t + 256 of a 512-row block), every load of
@@ -223,16 +229,24 @@ __device__ __forceinline__ void sten2_body(const StenArgs& a, const StenParam& p
 }
 
 template <int OP, bool ROWS, int LL>
+__device__ __forceinline__ void sten2_block(const StenArgs& a, const StenParam& p, int blk) {
+    const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+    const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+    if (!ROWS) sten_prefetch<OP, 512>(a, a.r, blk);
+    if (edge)
+        sten2_body<OP, ROWS, LL, true>(a, p, ia, ia + 256);
+    else
+        sten2_body<OP, ROWS, LL, false>(a, p, ia, ia + 256);
+}
+
+template <int OP, bool ROWS, int LL, bool GS = false>
 __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
-    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x)) {
-        const int ia = blk * 512 + static_cast<int>(threadIdx.x);
-        const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
-        if (!ROWS) sten_prefetch<OP, 512>(a, a.r, blk);
-        if (edge)
-            sten2_body<OP, ROWS, LL, true>(a, p, ia, ia + 256);
-        else
-            sten2_body<OP, ROWS, LL, false>(a, p, ia, ia + 256);
+    if constexpr (GS) {
+        for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+            sten2_block<OP, ROWS, LL>(a, p, blk);
+    } else {
+        sten2_block<OP, ROWS, LL>(a, p, static_cast<int>(blockIdx.x));
     }
 }
 
@@ -281,12 +295,16 @@ __device__ __forceinline__ void dots_block_store(double sa, double sb, double sg
 }
 
 // v = A w + per-CTA partials of (w.r, w.v, w.q) (fixed order -> deterministic).
-template <bool ROWS, int LL>
+template <bool ROWS, int LL, bool GS = false>
 __global__ void __launch_bounds__(256) k_sten_dots(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
-        sten1_dots_block<ROWS, LL>(a, p, blk, sa, sb, sg);
+    if constexpr (GS) {
+        for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+            sten1_dots_block<ROWS, LL>(a, p, blk, sa, sb, sg);
+    } else {
+        sten1_dots_block<ROWS, LL>(a, p, static_cast<int>(blockIdx.x), sa, sb, sg);
+    }
     dots_block_store(sa, sb, sg, a.partials);
 }
 
@@ -320,17 +338,26 @@ __device__ __forceinline__ void sten2_dots_body(const StenArgs& a, const StenPar
 }
 
 template <bool ROWS, int LL>
+__device__ __forceinline__ void sten2_dots_block(const StenArgs& a, const StenParam& p, int blk, double& sa, double& sb,
+                                                 double& sg) {
+    const int ia = blk * 512 + static_cast<int>(threadIdx.x);
+    const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
+    if (!ROWS) sten_prefetch<-1, 512>(a, a.r, blk);
+    if (edge)
+        sten2_dots_body<ROWS, LL, true>(a, p, ia, ia + 256, sa, sb, sg);
+    else
+        sten2_dots_body<ROWS, LL, false>(a, p, ia, ia + 256, sa, sb, sg);
+}
+
+template <bool ROWS, int LL, bool GS = false>
 __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_constant__ StenParam p) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x)) {
-        const int ia = blk * 512 + static_cast<int>(threadIdx.x);
-        const bool edge = ROWS || blk < a.safe_lo || blk >= a.safe_hi;
-        if (!ROWS) sten_prefetch<-1, 512>(a, a.r, blk);
-        if (edge)
-            sten2_dots_body<ROWS, LL, true>(a, p, ia, ia + 256, sa, sb, sg);
-        else
-            sten2_dots_body<ROWS, LL, false>(a, p, ia, ia + 256, sa, sb, sg);
+    if constexpr (GS) {
+        for (int blk = static_cast<int>(blockIdx.x); blk < a.nblk; blk += static_cast<int>(gridDim.x))
+            sten2_dots_block<ROWS, LL>(a, p, blk, sa, sb, sg);
+    } else {
+        sten2_dots_block<ROWS, LL>(a, p, static_cast<int>(blockIdx.x), sa, sb, sg);
     }
     dots_block_store(sa, sb, sg, a.partials);
 }
@@ -513,4 +540,5 @@ __global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __gri
     dots_block_store(sa, sb, sg, a.partials);
     halo_done_p2p(h);
 }
+
 
