@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <set>
 #include <string>
 
 #include "mmio.cuh"
@@ -12,8 +13,10 @@
 #include "spgemm.cuh"
 #include "solver.cuh"
 
+struct pairamg_solver;
 struct pairamg_runtime {
     std::unique_ptr<pb::Runtime> rt;
+    std::set<pairamg_solver*> solvers;  // live solvers: released before the runtime goes
 };
 
 struct pairamg_solver {
@@ -43,7 +46,8 @@ pairamg_status guarded(F&& f) {
 }
 
 pb::Solver& S(pairamg_solver* s) {
-    if (!s || !s->s) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null solver");
+    if (!s) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null solver");
+    if (!s->s) pb::fail(PAIRAMG_CONTRACT_VIOLATION, "solver used after its runtime was destroyed");
     PB_CUDA(cudaSetDevice(s->rt->rt->device()));
     return *s->s;
 }
@@ -217,8 +221,19 @@ pairamg_status pairamg_runtime_create(int device, int rank, int nranks, const ui
     });
 }
 
+// Either destruction order is safe: destroying a runtime first releases the
+// device state of every solver created on it (the handles stay valid, later
+// calls fail with CONTRACT_VIOLATION, pairamg_solver_destroy frees them).
 pairamg_status pairamg_runtime_destroy(pairamg_runtime* rt) {
-    return guarded([&] { delete rt; });
+    return guarded([&] {
+        if (!rt) return;
+        if (rt->rt) cudaSetDevice(rt->rt->device());
+        for (pairamg_solver* s : rt->solvers) {
+            s->s.reset();
+            s->rt = nullptr;
+        }
+        delete rt;
+    });
 }
 
 pairamg_status pairamg_solver_create(pairamg_runtime* rt, pairamg_solver** out) {
@@ -228,13 +243,17 @@ pairamg_status pairamg_solver_create(pairamg_runtime* rt, pairamg_solver** out) 
         auto s = std::make_unique<pairamg_solver>();
         s->rt = rt;
         s->s = std::make_unique<pb::Solver>(*rt->rt);
+        rt->solvers.insert(s.get());
         *out = s.release();
     });
 }
 
 pairamg_status pairamg_solver_destroy(pairamg_solver* s) {
     return guarded([&] {
-        if (s && s->rt) cudaSetDevice(s->rt->rt->device());
+        if (s && s->rt) {
+            cudaSetDevice(s->rt->rt->device());
+            s->rt->solvers.erase(s);
+        }
         delete s;
     });
 }

@@ -402,10 +402,11 @@ void Solver::ensure_vectors() {
     // block per 8 slices) and of the grid-stride reductions
     // (overlapped schedule: interior + boundary partials; exchange-then-compute: sell_all)
     int64_t dots_blocks = sell_dots_grid(L0.sell_all);
-    if (L0.A.halo.n_halo > 0)
+    if (L0.A.halo.n_halo > 0) {
         dots_blocks = std::max<int64_t>(dots_blocks, int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd));
         if (sell_split_ok(L0.sell_int, L0.sell_bnd))
             dots_blocks = std::max<int64_t>(dots_blocks, sell_split_dots_grid(L0.sell_int, L0.sell_bnd));
+    }
     max_blocks_ = static_cast<int>(std::max<int64_t>(dots_blocks, kSmCount * 8));
     partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
     stage_.alloc(static_cast<size_t>(3 * kStage), s_);

@@ -157,3 +157,24 @@ def test_errors(runtime):
     with pytest.raises(pb.PairamgError) as e:
         s.setup(2, [0, 2], rp, np.array([0], np.int64), np.ones(1), cfg=pb.SetupConfig(3, 40, 40))
     assert e.value.code == "singular_smoother"
+    # the failed setup leaves a usable solver: a valid setup + solve afterwards
+    rp, ci, va = pb.poisson(7, 6, 6, 6)
+    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(3, 40, 40))
+    assert s.solve(np.ones(len(rp) - 1)).converged
+    s.close()
+
+
+@pytest.mark.gpu
+def test_runtime_destroyed_before_solver():
+    """Either destruction order is safe (GC finalises reference cycles in any order)."""
+    import paper_2303_02352_b200 as pb
+
+    rt = pb.Runtime(0, 0, 1)
+    s = pb.Solver(rt)
+    rp, ci, va = pb.poisson(7, 6, 6, 6)
+    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(3, 40, 40))
+    rt.close()
+    with pytest.raises(pb.PairamgError) as e:
+        s.solve(np.ones(len(rp) - 1))
+    assert e.value.code == "contract_violation"
+    s.close()
