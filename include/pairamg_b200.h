@@ -200,7 +200,10 @@ pairamg_status pairamg_match_graph(pairamg_runtime* rt, int64_t n, const int64_t
 /* Per-kernel-class device time accumulated over the last solve (CUDA events
  * around every launch of the class when timing was enabled):
  * class 0 = level-0 smoother sweeps, 1 = level-0 residual, 2 = level-0 outer
- * SpMV+dots, 3 = FCG vector updates. *launches and *ms may be NULL. */
+ * SpMV+dots, 3 = FCG vector updates, 4 = fused level-0 zero-start sweeps,
+ * 5 = fused level-0 prolongation sweeps, 6 + k (k < 16) = level k's own
+ * V-cycle work (two intervals per cycle: entry to restriction, return from
+ * level k+1 to exit).  *launches and *ms may be NULL. */
 pairamg_status pairamg_set_kernel_timing(pairamg_solver* s, int enabled);
 pairamg_status pairamg_kernel_timing(pairamg_solver* s, int kclass, int64_t* launches, double* ms,
                                      double* bytes_per_launch);

@@ -370,7 +370,7 @@ class Solver:
         _check(lib().pairamg_level_info(self.h, k, *[C.byref(x) for x in v]))
         return dict(zip(["global_rows", "global_nnz", "row_begin", "local_rows", "local_nnz"], [x.value for x in v]))
 
-    STORAGE = ("plain", "dict", "pat", "sten")
+    STORAGE = ("plain", "dict", "pat", "sten", "coded")
 
     def level_storage(self, k) -> str:
         """Solve-time storage format of level k (which row kernels run)."""

@@ -77,7 +77,7 @@ struct Sell {
     //        byte per row names the subset (absent-record mask + l1 diagonal);
     //        the main records and the per-pattern data travel as a kernel
     //        parameter.  Preferred whenever it applies (sell_sten.cuh).
-    enum Format { kPlain = 0, kDict = 1, kPat = 2, kSten = 3 };
+    enum Format { kPlain = 0, kDict = 1, kPat = 2, kSten = 3, kCoded = 4 };
     int format = kPlain;
     int64_t nrows = 0, nslices = 0, padded_nnz = 0;
     DBuf<int64_t> slice_off;  // nslices+1; elements (PLAIN) or 32-bit code words (DICT), multiples of 32
@@ -169,7 +169,17 @@ struct HaloSrc {
     int from[8] = {};
     const double* staging = nullptr;            // parity stride nhalo
     int64_t nhalo = 0;
-    unsigned long long* ctr = nullptr;          // [0] exchanges done, [3] boundary blocks done
+    unsigned long long* ctr = nullptr;          // [0] exchanges done, [3] boundary blocks done,
+                                                // [4] pushes done, [5] push blocks done
+    // fused push (npeers > 0): this rank's boundary values go to the
+    // neighbours from the first blocks of the same launch
+    bool fused = false;
+    int npeers = 0;
+    int64_t off[9] = {};                        // send_off
+    double* dst[8] = {};                        // peer staging + my offset (parity 0)
+    int64_t stride[8] = {};                     // peer parity stride
+    unsigned long long* pflag[8] = {};          // peer flag slot of this rank
+    const int32_t* send_idx = nullptr;
 };
 // Interior (contiguous STEN) + boundary (STEN) rows in one launch; the
 // boundary blocks wait for the neighbours' pushes of this exchange.

@@ -36,7 +36,7 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 // parity (exchange count & 1); the last CTA raises the neighbours' flags.
 __global__ void __launch_bounds__(256) k_p2p_push(const double* x, const int32_t* send_idx, int64_t nsend,
                                                    const __grid_constant__ PushArgs pa, unsigned long long* ctr) {
-    const unsigned long long e = ctr[0];
+    const unsigned long long e = ctr[4];  // pushes done (== exchanges received on every rank)
     const int64_t par = static_cast<int64_t>(e & 1ull);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsend;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -46,8 +46,9 @@ __global__ void __launch_bounds__(256) k_p2p_push(const double* x, const int32_t
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1ull) == gridDim.x - 1) {
-        ctr[1] = 0;
+    if (threadIdx.x == 0 && atomicAdd(&ctr[5], 1ull) == gridDim.x - 1) {
+        ctr[5] = 0;
+        ctr[4] = e + 1;
         __threadfence_system();
         for (int p = 0; p < pa.npeers; ++p) st_release_sys(pa.flag[p], e + 1);
     }
@@ -164,7 +165,7 @@ void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s) {
         P.peer_flag.clear();
         return;
     }
-    P.ctr.alloc(4, s);
+    P.ctr.alloc(8, s);
     P.ctr.zero(s);
     PB_CUDA(cudaStreamSynchronize(s));
     P.ok = true;
@@ -217,6 +218,17 @@ HaloSrc p2p_halo_src(const HaloPlan& H, P2PHalo& P) {
     hs.staging = P.staging;
     hs.nhalo = H.n_halo;
     hs.ctr = P.ctr.get();
+    if (env_flag("PAIRAMG_FUSED_PUSH", true) && H.send_peers.size() <= 8) {
+        hs.fused = true;
+        hs.npeers = static_cast<int>(H.send_peers.size());
+        for (int i = 0; i <= hs.npeers; ++i) hs.off[i] = H.send_off[static_cast<size_t>(i)];
+        for (int i = 0; i < hs.npeers; ++i) {
+            hs.dst[i] = P.peer_staging[static_cast<size_t>(i)];
+            hs.stride[i] = P.peer_stride[static_cast<size_t>(i)];
+            hs.pflag[i] = P.peer_flag[static_cast<size_t>(i)];
+        }
+        hs.send_idx = H.send_idx.get();
+    }
     return hs;
 }
 

@@ -28,7 +28,7 @@ struct P2PHalo {
     std::vector<int64_t> peer_stride;          // per send peer: its n_halo (parity stride)
     std::vector<unsigned long long*> peer_flag;  // per send peer: its flags[my rank]
     std::vector<void*> opened;                 // IPC mappings to close
-    DBuf<unsigned long long> ctr;              // [0] exchanges done, [1] push / [2] pull / [3] split blocks done
+    DBuf<unsigned long long> ctr;              // [0] exchanges received, [2] pull / [3] split blocks done, [4] pushes, [5] push blocks done
     DBuf<double*> d_peer_staging;              // device copies of the per-peer tables
     DBuf<int64_t> d_peer_stride;
     DBuf<unsigned long long*> d_peer_flag;

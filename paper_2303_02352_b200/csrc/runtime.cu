@@ -28,7 +28,27 @@ Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
         static_assert(sizeof(uid.internal) == 128, "NCCL unique id size");
         std::memcpy(uid.internal, id, 128);
         PB_NCCL(ncclCommInitRank(&comm_, nranks, uid, rank));
+        if (env_flag("PAIRAMG_NCCL_WARMUP", true)) warmup();
     }
+}
+
+// NCCL connects peers lazily, on the first collective / send-recv between
+// them (buffers, IPC handles, proxy threads).  One tiny all-pairs exchange
+// plus the collective kinds the library uses moves that one-time cost from
+// the first setup into runtime creation.
+void Runtime::warmup() {
+    DBuf<double> buf(static_cast<size_t>(4 * nranks_), stream_);
+    buf.zero(stream_);
+    PB_NCCL(ncclGroupStart());
+    for (int d = 0; d < nranks_; ++d) {
+        if (d == rank_) continue;
+        PB_NCCL(ncclSend(buf.get() + d, 1, ncclDouble, d, comm_, stream_));
+        PB_NCCL(ncclRecv(buf.get() + nranks_ + d, 1, ncclDouble, d, comm_, stream_));
+    }
+    PB_NCCL(ncclGroupEnd());
+    PB_NCCL(ncclAllGather(buf.get(), buf.get() + 2 * nranks_, 1, ncclDouble, comm_, stream_));
+    PB_NCCL(ncclAllReduce(buf.get(), buf.get() + 3 * nranks_, 1, ncclDouble, ncclSum, comm_, stream_));
+    PB_CUDA(cudaStreamSynchronize(stream_));
 }
 
 Runtime::~Runtime() {

@@ -63,6 +63,7 @@ public:
     void allgather_f64(const double* send, double* recv, size_t count, cudaStream_t s);
 
 private:
+    void warmup();
     int device_ = 0, rank_ = 0, nranks_ = 1;
     ncclComm_t comm_ = nullptr;
     cudaStream_t stream_ = nullptr, comm_stream_ = nullptr;

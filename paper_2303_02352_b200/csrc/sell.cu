@@ -110,17 +110,20 @@ __device__ __forceinline__ double row_sum_plain(const SellArgs& a, int64_t slice
 // indexed constant-bank loads (LDC), served by the constant cache --
 // broadcast when a warp's lanes share a code (interior slices) -- instead
 // of competing with the gathers for L1TEX bandwidth.
-template <bool DICT>
+// F: kFPlain / kFDict / kFCoded (the row-sum flavour of k_sell).  CODED
+// uses only the value half of each record.
+constexpr int kFPlain = 0, kFDict = 1, kFCoded = 2;
+template <int F>
 struct DictParam {
     ulonglong2 e[256];
     double dg[256];  // distinct l1 diagonal values (when SellArgs::dcode is set)
 };
 template <>
-struct DictParam<false> {
+struct DictParam<kFPlain> {
     int unused;
 };
 
-__device__ __forceinline__ void dict_entry(const DictParam<true>& dp, uint32_t e, double& v, int& dc) {
+__device__ __forceinline__ void dict_entry(const DictParam<kFDict>& dp, uint32_t e, double& v, int& dc) {
     const ulonglong2 r = dp.e[e];
     v = __longlong_as_double(static_cast<long long>(r.x));
     dc = static_cast<int>(r.y);
@@ -136,7 +139,7 @@ __device__ __forceinline__ void dict_entry(const DictParam<true>& dp, uint32_t e
 // reproduced exactly with 5 fewer instructions per entry (predicate, two
 // selects, zeroing) on this issue-bound loop.
 template <int OP>
-__device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictParam<true>& dp, int slice, int lane,
+__device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictParam<kFDict>& dp, int slice, int lane,
                                                int row) {
     const int W = a.words;
     const uint32_t* cp = a.code + (slice * W) * 32 + lane;
@@ -160,16 +163,45 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, const DictPara
     return sum;
 }
 
-template <int OP, bool DICT>
-__device__ __forceinline__ double row_sum(const SellArgs& a, const DictParam<DICT>& dp, int slice, int lane, int row) {
-    if constexpr (DICT)
+// CODED row sum: one 32-bit word per entry, (column - row) in the high 24
+// bits (signed) and a value code in the low 8 (SELL-32 slices of the row
+// set's own widths, as PLAIN).  Pad word 0x000000FF = {+0.0, own row}: not
+// predicated, bit-neutral for the same reason as the DICT pads.
+template <int OP>
+__device__ __forceinline__ double row_sum_coded(const SellArgs& a, const DictParam<kFCoded>& dp, int slice, int lane,
+                                                int row) {
+    const int beg = static_cast<int>(a.soff[slice]);
+    const int width = (static_cast<int>(a.soff[slice + 1]) - beg) >> 5;
+    const uint32_t* cp = a.code + beg + lane;
+    double sum = 0.0;
+    for (int k = 0; k < width; k += 8) {
+        uint32_t w[8];
+        double av[8], xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = k + j < width ? __ldg(cp + (k + j) * 32) : 0xFFu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            av[j] = __longlong_as_double(static_cast<long long>(dp.e[w[j] & 0xFFu].x));
+            xv[j] = xval<OP>(a, row + (static_cast<int32_t>(w[j]) >> 8));
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum = dadd(sum, dmul(av[j], xv[j]));
+    }
+    return sum;
+}
+
+template <int OP, int F>
+__device__ __forceinline__ double row_sum(const SellArgs& a, const DictParam<F>& dp, int slice, int lane, int row) {
+    if constexpr (F == kFDict)
         return row_sum_dict<OP>(a, dp, slice, lane, row);
+    else if constexpr (F == kFCoded)
+        return row_sum_coded<OP>(a, dp, slice, lane, row);
     else
         return row_sum_plain<OP>(a, slice, lane);
 }
 
-template <int OP, bool ROWS, bool DICT>
-__global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_constant__ DictParam<DICT> dp) {
+template <int OP, bool ROWS, int F>
+__global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_constant__ DictParam<F> dp) {
     const int lane = threadIdx.x & 31;
     const int slice = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (slice >= a.nslices) return;
@@ -181,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
     if (valid) {
         if (OP == kJacobi || OP == kJacobiZero || OP == kJacobiProl) {
             ri = a.r[row];
-            if constexpr (DICT)
+            if constexpr (F != kFPlain)
                 di = a.dcode ? dp.dg[a.dcode[sr]] : a.d[row];
             else
                 di = a.d[row];
@@ -189,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
         if (OP == kResid) ri = a.r[row];
         if (OP == kJacobi) xi = a.x[row];
     }
-    const double sum = row_sum<OP, DICT>(a, dp, slice, lane, row);
+    const double sum = row_sum<OP, F>(a, dp, slice, lane, row);
     if (!valid) return;
     if (OP == kSpmv) {
         a.y[row] = sum;
@@ -204,8 +236,8 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
 // v = A w with block partials of (w.r, w.v, w.q) (fixed order ->
 // deterministic).  Launched with one warp per slice like the sweeps; the
 // grid-stride loop only matters for capped grids.
-template <bool DICT, bool ROWS>
-__global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, const __grid_constant__ DictParam<DICT> dp) {
+template <int F, bool ROWS>
+__global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, const __grid_constant__ DictParam<F> dp) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double sa = 0.0, sb = 0.0, sg = 0.0;
@@ -219,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, cons
             rr = a.r[row];
             qq = a.q[row];
         }
-        const double sum = row_sum<kSpmv, DICT>(a, dp, slice, lane, row);
+        const double sum = row_sum<kSpmv, F>(a, dp, slice, lane, row);
         if (valid) {
             a.y[row] = sum;
             sa = dadd(sa, dmul(wi, rr));
@@ -481,6 +513,30 @@ __global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __res
     }
 }
 
+__global__ void k_fill_u32(uint32_t* __restrict__ p, int64_t n, uint32_t v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// CODED words: ((column - row) << 8) | value code; bad = a delta outside 24 bits.
+__global__ void k_sell_fill_coded(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                  const uint8_t* __restrict__ vcode, const int32_t* __restrict__ rows, int64_t nrows,
+                                  const int64_t* __restrict__ soff, uint32_t* __restrict__ code, int* bad) {
+    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sr >= nrows) return;
+    const int64_t row = rows ? rows[sr] : sr;
+    const int64_t base = soff[sr >> 5] + (sr & 31);
+    const int64_t b = rp[row], e = rp[row + 1];
+    for (int64_t t = b; t < e; ++t) {
+        const int64_t d = static_cast<int64_t>(col[t]) - row;
+        if (d < -(int64_t(1) << 23) || d >= (int64_t(1) << 23) || vcode[t] == 0xFF) {
+            atomicExch(bad, 1);
+            return;
+        }
+        code[base + (t - b) * 32] = (static_cast<uint32_t>(static_cast<int32_t>(d)) << 8) | vcode[t];
+    }
+}
+
 __device__ __forceinline__ void ld_slot(const ull* p, ull& lo, ull& hi) {
     asm volatile(
         "{\n\t.reg .b128 v;\n\t"
@@ -735,8 +791,8 @@ WinArgs win_args_of(const Sell& S) {
     return a;
 }
 
-DictParam<true> win_param(const Sell& S) {
-    DictParam<true> dp;
+DictParam<kFDict> win_param(const Sell& S) {
+    DictParam<kFDict> dp;
     for (int i = 0; i < 256; ++i) {
         dp.e[i] = S.win.rec[i];
         dp.dg[i] = 1.0;
@@ -1202,29 +1258,37 @@ SellArgs args_of(const Sell& S) {
     return a;
 }
 
-DictParam<true> dict_param(const Sell& S) {
-    DictParam<true> dp;
+template <int F = kFDict>
+DictParam<F> dict_param(const Sell& S) {
+    DictParam<F> dp;
     for (int i = 0; i < 256; ++i) dp.e[i] = i < static_cast<int>(S.hdict.size()) ? S.hdict[i] : make_ulonglong2(0ULL, 0ULL);
     for (int i = 0; i < 256; ++i) dp.dg[i] = i < static_cast<int>(S.hdiag.size()) ? S.hdiag[i] : 1.0;
     return dp;
 }
+DictParam<kFCoded> coded_param(const Sell& S) { return dict_param<kFCoded>(S); }
 
 template <int OP>
 void launch_op(const Sell& S, const SellArgs& a, cudaStream_t s) {
     const int grid = blocks_for(S.nslices, kWarps);
     const bool rows = a.rows != nullptr;
     if (S.format == Sell::kDict) {
-        const DictParam<true> dp = dict_param(S);
+        const DictParam<kFDict> dp = dict_param(S);
         if (rows)
-            k_sell<OP, true, true><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell<OP, true, kFDict><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell<OP, false, true><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell<OP, false, kFDict><<<grid, kThreads, 0, s>>>(a, dp);
+    } else if (S.format == Sell::kCoded) {
+        const DictParam<kFCoded> dp = coded_param(S);
+        if (rows)
+            k_sell<OP, true, kFCoded><<<grid, kThreads, 0, s>>>(a, dp);
+        else
+            k_sell<OP, false, kFCoded><<<grid, kThreads, 0, s>>>(a, dp);
     } else {
-        const DictParam<false> dp{0};
+        const DictParam<kFPlain> dp{0};
         if (rows)
-            k_sell<OP, true, false><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell<OP, true, kFPlain><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell<OP, false, false><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell<OP, false, kFPlain><<<grid, kThreads, 0, s>>>(a, dp);
     }
     PB_CHECK_LAUNCH();
 }
@@ -1276,6 +1340,64 @@ bool build_value_codes(const double* v, int64_t n, DBuf<uint8_t>& code, std::vec
     return true;
 }
 
+namespace {
+
+// SELL-32 slice offsets (elements, multiples of 32) from the rows' lengths.
+void slice_widths(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) {
+    S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
+    PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
+    if (S.nslices) {
+        k_sell_width<<<blocks_for(S.nslices * 32, 256), 256, 0, s>>>(M.rp.get(), rows, S.nrows, S.nslices,
+                                                                     S.slice_off.get());
+        PB_CHECK_LAUNCH();
+        cub_call([&](void* t, size_t& bytes) {
+            return cub::DeviceScan::ExclusiveSum(t, bytes, S.slice_off.get(), S.slice_off.get(), S.nslices + 1, s);
+        }, s);
+    }
+    PB_CUDA(cudaMemcpyAsync(&S.padded_nnz, S.slice_off.get() + S.nslices, 8, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+}
+
+// CODED: <= 255 distinct values over the matrix and every |column - row| <
+// 2^23 (the irregular coarse levels of odd grids and general matrices: tens
+// of values, thousands of distinct offsets -> neither DICT nor PAT fits).
+bool try_coded(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) {
+    if (S.nrows == 0 || M.nnz == 0) return false;
+    DBuf<uint8_t> vcode;
+    std::vector<double> table;
+    if (!build_value_codes(M.val.get(), M.nnz, vcode, table, s) || table.size() > 255) return false;
+    slice_widths(M, rows, S, s);
+    if (S.padded_nnz >= (int64_t(1) << 31)) return false;
+    S.code.alloc(static_cast<size_t>(S.padded_nnz), s);
+    if (S.padded_nnz)
+        k_fill_u32<<<blocks_for(S.padded_nnz, 256), 256, 0, s>>>(S.code.get(), S.padded_nnz, 0xFFu);
+    DBuf<int> bad(1, s);
+    bad.zero(s);
+    k_sell_fill_coded<<<blocks_for(S.nrows, 256), 256, 0, s>>>(M.rp.get(), M.col.get(), vcode.get(), rows, S.nrows,
+                                                                S.slice_off.get(), S.code.get(), bad.get());
+    PB_CHECK_LAUNCH();
+    int hb = 0;
+    PB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (hb) {
+        S.code.reset();
+        S.slice_off.reset();
+        S.padded_nnz = 0;
+        return false;
+    }
+    S.hdict.assign(256, make_ulonglong2(0ULL, 0ULL));  // code 255 = pad {+0.0}
+    for (size_t c = 0; c < table.size(); ++c) {
+        ull vb;
+        std::memcpy(&vb, &table[c], 8);
+        S.hdict[c] = make_ulonglong2(vb, 0ULL);
+    }
+    S.ndict = static_cast<int>(table.size());
+    S.format = Sell::kCoded;
+    return true;
+}
+
+}  // namespace
+
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict,
                 const double* l1) {
     S = Sell();
@@ -1320,22 +1442,12 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
             reset_pat(S);
         }
         if (want_pat && try_pattern(M, rows, S, l1, s)) return;
-        if (try_dict(M, rows, S, l1, s)) return;
+        if (env_flag("PAIRAMG_SELL_PAIRS", true) && try_dict(M, rows, S, l1, s)) return;
         if (pref != 0 && !want_pat && try_pattern(M, rows, S, l1, s)) return;
+        if (env_flag("PAIRAMG_SELL_CODED", true) && try_coded(M, rows, S, s)) return;
     }
     S.format = Sell::kPlain;
-    S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
-    PB_CUDA(cudaMemsetAsync(S.slice_off.get(), 0, 8 * (S.nslices + 1), s));
-    if (S.nslices) {
-        k_sell_width<<<blocks_for(S.nslices * 32, 256), 256, 0, s>>>(M.rp.get(), rows, S.nrows, S.nslices,
-                                                                     S.slice_off.get());
-        PB_CHECK_LAUNCH();
-        cub_call([&](void* t, size_t& bytes) {
-            return cub::DeviceScan::ExclusiveSum(t, bytes, S.slice_off.get(), S.slice_off.get(), S.nslices + 1, s);
-        }, s);
-    }
-    PB_CUDA(cudaMemcpyAsync(&S.padded_nnz, S.slice_off.get() + S.nslices, 8, cudaMemcpyDeviceToHost, s));
-    PB_CUDA(cudaStreamSynchronize(s));
+    slice_widths(M, rows, S, s);
     S.col.alloc(static_cast<size_t>(S.padded_nnz), s);
     S.val.alloc(static_cast<size_t>(S.padded_nnz), s);
     if (S.padded_nnz) {
@@ -1353,6 +1465,7 @@ double sell_bytes(const Sell& S) {
     if (S.format == Sell::kSten) return 1.0 * S.nrows + 12.0 * S.sten_L + 12.0 * S.npat;
     if (S.format == Sell::kPat) return 1.0 * S.nrows + 16.0 * S.ptab.size() + 16.0 * S.npat;
     if (S.format == Sell::kDict) return 4.0 * S.padded_nnz + 16.0 * S.ndict;
+    if (S.format == Sell::kCoded) return 4.0 * S.padded_nnz + 8.0 * (S.nslices + 1) + 8.0 * S.ndict;
     return 12.0 * S.padded_nnz + 8.0 * (S.nslices + 1);
 }
 
@@ -1420,7 +1533,7 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
         w.r = o.r;
         w.d = o.d;
         w.omega = o.omega;
-        const DictParam<true> dp = win_param(S);
+        const DictParam<kFDict> dp = win_param(S);
         switch (o.op) {
             case kSpmv: k_win<kSpmv><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
             case kJacobi: k_win<kJacobi><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
@@ -1514,7 +1627,20 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
         P.h.nhalo = hs->nhalo;
         P.h.ctr = hs->ctr;
         P.h.b.nown = static_cast<int>(I.xlen - hs->nhalo);
+        if (hs->fused) {  // push blocks ahead of the boundary blocks
+            const int64_t nsend = hs->off[hs->npeers];
+            P.h.npush = static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(1, (nsend + 2047) / 2048)));
+            P.h.npeers = hs->npeers;
+            for (int i = 0; i <= hs->npeers; ++i) P.h.off[i] = hs->off[i];
+            for (int i = 0; i < hs->npeers; ++i) {
+                P.h.dst[i] = hs->dst[i];
+                P.h.stride[i] = hs->stride[i];
+                P.h.pflag[i] = hs->pflag[i];
+            }
+            P.h.send_idx = hs->send_idx;
+        }
     }
+    P.grid = P.h.npush + P.h.nblk_a + P.h.nblk_b;
     return P;
 }
 }  // namespace
@@ -1550,7 +1676,8 @@ void sell_apply_split(const Sell& I, const Sell& B, const SellOpArgs& o, const H
 #undef PB_SPLIT2
 }
 
-int sell_split_dots_grid(const Sell& I, const Sell& B) { return split_plan(I, B, true, nullptr).grid; }
+// upper bound: the fused push adds <= 32 blocks
+int sell_split_dots_grid(const Sell& I, const Sell& B) { return split_plan(I, B, true, nullptr).grid + 32; }
 
 int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* v, const double* r, const double* q,
                          double* partials, int max_blocks, const HaloSrc& hs, cudaStream_t s) {
@@ -1641,17 +1768,23 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
     a.q = q;
     a.partials = partials;
     if (S.format == Sell::kDict) {
-        const DictParam<true> dp = dict_param(S);
+        const DictParam<kFDict> dp = dict_param(S);
         if (rows)
-            k_sell_spmv_dots<true, true><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell_spmv_dots<kFDict, true><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell_spmv_dots<true, false><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell_spmv_dots<kFDict, false><<<grid, kThreads, 0, s>>>(a, dp);
+    } else if (S.format == Sell::kCoded) {
+        const DictParam<kFCoded> dp = coded_param(S);
+        if (rows)
+            k_sell_spmv_dots<kFCoded, true><<<grid, kThreads, 0, s>>>(a, dp);
+        else
+            k_sell_spmv_dots<kFCoded, false><<<grid, kThreads, 0, s>>>(a, dp);
     } else {
-        const DictParam<false> dp{0};
+        const DictParam<kFPlain> dp{0};
         if (rows)
-            k_sell_spmv_dots<false, true><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell_spmv_dots<kFPlain, true><<<grid, kThreads, 0, s>>>(a, dp);
         else
-            k_sell_spmv_dots<false, false><<<grid, kThreads, 0, s>>>(a, dp);
+            k_sell_spmv_dots<kFPlain, false><<<grid, kThreads, 0, s>>>(a, dp);
     }
     PB_CHECK_LAUNCH();
     return grid;

@@ -457,8 +457,42 @@ struct HaloSplit {
     int from[8];
     const double* staging;     // this rank's staging, parity stride nhalo
     int64_t nhalo;
-    unsigned long long* ctr;   // [0] exchanges done, [3] boundary blocks done
+    unsigned long long* ctr;   // [0] exchanges done, [3] boundary blocks done, [4]/[5] pushes / push blocks
+    // fused push: blocks [0, npush) store this rank's boundary values into
+    // the neighbours' staging, then [npush, npush + nblk_b) are the boundary
+    // rows and the rest the interior
+    int npush, npeers;
+    int64_t off[9];
+    double* dst[8];
+    int64_t stride[8];
+    unsigned long long* pflag[8];
+    const int32_t* send_idx;
 };
+
+// One push block: a grid-stride share of x[send_idx] into the peers' staging
+// slots of parity (pushes done & 1); the last push block advances the push
+// count and raises the peers' flags (system-scope release after a system
+// fence, as k_p2p_push).  Runs after the launch's griddepcontrol.wait, so x
+// is the previous kernel's complete output.
+__device__ __forceinline__ void halo_push_block(const HaloSplit& h, const double* x, int blk) {
+    const unsigned long long e = h.ctr[4];
+    const int64_t par = static_cast<int64_t>(e & 1ull);
+    const int64_t nsend = h.off[h.npeers];
+    for (int64_t i = blk * int64_t(256) + threadIdx.x; i < nsend; i += int64_t(h.npush) * 256) {
+        int p = 0;
+        while (p + 1 < h.npeers && i >= h.off[p + 1]) ++p;
+        h.dst[p][par * h.stride[p] + (i - h.off[p])] = x[h.send_idx[i]];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&h.ctr[5], 1ull) == static_cast<unsigned long long>(h.npush) - 1) {
+        h.ctr[5] = 0;
+        h.ctr[4] = e + 1;
+        __threadfence_system();
+        for (int p = 0; p < h.npeers; ++p)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(h.pflag[p]), "l"(e + 1) : "memory");
+    }
+}
 
 __device__ __forceinline__ const double* halo_wait_p2p(const HaloSplit& h) {
     const unsigned long long e = h.ctr[0];
@@ -491,9 +525,14 @@ __device__ __forceinline__ void halo_done_p2p(const HaloSplit& h) {
 template <int OP, int LLA, bool R2, bool BROWS>
 __global__ void __launch_bounds__(256) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();  // no early dependents: the boundary blocks wait on another GPU
-    // boundary blocks first: dispatched at once, their short wait for the
-    // neighbours' pushes and their slower generic rows overlap the interior
-    const int blk = static_cast<int>(blockIdx.x) - h.nblk_b;
+    // push blocks, then boundary blocks: dispatched at once, the push and the
+    // short wait for the neighbours' pushes overlap the interior rows
+    if (static_cast<int>(blockIdx.x) < h.npush) {
+        halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
+        return;
+    }
+    const int bb = static_cast<int>(blockIdx.x) - h.npush;
+    const int blk = bb - h.nblk_b;
     if (blk >= 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
@@ -510,15 +549,21 @@ __global__ void __launch_bounds__(256) k_sten_split(StenArgs a, const __grid_con
     }
     StenArgs b = h.b;
     b.hsrc = halo_wait_p2p(h);
-    sten1_block<OP, BROWS, 0, true>(b, h.pb, static_cast<int>(blockIdx.x));
+    sten1_block<OP, BROWS, 0, true>(b, h.pb, bb);
     halo_done_p2p(h);
 }
 
 template <int LLA, bool R2, bool BROWS>
 __global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();
-    const int blk = static_cast<int>(blockIdx.x) - h.nblk_b;  // boundary blocks first
     double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (static_cast<int>(blockIdx.x) < h.npush) {  // push blocks first (zero partials)
+        halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
+        dots_block_store(sa, sb, sg, a.partials);
+        return;
+    }
+    const int bb = static_cast<int>(blockIdx.x) - h.npush;
+    const int blk = bb - h.nblk_b;  // then the boundary blocks
     if (blk >= 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
@@ -536,7 +581,7 @@ __global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __gri
     }
     StenArgs b = h.b;
     b.hsrc = halo_wait_p2p(h);
-    sten1_dots_block<BROWS, 0, true>(b, h.pb, static_cast<int>(blockIdx.x), sa, sb, sg);
+    sten1_dots_block<BROWS, 0, true>(b, h.pb, bb, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
     halo_done_p2p(h);
 }

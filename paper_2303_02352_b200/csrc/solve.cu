@@ -8,6 +8,7 @@
 // stopping test.
 #include <cmath>
 #include <cstring>
+#include <string>
 
 #include <cstdio>
 
@@ -386,6 +387,24 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
     }
     ensure_vectors();
     ready = true;
+    if (env_flag("PAIRAMG_VERBOSE", false)) {  // per-level solve storage (stderr)
+        static const char* fmt[] = {"plain", "dict", "pat", "sten", "coded", "?", "?", "?"};
+        auto desc = [&](const Sell& S) {
+            char b[96];
+            std::snprintf(b, sizeof b, "%s(rows %lld, L %d, pat %d)", fmt[S.format & 7],
+                          static_cast<long long>(S.nrows), S.sten_L, S.npat);
+            return std::string(b);
+        };
+        for (int k = 0; k < h.nl(); ++k) {
+            Level& L = lvl(k);
+            const bool rep = h.rep_level >= 0 && k >= h.rep_level;
+            std::fprintf(stderr, "rank %d level %d %s rows %lld halo %lld p2p %d: %s%s%s\n", rt.rank(), k,
+                         rep ? "replicated" : "distributed", static_cast<long long>(L.A.n),
+                         static_cast<long long>(L.A.halo.n_halo), L.p2p.ok ? 1 : 0,
+                         L.A.halo.n_halo > 0 ? ("int " + desc(L.sell_int) + " bnd " + desc(L.sell_bnd) + " all ").c_str() : "",
+                         desc(L.sell_all).c_str(), L.pcode.empty() ? "" : " pcode");
+        }
+    }
 }
 
 void Solver::ensure_vectors() {
@@ -524,9 +543,10 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         (o.op == kSpmv || o.op == kJacobi || o.op == kResid)) {
         // push this rank's boundary values into the neighbours, then one
         // launch whose boundary blocks wait for theirs (no comm stream)
-        p2p_push(L.A.halo, L.p2p, o.x, s_);
-        sell_apply_split(L.sell_int, L.sell_bnd, o, p2p_halo_src(L.A.halo, L.p2p), s_);
-        launches_ += 2;
+        const HaloSrc hs = p2p_halo_src(L.A.halo, L.p2p);
+        if (!hs.fused) p2p_push(L.A.halo, L.p2p, o.x, s_);
+        sell_apply_split(L.sell_int, L.sell_bnd, o, hs, s_);
+        launches_ += hs.fused ? 1 : 2;
         end_time(kc);
         return;
     }
@@ -585,7 +605,8 @@ static SellOpArgs jacobi_args(int op, const double* x, double* y, const double* 
 
 bool Solver::fusable(int k) {
     const Level& L = lvl(k);
-    return fuse && !L.A.halo.has_traffic() && (L.sell_all.format == Sell::kDict || L.sell_all.format == Sell::kPlain);
+    return fuse && !L.A.halo.has_traffic() && (L.sell_all.format == Sell::kDict || L.sell_all.format == Sell::kPlain ||
+                                                  L.sell_all.format == Sell::kCoded);
 }
 
 void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
@@ -622,6 +643,8 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     double* xc = L.x.get();
     double* xo = L.xt.get();
     const bool l0 = k == 0;
+    const int lc = k < kTimedLevels ? kLevelClass + k : -1;
+    begin_time(lc);
     if (k == h.nl() - 1) {
         if (!L.A.halo.has_traffic() && !(k == 0 && zs_pending_) &&
             sell_coarse_solve(L.sell_all, rhs, xc, cc.coarsest_sweeps, cc.relax_weight, s_)) {
@@ -629,6 +652,7 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         } else {
             smooth(k, true, cc.coarsest_sweeps, rhs, xc, xo, cc.relax_weight, l0);
         }
+        end_time(lc);
         out = xc;
         return;
     }
@@ -660,7 +684,9 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         launches_ += 2;
     }
     double* e = nullptr;
+    end_time(lc);
     vcycle_enqueue(k + 1, C.rhs.get(), e, cc);
+    begin_time(lc);
     if (gather) e += h.rep_offsets[static_cast<size_t>(rt.rank())];
     int post = cc.post_sweeps;
     if (post >= 1 && fusable(k)) {
@@ -693,6 +719,7 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         launches_ += 1;
     }
     smooth(k, false, post, rhs, xc, xo, cc.relax_weight, l0);
+    end_time(lc);
     out = xc;
 }
 
@@ -781,10 +808,11 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
     } else if (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.sell_bnd)) {
-        p2p_push(L0.A.halo, L0.p2p, w, s_);
+        const HaloSrc hs = p2p_halo_src(L0.A.halo, L0.p2p);
+        if (!hs.fused) p2p_push(L0.A.halo, L0.p2p, w, s_);
         dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get(),
-                                          max_blocks_, p2p_halo_src(L0.A.halo, L0.p2p), s_);
-        launches_ += 2;
+                                          max_blocks_, hs, s_);
+        launches_ += hs.fused ? 1 : 2;
     } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
         const int g1 = sell_dots_grid(L0.sell_int, halo_grid_);
         PB_CUDA(cudaEventRecord(ev_fork_, s_));

@@ -31,8 +31,12 @@ struct FcgState {
 
 // Timed kernel classes (level 0): 0 plain l1-Jacobi sweep, 1 residual,
 // 2 SpMV + dot triple, 3 FCG vector update, 4 fused zero-start sweep,
-// 5 fused prolongation sweep.
-constexpr int kNumClasses = 6;
+// 5 fused prolongation sweep; kLevelClass + k: level k's own V-cycle work
+// (everything between entering level k and leaving it, minus level k+1's
+// cycle; two intervals per V-cycle), for k < kTimedLevels.
+constexpr int kLevelClass = 6;
+constexpr int kTimedLevels = 16;
+constexpr int kNumClasses = kLevelClass + kTimedLevels;
 
 struct KernelClassTiming {
     int64_t launches = 0;

@@ -52,10 +52,11 @@ FORMATS = {
     "pat": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "1"},
     "dict": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0"},
     "plain": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_DICT": "0"},
+    "coded": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0", "PAIRAMG_SELL_PAIRS": "0"},
 }
 
 
-def check_pair(runtime, rp, ci, va, target, s_exp=3):
+def check_pair(runtime, rp, ci, va, target, s_exp=3, all_levels=False):
     import paper_2303_02352_b200 as pb
 
     orc = oracle.Oracle("restatement", csr=(rp, ci, va), nranks=1, coarse_size_target=target,
@@ -74,9 +75,9 @@ def check_pair(runtime, rp, ci, va, target, s_exp=3):
     np.testing.assert_array_equal(bits(s.vcycle(r)), bits(orc.vcycle(r)), err_msg="vcycle")
     st = s.solve(np.ones(orc.n))
     assert st.converged and abs(st.iterations - orc.solve()["iterations"]) <= 1
-    fmt = s.level_storage(0)
+    fmts = [s.level_storage(k) for k in range(orc.num_levels)]
     s.close()
-    return fmt
+    return fmts if all_levels else fmts[0]
 
 
 @pytest.mark.parametrize("fmt", sorted(FORMATS))
@@ -106,3 +107,39 @@ def test_scaled_poisson_keeps_sten(runtime):
 
     rp, ci, va = pb.poisson(7, 14, 14, 14)
     assert check_pair(runtime, rp, ci, va * 225.0, target=560) == "sten"
+
+
+def test_odd_grid_coarse_levels_coded(runtime):
+    """Odd grids: the pairwise aggregates stop lining up, the coarse operators
+    have thousands of distinct column offsets (no DICT / PAT / STEN) but a few
+    dozen distinct values -> CODED storage (value code + 24-bit column delta),
+    still bitwise."""
+    import paper_2303_02352_b200 as pb
+
+    rp, ci, va = pb.poisson(7, 33, 31, 29)
+    fmts = check_pair(runtime, rp, ci, va, target=40 * 33, all_levels=True)
+    assert fmts[0] == "sten"
+    assert "coded" in fmts[1:], fmts
+
+
+@pytest.mark.parametrize("fmt", ["auto", "coded"])
+def test_random_pattern_few_values(runtime, fmt, monkeypatch):
+    """Random sparsity with quantised values: CODED at level 0."""
+    for k, v in FORMATS[fmt].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(7)
+    n = 400
+    A = np.zeros((n, n))
+    mask = np.triu(rng.random((n, n)) < 0.02, 1)
+    q = -rng.integers(1, 5, (n, n)) * 0.25
+    A[mask] = q[mask]
+    A = A + A.T
+    np.fill_diagonal(A, -A.sum(axis=1) + 1.0)
+    rp, ci, va = [0], [], []
+    for i in range(n):
+        nz = np.nonzero(A[i])[0]
+        ci.extend(nz.tolist())
+        va.extend(A[i, nz].tolist())
+        rp.append(len(ci))
+    fmts = check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=20, s_exp=2, all_levels=True)
+    assert fmts[0] == "coded", fmts

@@ -88,6 +88,7 @@ FORMATS = {  # solve-time storage of every level (csrc/sell.cu): all must be bit
     "pat": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "1"},
     "dict": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0"},
     "plain": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_DICT": "0"},
+    "coded": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0", "PAIRAMG_SELL_PAIRS": "0"},
 }
 
 
