@@ -356,5 +356,124 @@ void p2p_allgather(P2PGather& G, const double* send, double* recv, int K, cudaSt
                                G.kmax, G.ctr.get()));
 }
 
-}  // namespace pb
+// ---- segment allgather (replicated coarse right-hand side) ----------------
 
+namespace {
+struct SegArgs {
+    double* buf[kSegMaxRanks];                 // every rank's vector (own: local)
+    unsigned long long* flag[kSegMaxRanks];    // every rank's flag array
+    const unsigned long long* myflags;
+    int nranks, rank;
+};
+
+__global__ void __launch_bounds__(256) k_seg_gather(const double* src, int64_t cnt, int64_t off,
+                                                    const __grid_constant__ SegArgs a, unsigned long long* ctr) {
+    pdl_wait_only();
+    const unsigned long long e = ctr[0];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = src[i];
+        for (int r = 0; r < a.nranks; ++r) a.buf[r][off + i] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1ull) == gridDim.x - 1) {
+        ctr[1] = 0;
+        for (int r = 0; r < a.nranks; ++r)
+            if (r != a.rank) st_release_sys(a.flag[r] + a.rank, e + 1);
+        for (int r = 0; r < a.nranks; ++r) {
+            if (r == a.rank) continue;
+            long long spins = 0;
+            while (ld_acquire_sys(a.myflags + r) < e + 1) {
+                __nanosleep(64);
+                if (++spins == (1ll << 28)) {
+                    printf("pairamg: p2p segment gather flag wait timed out\n");
+                    __trap();
+                }
+            }
+        }
+        ctr[0] = e + 1;
+        __threadfence_system();
+    }
+}
+}  // namespace
+
+void p2p_seg_destroy(P2PSegGather& G) {
+    for (void* p : G.opened) cudaIpcCloseMemHandle(p);
+    G.opened.clear();
+    if (G.buf) cudaFree(G.buf);
+    if (G.flags) cudaFree(G.flags);
+    G.buf = nullptr;
+    G.flags = nullptr;
+    G.peer_buf.clear();
+    G.peer_flags.clear();
+    G.ok = false;
+}
+
+P2PSegGather::~P2PSegGather() { p2p_seg_destroy(*this); }
+
+void p2p_seg_setup(Runtime& rt, P2PSegGather& G, int64_t total, cudaStream_t s) {
+    p2p_seg_destroy(G);
+    if (rt.nranks() == 1 || rt.nranks() > kSegMaxRanks) return;
+    G.nranks = rt.nranks();
+    G.rank = rt.rank();
+    G.total = total;
+    struct SBlob {
+        cudaIpcMemHandle_t buf, flags;
+        int32_t ok;
+    } mine;
+    std::memset(&mine, 0, sizeof mine);
+    mine.ok = cudaMalloc(&G.buf, 8 * static_cast<size_t>(std::max<int64_t>(total, 1))) == cudaSuccess &&
+              cudaMalloc(&G.flags, 8 * G.nranks) == cudaSuccess && cudaMemset(G.flags, 0, 8 * G.nranks) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.buf, G.buf) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.flags, G.flags) == cudaSuccess;
+    cudaGetLastError();
+    const std::vector<uint8_t> all = rt.allgather_bytes(&mine, sizeof mine);
+    std::vector<SBlob> blobs(static_cast<size_t>(G.nranks));
+    std::memcpy(blobs.data(), all.data(), all.size());
+    bool ok = true;
+    for (const SBlob& b : blobs) ok = ok && b.ok;
+    for (int r = 0; ok && r < G.nranks; ++r) {
+        if (r == G.rank) {
+            G.peer_buf.push_back(G.buf);
+            G.peer_flags.push_back(G.flags);
+            continue;
+        }
+        void* m = nullptr;
+        void* f = nullptr;
+        if (cudaIpcOpenMemHandle(&m, blobs[static_cast<size_t>(r)].buf, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&f, blobs[static_cast<size_t>(r)].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+        }
+        G.opened.push_back(m);
+        G.opened.push_back(f);
+        G.peer_buf.push_back(static_cast<double*>(m));
+        G.peer_flags.push_back(static_cast<unsigned long long*>(f));
+    }
+    if (rt.allreduce_sum_i64(ok ? 1 : 0) != G.nranks) {  // all or none
+        p2p_seg_destroy(G);
+        return;
+    }
+    G.ctr.alloc(2, s);
+    G.ctr.zero(s);
+    PB_CUDA(cudaStreamSynchronize(s));
+    G.ok = true;
+}
+
+void p2p_seg_gather(P2PSegGather& G, const double* src, int64_t cnt, int64_t off, cudaStream_t s) {
+    SegArgs a{};
+    a.nranks = G.nranks;
+    a.rank = G.rank;
+    for (int r = 0; r < G.nranks; ++r) {
+        a.buf[r] = G.peer_buf[static_cast<size_t>(r)];
+        a.flag[r] = G.peer_flags[static_cast<size_t>(r)];
+    }
+    a.myflags = G.flags;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((cnt + 2047) / 2048, 2 * kSmCount)));
+    launch_k<4>(k_seg_gather, grid, 256, 0, s, src, cnt, off, a, G.ctr.get());
+    PB_CHECK_LAUNCH();
+}
+
+}  // namespace pb

@@ -64,6 +64,32 @@ struct P2PGather {
 };
 
 void p2p_gather_setup(Runtime& rt, P2PGather& G, int kmax, cudaStream_t s);
+
+// Segment allgather into one replicated vector (the restricted right-hand
+// side entering the first replicated coarse level): every rank stores its
+// rows [off, off + cnt) straight into every rank's copy of the vector over
+// NVLink, raises its flag there and waits for all flags.  Single-buffered:
+// consecutive gathers must be separated by a collective step (the FCG dot
+// allgather of every iteration does it; Solver::vcycle adds one).
+constexpr int kSegMaxRanks = 16;
+struct P2PSegGather {
+    bool ok = false;
+    int nranks = 0, rank = 0;
+    int64_t total = 0;
+    double* buf = nullptr;                       // total doubles (IPC-exported): the gathered vector
+    unsigned long long* flags = nullptr;         // nranks (IPC-exported), slot = sender
+    std::vector<double*> peer_buf;               // per rank (own: buf)
+    std::vector<unsigned long long*> peer_flags;
+    std::vector<void*> opened;
+    DBuf<unsigned long long> ctr;                // [0] gathers done, [1] blocks done
+    ~P2PSegGather();
+};
+// Collective; leaves G.ok = false (NCCL stays) when IPC is unavailable.
+void p2p_seg_setup(Runtime& rt, P2PSegGather& G, int64_t total, cudaStream_t s);
+void p2p_seg_destroy(P2PSegGather& G);
+// G.buf[off + i] = src[i] on every rank, all ranks' segments present when the
+// kernel completes (stream s, graph-capturable).
+void p2p_seg_gather(P2PSegGather& G, const double* src, int64_t cnt, int64_t off, cudaStream_t s);
 // recv[r*K + k] = rank r's send[k], on stream s (device-side, graph-capturable).
 void p2p_allgather(P2PGather& G, const double* send, double* recv, int K, cudaStream_t s);
 

@@ -1608,6 +1608,8 @@ struct SplitPlan {
     int grid;
 };
 
+constexpr int kMaxPush = 2 * kSmCount;  // push blocks of 2048 values (8 per thread)
+
 SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs) {
     SplitPlan P{};
     P.la = (I.sten_L == 7 || I.sten_L == 27) && sten_center(I) ? I.sten_L : 0;
@@ -1629,7 +1631,7 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
         P.h.b.nown = static_cast<int>(I.xlen - hs->nhalo);
         if (hs->fused) {  // push blocks ahead of the boundary blocks
             const int64_t nsend = hs->off[hs->npeers];
-            P.h.npush = static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(1, (nsend + 2047) / 2048)));
+            P.h.npush = static_cast<int>(std::min<int64_t>(kMaxPush, std::max<int64_t>(1, (nsend + 2047) / 2048)));
             P.h.npeers = hs->npeers;
             for (int i = 0; i <= hs->npeers; ++i) P.h.off[i] = hs->off[i];
             for (int i = 0; i < hs->npeers; ++i) {
@@ -1676,8 +1678,8 @@ void sell_apply_split(const Sell& I, const Sell& B, const SellOpArgs& o, const H
 #undef PB_SPLIT2
 }
 
-// upper bound: the fused push adds <= 32 blocks
-int sell_split_dots_grid(const Sell& I, const Sell& B) { return split_plan(I, B, true, nullptr).grid + 32; }
+// upper bound: the fused push adds <= kMaxPush blocks
+int sell_split_dots_grid(const Sell& I, const Sell& B) { return split_plan(I, B, true, nullptr).grid + kMaxPush; }
 
 int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* v, const double* r, const double* q,
                          double* partials, int max_blocks, const HaloSrc& hs, cudaStream_t s) {

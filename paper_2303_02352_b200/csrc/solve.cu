@@ -330,6 +330,22 @@ void Solver::destroy_graph() {
     loop_graph_ = nullptr;
 }
 
+// Multi-rank solves run the device-side loop only when nothing in the
+// iteration goes through NCCL (a conditional graph body with NCCL kernels
+// hung): NVLink halos on every distributed level, the P2P dot allgather and
+// the P2P replicated-rhs gather.
+bool Solver::nccl_free_iteration() {
+    if (rt.nranks() == 1) return true;
+    if (!env_flag("PAIRAMG_GRAPH_LOOP_MR", false) || !dots_gather_.ok) return false;  // measured no faster at N=2
+    if (h.rep_level >= 0 && !rep_gather_.ok) return false;
+    const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
+    for (int k = 0; k < nd; ++k) {
+        const Level& L = *h.levels[static_cast<size_t>(k)];
+        if (L.A.halo.has_traffic() && !L.p2p.ok) return false;
+    }
+    return true;
+}
+
 void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters) {
     if (loop_graph_ && loop_cc_.pre_sweeps == cc.pre_sweeps && loop_cc_.post_sweeps == cc.post_sweeps &&
         loop_cc_.coarsest_sweeps == cc.coarsest_sweeps && loop_cc_.relax_weight == cc.relax_weight &&
@@ -376,6 +392,9 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
         const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
         for (int k = 0; k < nd; ++k) p2p_setup(rt, h.levels[static_cast<size_t>(k)]->A.halo, h.levels[static_cast<size_t>(k)]->p2p, s_);
     }
+    p2p_seg_destroy(rep_gather_);
+    if (rt.nranks() > 1 && h.rep_level >= 0 && env_flag("PAIRAMG_P2P", true) && env_flag("PAIRAMG_P2P_REP", true))
+        p2p_seg_setup(rt, rep_gather_, h.rep[0]->A.n, s_);  // collective
     if (env_flag("PAIRAMG_TRANSFER_CODES", true)) {
         auto codes = [&](Level& L) {
             if (L.pval.empty()) return;
@@ -678,14 +697,19 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
                                                            T.rhs.get(), T.A.n);
     PB_CHECK_LAUNCH();
     launches_ += 1;
-    if (gather) {  // one padded allgather of the restricted rhs, then redundant coarse levels
+    const double* crhs = C.rhs.get();
+    if (gather && rep_gather_.ok) {  // NVLink stores of the restricted rhs into every rank's copy
+        p2p_seg_gather(rep_gather_, T.rhs.get(), T.A.n, h.rep_offsets[static_cast<size_t>(rt.rank())], s_);
+        crhs = rep_gather_.buf;
+        launches_ += 1;
+    } else if (gather) {  // one padded allgather of the restricted rhs, then redundant coarse levels
         gather_segments(rt, T.rhs.get(), T.A.n, h.rep_send.get(), h.rep_recv.get(), h.rep_max, h.rep_offsets,
                         h.rep_counts, C.rhs.get(), s_);
         launches_ += 2;
     }
     double* e = nullptr;
     end_time(lc);
-    vcycle_enqueue(k + 1, C.rhs.get(), e, cc);
+    vcycle_enqueue(k + 1, crhs, e, cc);
     begin_time(lc);
     if (gather) e += h.rep_offsets[static_cast<size_t>(rt.rank())];
     int post = cc.post_sweeps;
@@ -780,7 +804,9 @@ ZeroStart Solver::zero_start_args(const CycleConfig& cc) {
     z.x = L0.x.get();
     z.omega = cc.relax_weight;
     const Sell& S = L0.sell_all;
-    if (L0.A.halo.n_halo == 0 && S.format == Sell::kSten && S.nrows == L0.A.n) {
+    // the pattern id of every owned row names its l1 diagonal (pdiag), halo
+    // or not: 1 B per row instead of the 8 B l1 stream
+    if (S.format == Sell::kSten && S.nrows == L0.A.n && S.rows.empty() && S.row0 == 0) {
         z.pid = S.pid.get();
         z.ptab = S.pdiag.get();
     } else {
@@ -950,7 +976,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             graph_prec_ = precflag;
             graph_timing_ = timing;
         }
-        const bool device_loop = loop_ok && rt.nranks() == 1 && !timing && env_flag("PAIRAMG_GRAPH_LOOP", true);
+        const bool device_loop = loop_ok && !timing && env_flag("PAIRAMG_GRAPH_LOOP", true) && nccl_free_iteration();
         if (device_loop) {
             // the whole iteration loop as ONE graph launch: a conditional WHILE
             // node re-runs the captured iteration until k_loop_ctl clears it
@@ -1010,6 +1036,9 @@ void Solver::vcycle(const double* d_r, double* d_x, const CycleConfig& cc) {
     timing = t;
     if (n_) PB_CUDA(cudaMemcpyAsync(d_x, out, 8 * n_, cudaMemcpyDeviceToDevice, s_));
     PB_CUDA(cudaStreamSynchronize(s_));
+    // the single-buffered replicated-rhs gather needs a collective step between
+    // two V-cycles (inside FCG the dot allgather is one)
+    if (rep_gather_.ok) rt.allreduce_sum_i64(0);
 }
 
 void Solver::spmv(int level, const double* d_x, double* d_y) {

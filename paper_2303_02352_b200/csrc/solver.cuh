@@ -67,6 +67,7 @@ public:
     bool bnd_on_comm = true;  // halo boundary rows computed on the comm stream behind the receive
     int halo_grid_ = 0;       // CTA cap of interior kernels on halo levels (0 = uncapped)
     P2PGather dots_gather_;   // NVLink allgather of the per-iteration dot partials
+    P2PSegGather rep_gather_; // NVLink gather of the first replicated level's right-hand side
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
 
@@ -91,6 +92,7 @@ private:
     void begin_time(int kclass);
     void end_time(int kclass);
     void collect_times();
+    bool nccl_free_iteration();
     void destroy_graph();
 
     cudaStream_t s_;
