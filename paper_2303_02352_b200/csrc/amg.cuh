@@ -38,6 +38,8 @@ struct Level {
     // solve-time layout
     Sell sell_all;           // all rows (no halo)
     Sell sell_int, sell_bnd; // interior / boundary rows (halo present)
+    Sell sell_bndw;          // boundary rows as wide STEN (split launches) when sell_bnd is not STEN
+    const Sell& split_bnd() const { return sell_bnd.format == Sell::kSten ? sell_bnd : sell_bndw; }
     // V-cycle work vectors
     DBuf<double> x, xt;      // n + n_halo (ping-pong iterates)
     DBuf<double> rhs, res;   // n

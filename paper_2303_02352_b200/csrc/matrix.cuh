@@ -102,7 +102,8 @@ struct Sell {
     int sten_L = 0, sten_offmin = 0, sten_offmax = 0;  // STEN: main pattern
     std::vector<int> sten_off;
     std::vector<double> sten_val;
-    std::vector<uint32_t> sten_mask;  // per pattern: absent main records
+    std::vector<uint32_t> sten_mask;  // per pattern: absent main records (L <= 32)
+    std::vector<unsigned long long> sten_mask64;  // the same, any L <= 64
     int64_t xlen = 0;         // gathered vector length (owned + halo slots)
     DBuf<int32_t> rows;       // row id of each SELL row; empty = row0 + index
     int64_t row0 = 0;
@@ -184,6 +185,10 @@ struct HaloSrc {
 // Interior (contiguous STEN) + boundary (STEN) rows in one launch; the
 // boundary blocks wait for the neighbours' pushes of this exchange.
 bool sell_split_ok(const Sell& interior, const Sell& boundary);
+// STEN with a main pattern of up to 64 records (split-launch boundary rows
+// only); false (S unusable) when the rows do not nest into one.
+bool build_sten_wide(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s,
+                     const double* l1);
 void sell_apply_split(const Sell& interior, const Sell& boundary, const SellOpArgs& o, const HaloSrc& hs,
                       cudaStream_t s);
 int sell_split_dots_grid(const Sell& interior, const Sell& boundary);

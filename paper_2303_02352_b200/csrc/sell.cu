@@ -955,19 +955,19 @@ void reset_pat(Sell& S) {
 // supersequence of the two, LCS dynamic programme); <= kStenMax records.
 // Slab-partition boundary rows, whose halo neighbour sits at a different
 // local offset on each face, nest this way.
-bool try_sten(Sell& S) {
+bool try_sten(Sell& S, int max_len = kStenMax) {
     if (S.npat < 1) return false;
     auto eq = [](const ulonglong2& a, const ulonglong2& b) { return a.x == b.x && a.y == b.y; };
     auto pat = [&](int p) {
         return std::vector<ulonglong2>(S.hptab.begin() + S.hpmeta[p].x, S.hptab.begin() + S.hpmeta[p].x + S.hpmeta[p].y);
     };
-    auto subseq = [&](const std::vector<ulonglong2>& P, const std::vector<ulonglong2>& M, uint32_t* present) {
+    auto subseq = [&](const std::vector<ulonglong2>& P, const std::vector<ulonglong2>& M, unsigned long long* present) {
         size_t j = 0;
-        uint32_t pr = 0;
+        unsigned long long pr = 0;
         for (const auto& r : P) {
             while (j < M.size() && !eq(M[j], r)) ++j;
             if (j == M.size()) return false;
-            pr |= 1u << j;
+            pr |= 1ull << j;
             ++j;
         }
         if (present) *present = pr;
@@ -999,17 +999,17 @@ bool try_sten(Sell& S) {
         }
         while (i < a) U.push_back(M[i++]);
         while (j < b) U.push_back(P[j++]);
-        if (U.size() > static_cast<size_t>(kStenMax)) return false;
+        if (U.size() > static_cast<size_t>(max_len)) return false;
         M.swap(U);
     }
     const int L = static_cast<int>(M.size());
-    if (L < 1 || L > kStenMax) return false;
+    if (L < 1 || L > max_len) return false;
     const ulonglong2* mr = M.data();
-    std::vector<uint32_t> mask(S.npat, 0u);
+    std::vector<unsigned long long> mask(S.npat, 0ull);
     for (int p = 0; p < S.npat; ++p) {
-        uint32_t present = 0;
+        unsigned long long present = 0;
         if (!subseq(pat(p), M, &present)) return false;
-        mask[p] = ~present & (L == 32 ? 0xFFFFFFFFu : ((1u << L) - 1u));
+        mask[p] = ~present & (L == 64 ? ~0ull : ((1ull << L) - 1ull));
     }
     S.sten_L = L;
     S.sten_off.assign(L, 0);
@@ -1024,7 +1024,9 @@ bool try_sten(Sell& S) {
     }
     S.sten_offmin = static_cast<int>(omin);
     S.sten_offmax = static_cast<int>(omax);
-    S.sten_mask = mask;
+    S.sten_mask64 = mask;
+    S.sten_mask.assign(mask.size(), 0u);
+    for (size_t p = 0; p < mask.size(); ++p) S.sten_mask[p] = static_cast<uint32_t>(mask[p]);  // used iff L <= 32
     S.ptab.reset();
     S.pmeta.reset();  // pdiag stays: the FCG update reads it (fused zero-start)
     S.format = Sell::kSten;
@@ -1154,6 +1156,19 @@ StenParam sten_param(const Sell& S) {
     }
     for (int q = 0; q < 256; ++q) {
         p.pmask[q] = q < S.npat ? S.sten_mask[q] : 0u;
+        p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
+    }
+    return p;
+}
+
+StenParamW sten_param_w(const Sell& S) {
+    StenParamW p{};
+    for (int k = 0; k < S.sten_L; ++k) {
+        p.off[k] = S.sten_off[k];
+        p.val[k] = S.sten_val[k];
+    }
+    for (int q = 0; q < 256; ++q) {
+        p.pmask[q] = q < S.npat ? S.sten_mask64[q] : 0ull;
         p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
     }
     return p;
@@ -1342,6 +1357,29 @@ bool build_value_codes(const double* v, int64_t n, DBuf<uint8_t>& code, std::vec
 
 namespace {
 
+void sell_prologue(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s) {
+    S = Sell();
+    S.nrows = nrows;
+    S.nslices = (nrows + 31) / 32;
+    S.xlen = M.n + M.halo.n_halo;
+    if (S.nslices * 32 >= (int64_t(1) << 31))
+        fail(PAIRAMG_INVALID_ARGUMENT, "sell: more than 2^31 rows per rank");
+    if (rows && nrows) {
+        // An ascending row set that is one contiguous range (the interior of a
+        // slab partition) is addressed by offset: no row-id load per row.
+        int32_t ends[2] = {0, 0};
+        PB_CUDA(cudaMemcpyAsync(&ends[0], rows, 4, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaMemcpyAsync(&ends[1], rows + nrows - 1, 4, cudaMemcpyDeviceToHost, s));
+        PB_CUDA(cudaStreamSynchronize(s));
+        if (static_cast<int64_t>(ends[1]) - ends[0] == nrows - 1) {
+            S.row0 = ends[0];
+        } else {
+            S.rows.alloc(static_cast<size_t>(nrows), s);
+            PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+}
+
 // SELL-32 slice offsets (elements, multiples of 32) from the rows' lengths.
 void slice_widths(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s) {
     S.slice_off.alloc(static_cast<size_t>(S.nslices + 1), s);
@@ -1398,28 +1436,22 @@ bool try_coded(const DevMatrix& M, const int32_t* rows, Sell& S, cudaStream_t s)
 
 }  // namespace
 
+namespace {
+void sell_prologue(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s);
+}
+
+bool build_sten_wide(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s,
+                     const double* l1) {
+    sell_prologue(M, rows, nrows, S, s);
+    if (nrows && try_pattern(M, rows, S, l1, s) && try_sten(S, kStenWide)) return true;
+    S = Sell();
+    return false;
+}
+
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict,
                 const double* l1) {
-    S = Sell();
-    S.nrows = nrows;
-    S.nslices = (nrows + 31) / 32;
-    S.xlen = M.n + M.halo.n_halo;
-    if (S.nslices * 32 >= (int64_t(1) << 31))
-        fail(PAIRAMG_INVALID_ARGUMENT, "sell: more than 2^31 rows per rank");
-    if (rows && nrows) {
-        // An ascending row set that is one contiguous range (the interior of a
-        // slab partition) is addressed by offset: no row-id load per row.
-        int32_t ends[2] = {0, 0};
-        PB_CUDA(cudaMemcpyAsync(&ends[0], rows, 4, cudaMemcpyDeviceToHost, s));
-        PB_CUDA(cudaMemcpyAsync(&ends[1], rows + nrows - 1, 4, cudaMemcpyDeviceToHost, s));
-        PB_CUDA(cudaStreamSynchronize(s));
-        if (static_cast<int64_t>(ends[1]) - ends[0] == nrows - 1) {
-            S.row0 = ends[0];
-        } else {
-            S.rows.alloc(static_cast<size_t>(nrows), s);
-            PB_CUDA(cudaMemcpyAsync(S.rows.get(), rows, 4 * nrows, cudaMemcpyDeviceToDevice, s));
-        }
-    }
+    sell_prologue(M, rows, nrows, S, s);
+
     // Format choice (measured on B200): DICT keeps 32 registers
     // and full occupancy, best for short rows; PAT removes the per-entry code
     // stream, best once rows are long (27-point: 187 vs 198 us per L0 sweep).
@@ -1616,7 +1648,7 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
     P.r2 = P.la != 0 && sten_rpt2(I, dots);
     P.a = sten_args_of(I, P.r2 ? 512 : 256);
     P.h.pa = sten_param(I);
-    P.h.pb = sten_param(B);
+    P.h.pb = sten_param_w(B);
     P.h.b = sten_args_of(B);
     P.h.nblk_a = P.a.nblk;
     P.h.nblk_b = P.h.b.nblk;

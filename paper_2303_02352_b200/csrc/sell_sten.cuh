@@ -30,6 +30,17 @@ struct StenParam {
     double pdiag[256];    // l1 diagonal of the pattern (bitwise = l1_diagonal)
 };
 
+// Boundary rows of a split launch: the faces of an interior rank reach
+// different halo slots, so their merged main pattern can exceed 32 records
+// (27-point: 36); the boundary blocks take up to 64 (generic length only).
+constexpr int kStenWide = 64;
+struct StenParamW {
+    int off[kStenWide];
+    double val[kStenWide];
+    unsigned long long pmask[256];
+    double pdiag[256];
+};
+
 struct StenArgs {
     const uint8_t* pid;  // pattern id per row (indexed by row id)
     const int32_t* rows;
@@ -53,9 +64,8 @@ struct StenArgs {
 // runtime a.L <= kStenMax).  EDGE clamps the gather columns into [0, xlen).
 // With LL > 0 the launcher guarantees record LL/2 is the diagonal (offset
 // 0, sorted symmetric stencil), so its gather doubles as the row's own x.
-template <int LL, bool EDGE, bool HALO = false>
-__device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m,
-                                               double& own) {
+template <int LL, bool EDGE, bool HALO = false, typename PT = StenParam, typename MT = uint32_t>
+__device__ __forceinline__ double sten_row_sum(const StenArgs& a, const PT& p, int row, MT m, double& own) {
     if constexpr (LL == 0) {
         // generic length: batches of 8 loads (registers, no local-memory array)
         double sum = 0.0;
@@ -70,7 +80,7 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenPara
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int k = k0 + j;
-                if (k < a.L && !((m >> k) & 1u)) sum = dadd(sum, dmul(p.val[k], xv[j]));
+                if (k < a.L && !((m >> k) & 1u)) sum = dadd(sum, dmul(p.val[k < a.L ? k : 0], xv[j]));
             }
         }
         return sum;
@@ -98,10 +108,10 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const StenPara
     }
 }
 
-template <int LL, bool HALO = false>
-__device__ __forceinline__ double sten_sum(const StenArgs& a, const StenParam& p, int row, uint32_t m, bool edge,
-                                           double& own) {
-    return edge ? sten_row_sum<LL, true, HALO>(a, p, row, m, own) : sten_row_sum<LL, false, HALO>(a, p, row, m, own);
+template <int LL, bool HALO = false, typename PT = StenParam, typename MT = uint32_t>
+__device__ __forceinline__ double sten_sum(const StenArgs& a, const PT& p, int row, MT m, bool edge, double& own) {
+    return edge ? sten_row_sum<LL, true, HALO, PT, MT>(a, p, row, m, own)
+                : sten_row_sum<LL, false, HALO, PT, MT>(a, p, row, m, own);
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
@@ -127,8 +137,8 @@ __device__ __forceinline__ void sten_prefetch(const StenArgs& a, const double* o
 // One thread per row (32-bit indices: a Sell holds < 2^31 rows); rows past
 // nrows recompute the last row and do not store (every lane reaches the
 // warp vote).  The clamp test is per block (uniform).
-template <int OP, bool ROWS, int LL, bool HALO = false>
-__device__ __forceinline__ void sten1_block(const StenArgs& a, const StenParam& p, int blk) {
+template <int OP, bool ROWS, int LL, bool HALO = false, typename PT = StenParam>
+__device__ __forceinline__ void sten1_block(const StenArgs& a, const PT& p, int blk) {
     const int i = blk * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
     const int ic = valid ? i : a.nrows - 1;
@@ -251,8 +261,8 @@ __global__ void __launch_bounds__(256) k_sten2(StenArgs a, const __grid_constant
 }
 
 // v = A w + block partials of (w.r, w.v, w.q) (fixed order -> deterministic).
-template <bool ROWS, int LL, bool HALO = false>
-__device__ __forceinline__ void sten1_dots_block(const StenArgs& a, const StenParam& p, int blk, double& sa, double& sb,
+template <bool ROWS, int LL, bool HALO = false, typename PT = StenParam>
+__device__ __forceinline__ void sten1_dots_block(const StenArgs& a, const PT& p, int blk, double& sa, double& sb,
                                                  double& sg) {
     const int i = blk * 256 + static_cast<int>(threadIdx.x);
     const bool valid = i < a.nrows;
@@ -449,7 +459,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
 // other GPU: no deadlock, whatever holds SM slots here.  The last boundary
 // block advances the exchange counter (read by the next push).
 struct HaloSplit {
-    StenParam pa, pb;          // interior / boundary main patterns
+    StenParam pa;              // interior main pattern
+    StenParamW pb;             // boundary main pattern (<= 64 records)
     StenArgs b;                // boundary rows (list, or range on an end rank)
     int nblk_a, nblk_b;
     const unsigned long long* flags;  // this rank's flag slots (indexed by sender)

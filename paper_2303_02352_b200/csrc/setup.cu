@@ -938,6 +938,12 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             // one main pattern (slab partitions), else PAT/DICT/PLAIN
             build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s,
                        env_flag("PAIRAMG_SELL_DICT", true) && env_flag("PAIRAMG_BND_FORMATS", true), L.l1.get());
+            // an interior rank's two faces reach different halo slots: with
+            // 27 points their merged pattern has 36 records -> wide STEN for
+            // the split launch (boundary blocks take up to 64)
+            if (L.sell_bnd.format != Sell::kSten && env_flag("PAIRAMG_SELL_STEN", true) &&
+                env_flag("PAIRAMG_STEN_WIDE", true))
+                build_sten_wide(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bndw, s, L.l1.get());
             // whole level incl. halo columns, for the exchange-then-compute
             // schedule (slab partitions keep constant halo column offsets,
             // so DICT/PAT usually still apply)

@@ -420,7 +420,8 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
             std::fprintf(stderr, "rank %d level %d %s rows %lld halo %lld p2p %d: %s%s%s\n", rt.rank(), k,
                          rep ? "replicated" : "distributed", static_cast<long long>(L.A.n),
                          static_cast<long long>(L.A.halo.n_halo), L.p2p.ok ? 1 : 0,
-                         L.A.halo.n_halo > 0 ? ("int " + desc(L.sell_int) + " bnd " + desc(L.sell_bnd) + " all ").c_str() : "",
+                         L.A.halo.n_halo > 0 ? ("int " + desc(L.sell_int) + " bnd " + desc(L.sell_bnd) +
+                                                (L.sell_bndw.format == Sell::kSten ? " bnd-wide " + desc(L.sell_bndw) : "") + " all ").c_str() : "",
                          desc(L.sell_all).c_str(), L.pcode.empty() ? "" : " pcode");
         }
     }
@@ -442,8 +443,8 @@ void Solver::ensure_vectors() {
     int64_t dots_blocks = sell_dots_grid(L0.sell_all);
     if (L0.A.halo.n_halo > 0) {
         dots_blocks = std::max<int64_t>(dots_blocks, int64_t(sell_dots_grid(L0.sell_int)) + sell_dots_grid(L0.sell_bnd));
-        if (sell_split_ok(L0.sell_int, L0.sell_bnd))
-            dots_blocks = std::max<int64_t>(dots_blocks, sell_split_dots_grid(L0.sell_int, L0.sell_bnd));
+        if (sell_split_ok(L0.sell_int, L0.split_bnd()))
+            dots_blocks = std::max<int64_t>(dots_blocks, sell_split_dots_grid(L0.sell_int, L0.split_bnd()));
     }
     max_blocks_ = static_cast<int>(std::max<int64_t>(dots_blocks, kSmCount * 8));
     partials_.alloc(static_cast<size_t>(3 * max_blocks_), s_);
@@ -558,13 +559,13 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         tr = &htrace_[static_cast<size_t>(hcount_++)];
         hrec((*tr)[0], s_);
     }
-    if (L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.sell_bnd) &&
+    if (L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) &&
         (o.op == kSpmv || o.op == kJacobi || o.op == kResid)) {
         // push this rank's boundary values into the neighbours, then one
         // launch whose boundary blocks wait for theirs (no comm stream)
         const HaloSrc hs = p2p_halo_src(L.A.halo, L.p2p);
         if (!hs.fused) p2p_push(L.A.halo, L.p2p, o.x, s_);
-        sell_apply_split(L.sell_int, L.sell_bnd, o, hs, s_);
+        sell_apply_split(L.sell_int, L.split_bnd(), o, hs, s_);
         launches_ += hs.fused ? 1 : 2;
         end_time(kc);
         return;
@@ -833,10 +834,10 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         exchange(L0, w, s_);
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
-    } else if (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.sell_bnd)) {
+    } else if (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.split_bnd())) {
         const HaloSrc hs = p2p_halo_src(L0.A.halo, L0.p2p);
         if (!hs.fused) p2p_push(L0.A.halo, L0.p2p, w, s_);
-        dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get(),
+        dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.split_bnd(), w, v_.get(), r_.get(), q_.get(), partials_.get(),
                                           max_blocks_, hs, s_);
         launches_ += hs.fused ? 1 : 2;
     } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
@@ -861,7 +862,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         launches_ += 1;
     }
     if ((L0.A.halo.has_traffic() && !overlap) || (L0.A.halo.n_halo > 0 && bnd_on_comm) ||
-        (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.sell_bnd))) {
+        (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.split_bnd()))) {
         // done above
     } else if (L0.A.halo.n_halo > 0) {
         const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
