@@ -95,6 +95,7 @@ struct Sell {
     DBuf<ulonglong2> ptab;    // PAT: pattern records {value bits, column - row}
     DBuf<int2> pmeta;         // PAT: {first record, length} per pattern
     DBuf<double> pdiag;       // PAT: l1 diagonal per pattern (bitwise = l1_diagonal)
+    DBuf<double> pinv;        // RN(1 / pdiag) per pattern (ddiv_recip; 0 = divide)
     int npat = 0, maxlen = 0;
     std::vector<ulonglong2> hptab;  // PAT host copies (STEN conversion)
     std::vector<int2> hpmeta;

@@ -50,6 +50,13 @@ constexpr int kDictMax = 255;
 constexpr int kTableCap = 1024;
 constexpr ull kEmptyLo = 0x8000000000000000ULL;
 
+// STEN sweeps divide by the pattern's l1 diagonal through ddiv_recip
+// (common.cuh) with a host-computed reciprocal; PAIRAMG_FAST_DIV=0 divides.
+bool fast_div() {
+    static const bool on = env_flag("PAIRAMG_FAST_DIV", true);
+    return on;
+}
+
 struct SellArgs {
     const int64_t* soff;  // PLAIN
     const int32_t* col;
@@ -941,6 +948,7 @@ void reset_pat(Sell& S) {
     S.ptab.reset();
     S.pmeta.reset();
     S.pdiag.reset();
+    S.pinv.reset();
     S.npat = 0;
     S.maxlen = 0;
     S.hptab.clear();
@@ -1101,6 +1109,13 @@ bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double*
     if (!rec.empty()) PB_CUDA(cudaMemcpyAsync(S.ptab.get(), rec.data(), 16 * rec.size(), cudaMemcpyHostToDevice, s));
     PB_CUDA(cudaMemcpyAsync(S.pmeta.get(), meta.data(), 8 * meta.size(), cudaMemcpyHostToDevice, s));
     PB_CUDA(cudaMemcpyAsync(S.pdiag.get(), pd.data(), 8 * pd.size(), cudaMemcpyHostToDevice, s));
+    {
+        std::vector<double> inv(pd.size());
+        for (size_t i = 0; i < pd.size(); ++i) inv[i] = fast_div() && pd[i] != 0.0 ? 1.0 / pd[i] : 0.0;
+        S.pinv.alloc(inv.size(), s);
+        PB_CUDA(cudaMemcpyAsync(S.pinv.get(), inv.data(), 8 * inv.size(), cudaMemcpyHostToDevice, s));
+        PB_CUDA(cudaStreamSynchronize(s));  // inv is a host temporary
+    }
     DBuf<int> dsp(kTableCap, s);
     PB_CUDA(cudaMemcpyAsync(dsp.get(), slot_pid.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
     S.pid.alloc(static_cast<size_t>(M.n), s);
@@ -1157,6 +1172,7 @@ StenParam sten_param(const Sell& S) {
     for (int q = 0; q < 256; ++q) {
         p.pmask[q] = q < S.npat ? S.sten_mask[q] : 0u;
         p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
+        p.pinv[q] = fast_div() ? 1.0 / p.pdiag[q] : 0.0;
     }
     return p;
 }
@@ -1170,6 +1186,7 @@ StenParamW sten_param_w(const Sell& S) {
     for (int q = 0; q < 256; ++q) {
         p.pmask[q] = q < S.npat ? S.sten_mask64[q] : 0ull;
         p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
+        p.pinv[q] = fast_div() ? 1.0 / p.pdiag[q] : 0.0;
     }
     return p;
 }

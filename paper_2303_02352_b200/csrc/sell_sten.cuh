@@ -28,6 +28,7 @@ struct StenParam {
     double val[kStenMax];
     uint32_t pmask[256];  // main records absent from the pattern (bit k = record k)
     double pdiag[256];    // l1 diagonal of the pattern (bitwise = l1_diagonal)
+    double pinv[256];     // RN(1 / pdiag) for ddiv_recip (0 = divide)
 };
 
 // Boundary rows of a split launch: the faces of an interior rank reach
@@ -39,6 +40,7 @@ struct StenParamW {
     double val[kStenWide];
     unsigned long long pmask[256];
     double pdiag[256];
+    double pinv[256];
 };
 
 struct StenArgs {
@@ -157,7 +159,7 @@ __device__ __forceinline__ void sten1_block(const StenArgs& a, const PT& p, int 
         a.y[row] = dsub(ri, sum);
     } else {
         const double t = dsub(ri, sum);  // omega = 1 (the paper's setting) multiplies exactly: skip it
-        a.y[row] = dadd(xi, ddiv(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q]));
+        a.y[row] = dadd(xi, ddiv_recip(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q], p.pinv[q]));
     }
 }
 
@@ -214,7 +216,7 @@ __device__ __forceinline__ void sten_store(const StenArgs& a, const StenParam& p
         a.y[row] = dsub(ri, sum);
     } else {
         const double t = dsub(ri, sum);
-        a.y[row] = dadd(xi, ddiv(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q]));
+        a.y[row] = dadd(xi, ddiv_recip(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q], p.pinv[q]));
     }
 }
 
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
     const int n = a.nrows;
     const int L = LL ? LL : a.L;
     int rowv[2];
-    double rv[2], dv[2];
+    double rv[2], dv[2], yv[2];
     uint32_t mv[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -407,8 +409,9 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
             const int q = a.pid[row];
             rv[h] = a.r[row];
             dv[h] = p.pdiag[q];
+            yv[h] = p.pinv[q];
             mv[h] = p.pmask[q];
-            xs[0][t] = ddiv(a.omega == 1.0 ? rv[h] : dmul(a.omega, rv[h]), dv[h]);  // zero start
+            xs[0][t] = ddiv_recip(a.omega == 1.0 ? rv[h] : dmul(a.omega, rv[h]), dv[h], yv[h]);  // zero start
         }
     }
     cl.sync();
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
             }
             const int t = row - me * R;
             const double t1 = dsub(rv[h], sum);
-            xs[nxt][t] = dadd(xs[cur][t], ddiv(a.omega == 1.0 ? t1 : dmul(a.omega, t1), dv[h]));
+            xs[nxt][t] = dadd(xs[cur][t], ddiv_recip(a.omega == 1.0 ? t1 : dmul(a.omega, t1), dv[h], yv[h]));
         }
         cl.sync();
     }

@@ -109,8 +109,12 @@ CodeTab code_tab(const std::vector<double>& v) {
 template <bool ZS>
 __device__ __forceinline__ void zs_store(const ZeroStart& z, int64_t i, double rn) {
     if (!ZS) return;
-    const double di = z.pid ? z.ptab[z.pid[i]] : z.l1[i];
-    z.x[i] = ddiv(dmul(z.omega, rn), di);
+    if (z.pid) {
+        const int q = z.pid[i];
+        z.x[i] = ddiv_recip(dmul(z.omega, rn), z.ptab[q], z.pinv[q]);
+    } else {
+        z.x[i] = ddiv(dmul(z.omega, rn), z.l1[i]);
+    }
 }
 
 template <bool ZS>
@@ -810,6 +814,7 @@ ZeroStart Solver::zero_start_args(const CycleConfig& cc) {
     if (S.format == Sell::kSten && S.nrows == L0.A.n && S.rows.empty() && S.row0 == 0) {
         z.pid = S.pid.get();
         z.ptab = S.pdiag.get();
+        z.pinv = S.pinv.get();
     } else {
         z.l1 = L0.l1.get();
     }

@@ -16,6 +16,7 @@ struct ZeroStart {
     double* x = nullptr;
     const uint8_t* pid = nullptr;  // STEN level 0: pattern byte per row ...
     const double* ptab = nullptr;  // ... and the per-pattern l1 diagonal
+    const double* pinv = nullptr;  // ... and its reciprocal (ddiv_recip)
     const double* l1 = nullptr;    // otherwise the l1 array
     double omega = 1.0;
 };
