@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, cons
 
 #include "sell_win.cuh"
 #include "sell_sten.cuh"
+#include "sell_stenwin.cuh"
 
 // ------------------------------------------------------------------ PAT ---
 //
@@ -1191,6 +1192,107 @@ StenParamW sten_param_w(const Sell& S) {
     return p;
 }
 
+// Shared-memory window plan of a contiguous STEN row set (k_stenwin):
+// offsets closer than T/2 share a window.  Stored in S.win (rec[k].y = the
+// shared-memory base of main record k).
+constexpr int kStenWinT = 512;
+constexpr int kStenWinSmemCap = 96 * 1024;
+
+void plan_sten_windows(Sell& S) {
+    SellWin& P = S.win;
+    P = SellWin();
+    if (S.format != Sell::kSten || !S.rows.empty() || S.nrows == 0 || !sten_center(S) ||
+        (S.sten_L != 7 && S.sten_L != 27) || !env_flag("PAIRAMG_STEN_WIN", false))
+        return;
+    const int T = kStenWinT;
+    std::vector<int64_t> offs(S.sten_off.begin(), S.sten_off.end());
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    std::vector<std::pair<int64_t, int64_t>> win;
+    for (int64_t o : offs) {
+        if (!win.empty() && o - win.back().second <= T / 2)
+            win.back().second = o;
+        else
+            win.push_back({o, o});
+    }
+    if (win.size() > static_cast<size_t>(kWinMax)) return;
+    P.T = T;
+    P.nwin = static_cast<int>(win.size());
+    int off = 0;
+    std::vector<int> al(win.size());
+    for (size_t k = 0; k < win.size(); ++k) {
+        const int64_t lo = win[k].first, span = win[k].second - win[k].first;
+        al[k] = static_cast<int>((S.row0 + lo) & 1);
+        P.lo[k] = static_cast<int>(lo);
+        P.len[k] = static_cast<int>((al[k] + T + span + 1) & ~int64_t(1));
+        P.soff[k] = off;
+        off += P.len[k];
+    }
+    P.al_r = static_cast<int>(S.row0 & 1);
+    P.r_soff = off;
+    off += T + 2;
+    P.stage = off;
+    P.smem = static_cast<size_t>(2) * off * 8;
+    if (P.smem > static_cast<size_t>(kStenWinSmemCap)) return;
+    P.rec.assign(static_cast<size_t>(S.sten_L), make_ulonglong2(0ULL, 0ULL));
+    for (int k = 0; k < S.sten_L; ++k) {
+        const int64_t o = S.sten_off[static_cast<size_t>(k)];
+        for (size_t w = 0; w < win.size(); ++w)
+            if (o >= win[w].first && o <= win[w].second)
+                P.rec[static_cast<size_t>(k)].y = static_cast<ull>(P.soff[w] + al[w] + (o - win[w].first));
+    }
+    P.ntiles = static_cast<int>((S.nrows + T - 1) / T);
+    int per_sm = 0;
+    const void* fns[] = {reinterpret_cast<const void*>(&k_stenwin<kSpmv, 7>),
+                         reinterpret_cast<const void*>(&k_stenwin<kJacobi, 7>),
+                         reinterpret_cast<const void*>(&k_stenwin<kResid, 7>),
+                         reinterpret_cast<const void*>(&k_stenwin<kSpmv, 27>),
+                         reinterpret_cast<const void*>(&k_stenwin<kJacobi, 27>),
+                         reinterpret_cast<const void*>(&k_stenwin<kResid, 27>)};
+    for (const void* f : fns) {
+        PB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStenWinSmemCap));
+        int nb = 0;
+        PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 256, P.smem));
+        per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
+    }
+    if (per_sm < 1) return;
+    P.grid = std::min(P.ntiles, kSmCount * per_sm);
+    P.ok = true;
+}
+
+template <int OP>
+bool launch_stenwin(const Sell& S, const StenArgs& a0, cudaStream_t s) {
+    const SellWin& P = S.win;
+    if (!P.ok || S.format != Sell::kSten) return false;
+    StenWinArgs a{};
+    a.row0 = static_cast<int>(S.row0);
+    a.nrows = static_cast<int>(S.nrows);
+    a.ntiles = P.ntiles;
+    a.T = P.T;
+    a.xlen = S.xlen;
+    a.nwin = P.nwin;
+    for (int k = 0; k < P.nwin; ++k) {
+        a.lo[k] = P.lo[k];
+        a.len[k] = P.len[k];
+        a.soff[k] = P.soff[k];
+    }
+    a.r_soff = P.r_soff;
+    a.stage = P.stage;
+    a.al_r = P.al_r;
+    for (int k = 0; k < S.sten_L; ++k) a.base[k] = static_cast<int>(P.rec[static_cast<size_t>(k)].y);
+    a.pid = S.pid.get();
+    a.x = a0.x;
+    a.y = a0.y;
+    a.r = a0.r;
+    a.omega = a0.omega;
+    const StenParam p = sten_param(S);
+    if (S.sten_L == 7)
+        launch_k<2>(k_stenwin<OP, 7>, P.grid, 256, P.smem, s, a, p);
+    else
+        launch_k<2>(k_stenwin<OP, 27>, P.grid, 256, P.smem, s, a, p);
+    return true;
+}
+
 // Two rows per thread for the 7-record main pattern (k_sten2): +10% bandwidth.
 // 27 records: only the SpMV+dots kernel gains (122 vs 132 us; sweeps lose).
 bool sten_rpt2(const Sell& S, bool dots = false) {
@@ -1204,6 +1306,7 @@ inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nb
 // cap > 0: at most `cap` CTAs, grid-striding over the logical blocks.
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
+    if (!ROWS && cap == 0 && launch_stenwin<OP>(S, a0, s)) return;
     const StenParam p = sten_param(S);
     if (sten_rpt2(S)) {
         StenArgs a = sten_args_of(S, 512);
@@ -1486,7 +1589,10 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
         const int pref = env_int("PAIRAMG_SELL_PAT", -1);  // 1 force PAT, 0 never, -1 auto
         const bool want_pat = pref == 1 || (pref == -1 && maxlen > 16);
         if (env_flag("PAIRAMG_SELL_STEN", true) && maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
-            if (try_sten(S)) return;
+            if (try_sten(S)) {
+                plan_sten_windows(S);
+                return;
+            }
             if (want_pat) return;
             reset_pat(S);
         }
