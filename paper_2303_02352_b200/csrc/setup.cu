@@ -570,9 +570,52 @@ int64_t galerkin(const DevMatrix& A, const int64_t* pc, const double* pv, const 
     return nnz;
 }
 
+// P over A's column slots, overlapped: the owned part and
+// the halo exchange of P run on the communication stream as soon as the
+// matching is done, while the compute stream builds R, w_next and the
+// composed prolongator; extend_p_join makes the compute stream wait and
+// books only the exposed wait as spmm_comm.
+struct PExt {
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+};
+
+void extend_p_begin(Runtime& rt, DevMatrix& A, const int32_t* pcol, const double* pval, int64_t cbase,
+                    DBuf<int64_t>& pc, DBuf<double>& pv, PExt& x) {
+    cudaStream_t s = rt.stream(), c = rt.comm_stream();
+    const int64_t next = A.n + A.halo.n_halo;
+    pc.alloc(static_cast<size_t>(next), s);
+    pv.alloc(static_cast<size_t>(next), s);
+    cudaEvent_t ready;
+    PB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    PB_CUDA(cudaEventRecord(ready, s));  // pcol / pval and the buffers are ready
+    PB_CUDA(cudaStreamWaitEvent(c, ready, 0));
+    PB_CUDA(cudaEventDestroy(ready));
+    if (A.n) {
+        k_pext<<<blocks_for(A.n, 256), 256, 0, c>>>(pcol, pval, A.n, cbase, pc.get(), pv.get());
+        PB_CHECK_LAUNCH();
+    }
+    if (A.halo.has_traffic())
+        halo_exchange_pair(rt, A.halo, pc.get(), pc.get() + A.n, pv.get(), pv.get() + A.n, c);
+    PB_CUDA(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
+    PB_CUDA(cudaEventRecord(x.done, c));
+    x.pending = true;
+}
+
+void extend_p_join(Runtime& rt, PExt& x, SetupStats& st) {
+    if (!x.pending) return;
+    const auto t0 = Clock::now();
+    PB_CUDA(cudaEventSynchronize(x.done));
+    st.t_spmm_comm += since(t0);
+    PB_CUDA(cudaStreamWaitEvent(rt.stream(), x.done, 0));
+    PB_CUDA(cudaEventDestroy(x.done));
+    x.done = nullptr;
+    x.pending = false;
+}
+
 // P over A's column slots: owned from (pcol + cbase, pval), halo by exchange.
-void extend_p(Runtime& rt, DevMatrix& A, const int32_t* pcol, const double* pval, int64_t cbase,
-              DBuf<int64_t>& pc, DBuf<double>& pv, SetupStats& st) {
+[[maybe_unused]] void extend_p(Runtime& rt, DevMatrix& A, const int32_t* pcol, const double* pval, int64_t cbase,
+                               DBuf<int64_t>& pc, DBuf<double>& pv, SetupStats& st) {
     cudaStream_t s = rt.stream();
     const int64_t next = A.n + A.halo.n_halo;
     pc.alloc(static_cast<size_t>(next), s);
@@ -841,6 +884,15 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
                                      std::to_string(fine_n - coarse_n) + " of " + std::to_string(fine_n) +
                                      " rows");
 
+            // P's halo exchange in flight (comm stream) during R / w_next / composition
+            const bool more = step + 1 < cfg.aggregation_exponent && coarse_n > cfg.coarse_size_target;
+            const bool pair_galerkin = more || nsteps == 0;
+            DBuf<int64_t> pc;
+            DBuf<double> pv;
+            PExt px;
+            if (pair_galerkin && env_flag("PAIRAMG_SETUP_OVERLAP", false))
+                extend_p_begin(rt, *A_pair, agg.get(), pval.get(), cpart[rank], pc, pv, px);
+
             // ---- R, w_next, composition ----
             const auto tg = Clock::now();
             DBuf<int64_t> rrp;
@@ -866,11 +918,11 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             // ---- pairwise Galerkin, only when the next step (or a
             // single-step level) consumes it; the reference discards the
             // last pairwise product of a multi-step level (amg.cpp:261-264).
-            const bool more = step + 1 < cfg.aggregation_exponent && coarse_n > cfg.coarse_size_target;
-            if (more || nsteps == 1) {
-                DBuf<int64_t> pc;
-                DBuf<double> pv;
-                extend_p(rt, *A_pair, agg.get(), pval.get(), cpart[rank], pc, pv, h.stats);
+            if (pair_galerkin) {
+                if (px.pending)
+                    extend_p_join(rt, px, h.stats);
+                else
+                    extend_p(rt, *A_pair, agg.get(), pval.get(), cpart[rank], pc, pv, h.stats);
                 const auto tp = Clock::now();
                 const int64_t msg1 = rt.stats().total_messages();
                 DBuf<int64_t> orp, ocol;
@@ -898,13 +950,19 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         if (nsteps == 1) {
             Lc->A = std::move(*A_pair_own);
         } else {
+            DBuf<int64_t> pc;
+            DBuf<double> pv;
+            PExt px;
+            const bool ov = env_flag("PAIRAMG_SETUP_OVERLAP", false);
+            if (ov) extend_p_begin(rt, Lf.A, comp_col.get(), comp_val.get(), part[rank], pc, pv, px);
             DBuf<int64_t> rrp;
             DBuf<int32_t> rcol;
             DBuf<double> rval;
             build_R(comp_col.get(), comp_val.get(), Lf.A.n, nc_local, rrp, rcol, rval, s);
-            DBuf<int64_t> pc;
-            DBuf<double> pv;
-            extend_p(rt, Lf.A, comp_col.get(), comp_val.get(), part[rank], pc, pv, h.stats);
+            if (ov)
+                extend_p_join(rt, px, h.stats);
+            else
+                extend_p(rt, Lf.A, comp_col.get(), comp_val.get(), part[rank], pc, pv, h.stats);
             const auto tp = Clock::now();
             DBuf<int64_t> orp, ocol;
             DBuf<double> oval;
