@@ -13,15 +13,22 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-@pytest.mark.parametrize("world,overlap", [(2, 1), (2, 0), (4, 1)])
+ALT = {"PAIRAMG_FUSED_PUSH": "0", "PAIRAMG_SETUP_OVERLAP": "1", "PAIRAMG_GRAPH_LOOP_MR": "1"}
+
+
+@pytest.mark.parametrize("world,overlap", [(2, 1), (2, 0), (2, 2), (4, 1)])
 def test_distributed_parity(world, overlap):
-    """overlap=0: exchange-then-compute over the whole level (one Sell with halo columns)."""
+    """overlap=0: exchange-then-compute over the whole level (one Sell with halo columns);
+    overlap=2: the non-default paths (separate push launch, setup exchange
+    overlapped with R / composition, device-side FCG loop across ranks)."""
     if gpu_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + 10 * world + overlap),
            os.path.join(ROOT, "tests", "mp_parity.py")]
-    env = dict(os.environ, PAIRAMG_OVERLAP=str(overlap))
+    env = dict(os.environ, PAIRAMG_OVERLAP=str(min(overlap, 1)))
+    if overlap == 2:
+        env.update(ALT)
     r = subprocess.run(["timeout", "-k", "10", "300", *cmd], capture_output=True, text=True, timeout=400, cwd=ROOT,
                        env=env)
     out = r.stdout + r.stderr
