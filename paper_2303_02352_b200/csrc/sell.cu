@@ -1797,6 +1797,7 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
             P.h.send_idx = hs->send_idx;
         }
     }
+    P.h.bnd_last = env_flag("PAIRAMG_BND_LAST", true) ? 1 : 0;
     P.grid = P.h.npush + P.h.nblk_a + P.h.nblk_b;
     return P;
 }

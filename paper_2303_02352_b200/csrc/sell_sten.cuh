@@ -476,6 +476,7 @@ struct HaloSplit {
     // the neighbours' staging, then [npush, npush + nblk_b) are the boundary
     // rows and the rest the interior
     int npush, npeers;
+    int bnd_last;              // block order push | interior | boundary (else push | boundary | interior)
     int64_t off[9];
     double* dst[8];
     int64_t stride[8];
@@ -536,18 +537,24 @@ __device__ __forceinline__ void halo_done_p2p(const HaloSplit& h) {
     }
 }
 
+// 7 records: hold the interior at k_sten2's 5 CTAs/SM (<= 51 registers); the
+// push / generic boundary paths otherwise raise the whole kernel to 54 and
+// cost the interior a fifth of its warps.
 template <int OP, int LLA, bool R2, bool BROWS>
-__global__ void __launch_bounds__(256) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
+__global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();  // no early dependents: the boundary blocks wait on another GPU
-    // push blocks, then boundary blocks: dispatched at once, the push and the
-    // short wait for the neighbours' pushes overlap the interior rows
+    // push blocks first; then (bnd_last) the interior rows, whose pass covers
+    // the neighbours' pushes, and the boundary rows last, when their halo has
+    // arrived -- boundary blocks dispatched early would hold SM slots while
+    // they wait (measured +25-30 us per level-0 sweep at 4 GPUs)
     if (static_cast<int>(blockIdx.x) < h.npush) {
         halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
         return;
     }
-    const int bb = static_cast<int>(blockIdx.x) - h.npush;
-    const int blk = bb - h.nblk_b;
-    if (blk >= 0) {
+    const int rel = static_cast<int>(blockIdx.x) - h.npush;
+    const int bb = h.bnd_last ? rel - h.nblk_a : rel;
+    const int blk = h.bnd_last ? rel : rel - h.nblk_b;
+    if (h.bnd_last ? bb < 0 : blk >= 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
             const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
@@ -568,7 +575,7 @@ __global__ void __launch_bounds__(256) k_sten_split(StenArgs a, const __grid_con
 }
 
 template <int LLA, bool R2, bool BROWS>
-__global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
+__global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();
     double sa = 0.0, sb = 0.0, sg = 0.0;
     if (static_cast<int>(blockIdx.x) < h.npush) {  // push blocks first (zero partials)
@@ -576,9 +583,10 @@ __global__ void __launch_bounds__(256) k_sten_split_dots(StenArgs a, const __gri
         dots_block_store(sa, sb, sg, a.partials);
         return;
     }
-    const int bb = static_cast<int>(blockIdx.x) - h.npush;
-    const int blk = bb - h.nblk_b;  // then the boundary blocks
-    if (blk >= 0) {
+    const int rel = static_cast<int>(blockIdx.x) - h.npush;  // then interior / boundary as k_sten_split
+    const int bb = h.bnd_last ? rel - h.nblk_a : rel;
+    const int blk = h.bnd_last ? rel : rel - h.nblk_b;
+    if (h.bnd_last ? bb < 0 : blk >= 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
             const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
