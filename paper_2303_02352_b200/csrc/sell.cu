@@ -1164,6 +1164,16 @@ StenArgs sten_args_of(const Sell& S, int block_rows = 256) {
 // The fixed-length kernels take the row's own x from record L/2.
 bool sten_center(const Sell& S) { return S.sten_L > 0 && S.sten_off[static_cast<size_t>(S.sten_L / 2)] == 0; }
 
+// Every main record but the centre (L/2, the fixed-length kernels' diagonal)
+// is exactly -1.0: the row sums subtract instead of multiplying (bitwise equal).
+int sten_neg1(const Sell& S) {
+    static const bool on = env_flag("PAIRAMG_STEN_NEG1", true);
+    if (!on || S.sten_L <= 0) return 0;
+    for (int k = 0; k < S.sten_L; ++k)
+        if (k != S.sten_L / 2 && S.sten_val[k] != -1.0) return 0;
+    return 1;
+}
+
 StenParam sten_param(const Sell& S) {
     StenParam p{};
     for (int k = 0; k < S.sten_L; ++k) {
@@ -1175,6 +1185,7 @@ StenParam sten_param(const Sell& S) {
         p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
         p.pinv[q] = fast_div() ? 1.0 / p.pdiag[q] : 0.0;
     }
+    p.neg1 = sten_neg1(S);
     return p;
 }
 
@@ -1189,6 +1200,7 @@ StenParamW sten_param_w(const Sell& S) {
         p.pdiag[q] = q < S.npat ? S.hpdiag[q] : 1.0;
         p.pinv[q] = fast_div() ? 1.0 / p.pdiag[q] : 0.0;
     }
+    p.neg1 = sten_neg1(S);
     return p;
 }
 

@@ -29,6 +29,7 @@ struct StenParam {
     uint32_t pmask[256];  // main records absent from the pattern (bit k = record k)
     double pdiag[256];    // l1 diagonal of the pattern (bitwise = l1_diagonal)
     double pinv[256];     // RN(1 / pdiag) for ddiv_recip (0 = divide)
+    int neg1;             // every record but the centre (L/2) holds exactly -1.0
 };
 
 // Boundary rows of a split launch: the faces of an interior rank reach
@@ -41,6 +42,7 @@ struct StenParamW {
     unsigned long long pmask[256];
     double pdiag[256];
     double pinv[256];
+    int neg1;
 };
 
 struct StenArgs {
@@ -95,7 +97,17 @@ __device__ __forceinline__ double sten_row_sum(const StenArgs& a, const PT& p, i
             xv[k] = a.x[c];  // coherent load: this kernel may start before x's producer completes (PDL)
         }
         double sum = 0.0;
-        if (__all_sync(0xffffffffu, m == 0u)) {
+        if (p.neg1) {  // as sten_fold_neg1: -1.0 records subtract (bitwise the same sum)
+            if (__all_sync(0xffffffffu, m == 0u)) {
+#pragma unroll
+                for (int k = 0; k < LL; ++k)
+                    sum = k == LL / 2 ? dadd(sum, dmul(p.val[k], xv[k])) : dsub(sum, xv[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < LL; ++k)
+                    if (!((m >> k) & 1u)) sum = k == LL / 2 ? dadd(sum, dmul(p.val[k], xv[k])) : dsub(sum, xv[k]);
+            }
+        } else if (__all_sync(0xffffffffu, m == 0u)) {
 #pragma unroll
             for (int k = 0; k < LL; ++k) sum = dadd(sum, dmul(p.val[k], xv[k]));
         } else {
@@ -191,8 +203,25 @@ __device__ __forceinline__ void sten_load(const StenArgs& a, const StenParam& p,
     }
 }
 
+// x * -1.0 is exactly -x, so sum + (-1.0 * x) is bitwise sum - x: with
+// p.neg1 (a uniform branch) the off-centre records skip their multiply.
+template <int LL>
+__device__ __forceinline__ double sten_fold_neg1(const StenParam& p, const double (&xv)[LL], uint32_t m) {
+    double sum = 0.0;
+    if (__all_sync(0xffffffffu, m == 0u)) {
+#pragma unroll
+        for (int k = 0; k < LL; ++k) sum = k == LL / 2 ? dadd(sum, dmul(p.val[k], xv[k])) : dsub(sum, xv[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < LL; ++k)
+            if (!((m >> k) & 1u)) sum = k == LL / 2 ? dadd(sum, dmul(p.val[k], xv[k])) : dsub(sum, xv[k]);
+    }
+    return sum;
+}
+
 template <int LL>
 __device__ __forceinline__ double sten_fold(const StenParam& p, const double (&xv)[LL], uint32_t m) {
+    if (p.neg1) return sten_fold_neg1<LL>(p, xv, m);
     double sum = 0.0;
     if (__all_sync(0xffffffffu, m == 0u)) {
 #pragma unroll
