@@ -171,7 +171,7 @@ __device__ __forceinline__ void sten1_block(const StenArgs& a, const PT& p, int 
         a.y[row] = dsub(ri, sum);
     } else {
         const double t = dsub(ri, sum);  // omega = 1 (the paper's setting) multiplies exactly: skip it
-        a.y[row] = dadd(xi, ddiv_recip(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q], p.pinv[q]));
+        a.y[row] = dadd(xi, ddiv_recip(dmul(a.omega, t), p.pdiag[q], p.pinv[q]));  // 1.0 * t == t exactly
     }
 }
 
@@ -245,7 +245,7 @@ __device__ __forceinline__ void sten_store(const StenArgs& a, const StenParam& p
         a.y[row] = dsub(ri, sum);
     } else {
         const double t = dsub(ri, sum);
-        a.y[row] = dadd(xi, ddiv_recip(a.omega == 1.0 ? t : dmul(a.omega, t), p.pdiag[q], p.pinv[q]));
+        a.y[row] = dadd(xi, ddiv_recip(dmul(a.omega, t), p.pdiag[q], p.pinv[q]));  // 1.0 * t == t exactly
     }
 }
 
