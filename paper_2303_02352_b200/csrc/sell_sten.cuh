@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split(StenArgs a
 }
 
 template <int LLA, bool R2, bool BROWS>
-__global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
+__global__ void __launch_bounds__(256, LLA == 7 ? 5 : 2) k_sten_split_dots(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();
     double sa = 0.0, sb = 0.0, sg = 0.0;
     if (static_cast<int>(blockIdx.x) < h.npush) {  // push blocks first (zero partials)
