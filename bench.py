@@ -312,7 +312,7 @@ def bench_ours(args, rank, world, local_rank):
     u.zero_()
     s.solve(b, u)
     s.set_kernel_timing(False)
-    kt = [s.kernel_timing(k) for k in range(6)]
+    kt = [s.kernel_timing(k) for k in range(4)]
     peak, peak_src = measured_peaks()
     li0 = s.level_info(0)
     fmt0 = s.level_storage(0)
@@ -397,7 +397,7 @@ def bench_ours(args, rank, world, local_rank):
                      "classes": {name: {"avg_us": 1e3 * k["ms"] / max(k["launches"], 1), "launches": k["launches"],
                                         "gbs": (k["bytes_per_launch"] / (k["ms"] / max(k["launches"], 1) * 1e-3) / 1e9)
                                         if k["launches"] else None}
-                                 for name, k in zip(["sweep", "residual", "spmv_dots", "fcg_update", "sweep_zero_fused", "sweep_prolong_fused"], kt)}},
+                                 for name, k in zip(["sweep", "residual", "spmv_dots", "fcg_update"], kt)}},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16 * m, "d2h_bytes_per_step": 8 * m,
                 "api": "pairamg_solve (C ABI, pinned host b/u0 in, u out)"},
         "e2e_pipeline_s": pipe,

@@ -11,8 +11,8 @@
  *   pairamg_runtime_create     <- spawn_ranks / RankCtx        (runtime.hpp:71-136)
  *   pairamg_setup              <- setup_hierarchy               (amg.hpp:84-85, amg.cpp:144-295)
  *   pairamg_solve              <- pcg_solve (absent)
- *   pairamg_vcycle             <- vcycle_apply                  (cycle.hpp:31-32, cycle.cpp:126-152)
- *   pairamg_spmv               <- spmv_dist                     (dist.hpp:83-86, dist.cpp:241-312)
+ *   pairamg_vcycle             <- vcycle_apply                  (cycle.hpp:31-32, cycle.cpp:86-112)
+ *   pairamg_spmv               <- spmv_dist                     (dist.hpp:83-86, dist.cpp:128-199)
  *   pairamg_hierarchy_info /
  *   pairamg_level_info         <- Hierarchy::level_sizes/level_nnz/opc, hierarchy_summary
  *                                                               (amg.hpp:49-58, amg.cpp:297-313)
@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PAIRAMG_B200_ABI_VERSION 1
+#define PAIRAMG_B200_ABI_VERSION 2
 
 /* ErrorCode (types.hpp:13-24), shifted by one; 0 = success. */
 typedef enum pairamg_status {
@@ -67,12 +67,47 @@ typedef enum pairamg_status {
     PAIRAMG_INTERNAL = 10
 } pairamg_status;
 
+/* Solve-time storage of a level's rows (B200 extension, no reference
+ * counterpart).  Every format reproduces each entry's column and value
+ * exactly and sums rows in CSR order, so results are bitwise equal; the
+ * format only decides which kernels run and how many bytes they move. */
+typedef enum pairamg_storage {
+    PAIRAMG_STORAGE_AUTO = -1, /* STEN, else PAT (rows > 16 entries), DICT, PAT, CODED, PLAIN */
+    PAIRAMG_STORAGE_PLAIN = 0, /* SELL-32, int32 column + f64 value per entry */
+    PAIRAMG_STORAGE_DICT = 1,  /* one byte per entry into <= 255 (column - row, value) pairs */
+    PAIRAMG_STORAGE_PAT = 2,   /* one byte per row into <= 255 row patterns */
+    PAIRAMG_STORAGE_STEN = 3,  /* one byte per row: subset of one main stencil pattern */
+    PAIRAMG_STORAGE_CODED = 4  /* SELL-32, one 32-bit (column - row, value code) word per entry */
+} pairamg_storage;
+
 /* SetupConfig (amg.hpp:17-23).  Matching ties are broken by the total order
- * key(e) = (w(e), -min(e), -max(e)) (hard part 1). */
+ * key(e) = (w(e), -min(e), -max(e)) (hard part 1); the
+ * reference's sequential Suitor keeps the incumbent on equal weights
+ * (matching.cpp:82), so on coarse steps of odd grids the two may pick
+ * different matchings.  `replay` reproduces any recorded matching exactly. */
 typedef struct pairamg_setup_config {
     int aggregation_exponent; /* s: pairwise steps composed per level (default 3) */
     int64_t coarse_size_target; /* stop when global rows <= this (default 40) */
     int max_levels;             /* default 40 */
+    /* SetupConfig::replay / MatchingTrace (amg.hpp:13-23, amg.cpp:182-197):
+     * replay_steps > 0 skips the matching kernels; pairwise step t takes its
+     * matching from replay_mates[t], the GLOBAL mate of every global row of
+     * that step's fine level (replay_sizes[t] entries, -1 = unmatched), e.g.
+     * the reference's MatchingTrace::steps or pairamg_matching_export.  A
+     * mate outside the rank's owned block is CONTRACT_VIOLATION ("replayed
+     * matching crosses the rank partition"), too few steps is
+     * CONTRACT_VIOLATION ("matching trace exhausted").  Host pointers. */
+    int replay_steps;
+    const int64_t* const* replay_mates;
+    const int64_t* replay_sizes;
+    /* B200 extensions (no reference counterpart): */
+    int storage;             /* pairamg_storage; default PAIRAMG_STORAGE_AUTO.  A forced
+                                format falls back to PLAIN on rows it cannot encode. */
+    int64_t replicate_rows;  /* nranks > 1: coarse levels with <= this many global rows
+                                are also held in full on every rank (default 2500000; 0 = off) */
+    int setup_overlap;       /* nranks > 1: P's halo exchange on the communication stream
+                                while R, w_next and the composed P are built (default 0:
+                                measured no gain) */
 } pairamg_setup_config;
 
 /* CycleConfig (cycle.hpp:7-12). */
@@ -100,6 +135,13 @@ typedef struct pairamg_solve_stats {
     double t_solve_s; /* device time of the solve (CUDA events) */
     double* history;
     int history_cap;
+    /* pairamg_solve (host buffers) only: device time of the b/u0 upload and
+     * of the u download (CUDA events on the solver stream); 0 otherwise. */
+    double t_h2d_s, t_d2h_s;
+    /* cross-rank exchanges of the FCG reduction per iteration (contract: 1;
+     * SPEC.md:477) and halo exchanges per iteration, from CommStats deltas. */
+    int reductions_per_iter;
+    int halo_exchanges_per_iter;
 } pairamg_solve_stats;
 
 /* SetupStats (amg.hpp:40-47) plus the hierarchy summary. */
@@ -170,10 +212,10 @@ pairamg_status pairamg_hierarchy_info(pairamg_solver* s, int* nlevels, double* o
 pairamg_status pairamg_level_info(pairamg_solver* s, int level, int64_t* global_rows,
                                   int64_t* global_nnz, int64_t* row_begin, int64_t* local_rows,
                                   int64_t* local_nnz);
-/* Solve-time storage of level k's owned rows (B200 extension, no reference
- * counterpart): 0 PLAIN SELL-32, 1 DICT, 2 PAT, 3 STEN -- for the interior
- * row set when the level has halo traffic.  All formats give bitwise-equal
- * results; this only reports which kernels run. */
+/* Solve-time storage of level k's owned rows (pairamg_storage: 0 PLAIN,
+ * 1 DICT, 2 PAT, 3 STEN, 4 CODED) -- for the interior row set when the level
+ * has halo traffic.  All formats give bitwise-equal results; this only
+ * reports which kernels run. */
 pairamg_status pairamg_level_storage(pairamg_solver* s, int level, int* format);
 /* Owned rows of A^k: row_ptr (local_rows+1), col (local_nnz, GLOBAL ids,
  * ascending), val; w^k and the l1 diagonal (local_rows).  Any pointer may be NULL. */
@@ -187,6 +229,12 @@ pairamg_status pairamg_prolongator_export(pairamg_solver* s, int level, int64_t*
 pairamg_status pairamg_num_matchings(pairamg_solver* s, int* steps);
 pairamg_status pairamg_matching_export(pairamg_solver* s, int step, int64_t* n, int64_t* mate);
 pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* out);
+/* Hierarchy::warnings (amg.hpp:56, amg.cpp:230-234) plus the cycle-config
+ * warning of validate_cycle_config (cycle.cpp:7-13): *count receives the
+ * number; pairamg_setup_warning copies warning i (NUL-terminated, truncated
+ * to cap bytes) and returns its full length in *len (either may be NULL). */
+pairamg_status pairamg_setup_warnings(pairamg_solver* s, int* count);
+pairamg_status pairamg_setup_warning(pairamg_solver* s, int i, char* buf, size_t cap, size_t* len);
 
 /* ---- matching KAT hook ---- */
 /* suitor_match (matching.cpp:62-100) under the total-order tie rule, run by
@@ -200,8 +248,7 @@ pairamg_status pairamg_match_graph(pairamg_runtime* rt, int64_t n, const int64_t
 /* Per-kernel-class device time accumulated over the last solve (CUDA events
  * around every launch of the class when timing was enabled):
  * class 0 = level-0 smoother sweeps, 1 = level-0 residual, 2 = level-0 outer
- * SpMV+dots, 3 = FCG vector updates, 4 = fused level-0 zero-start sweeps,
- * 5 = fused level-0 prolongation sweeps, 6 + k (k < 16) = level k's own
+ * SpMV+dots, 3 = FCG vector updates, 4 + k (k < 16) = level k's own
  * V-cycle work (two intervals per cycle: entry to restriction, return from
  * level k+1 to exit).  *launches and *ms may be NULL. */
 pairamg_status pairamg_set_kernel_timing(pairamg_solver* s, int enabled);

@@ -14,12 +14,12 @@
  * Global-view emulation of p row blocks.  Every quantity the reference
  * computes per rank is either block-local (matching on the diagonal block,
  * aggregate numbering, P, R, R*C) or partition-independent by construction
- * (spmv_dist sums each row in ascending global column order, dist.cpp:277-300;
- * spgemm_local sums each entry in ascending inner index, csr.cpp:363-429), so
+ * (spmv_dist sums each row in ascending global column order, dist.cpp:164-187;
+ * spgemm_local sums each entry in ascending inner index, csr.cpp:206-272), so
  * one process holding global arrays reproduces the distributed result bit for
- * bit.  The only explicitly per-rank arithmetic is dot_dist (dist.cpp:412-419:
+ * bit.  The only explicitly per-rank arithmetic is dot_dist (dist.cpp:299-306:
  * sequential per-rank partial, then rank-ascending allreduce,
- * runtime.cpp:381-397), which is emulated as such.
+ * runtime.cpp:243-259), which is emulated as such.
  *
  * Floating point: built with -ffp-contract=off (no FMA) to match the
  * reference's Release objects, which contain no FMA.
@@ -128,7 +128,7 @@ static int csr_validate(const csr_t* A) {
     return 0;
 }
 
-/* spmv_local / spmv_dist row loop (csr.cpp:100-117, dist.cpp:277-300):
+/* spmv_local / spmv_dist row loop (csr.cpp:100-117, dist.cpp:164-187):
  * sum = 0.0; sum += a_ij * x_j in CSR (ascending global column) order. */
 static void spmv(const csr_t* A, const double* x, double* y) {
     for (int64_t i = 0; i < A->n; ++i) {
@@ -156,8 +156,8 @@ static void stable_sort_pairs(int64_t* c, double* v, int64_t m) {
 
 /* Merge a stably sorted contribution list: per column the first contribution
  * is assigned and later ones added in encounter order, output ascending --
- * exactly HashAccumulator::add + extract_sorted (csr.cpp:302-329) and
- * merge_row (csr.cpp:343-359). Returns the merged length. */
+ * exactly HashAccumulator::add + extract_sorted (csr.cpp:145-172) and
+ * merge_row (csr.cpp:186-202). Returns the merged length. */
 static int64_t merge_sorted(int64_t* c, double* v, int64_t m) {
     int64_t out = 0, i = 0;
     while (i < m) {
@@ -423,7 +423,7 @@ static void transpose_p(const int64_t* pcol, const double* pval, int64_t nf, int
 }
 
 /* galerkin_product (amg.cpp:110-142): C = A*P by spmm_dist/spgemm_local
- * (dist.cpp:321-410, csr.cpp:363-429) with P one entry per row, then
+ * (dist.cpp:208-297, csr.cpp:206-272) with P one entry per row, then
  * A_c = R*C with R = transpose_block(P) (communication-free). */
 static void galerkin(const csr_t* A, const int64_t* pcol, const double* pval, int64_t nc,
                      csr_t* Ac) {
@@ -682,7 +682,7 @@ static int setup_hierarchy(session_t* s) {
 
 /* ------------------------------------------------------------- cycle --- */
 
-/* l1_jacobi_sweeps (cycle.cpp:77-102). x0 == NULL: zero start. */
+/* l1_jacobi_sweeps (cycle.cpp:37-62). x0 == NULL: zero start. */
 static void jacobi(const level_t* L, const double* r, double* x, int have_x0, int nu, double omega,
                    double* tmp) {
     const int64_t n = L->A.n;
@@ -700,8 +700,8 @@ static void jacobi(const level_t* L, const double* r, double* x, int have_x0, in
     }
 }
 
-/* vcycle_apply (cycle.cpp:126-152) with restrict_to_coarse (cycle.cpp:104-115)
- * and prolongate_add (cycle.cpp:117-124). */
+/* vcycle_apply (cycle.cpp:86-112) with restrict_to_coarse (cycle.cpp:64-75)
+ * and prolongate_add (cycle.cpp:77-84). */
 static void vcycle(const session_t* s, int k, const double* r, double* x) {
     const level_t* L = &s->lv[k];
     const orc_config* c = &s->cfg;
@@ -732,8 +732,8 @@ static void vcycle(const session_t* s, int k, const double* r, double* x) {
     free(tmp);
 }
 
-/* dot_dist (dist.cpp:412-419): per-rank sequential partial, then the
- * rank-ascending allreduce_sum (runtime.cpp:381-397). */
+/* dot_dist (dist.cpp:299-306): per-rank sequential partial, then the
+ * rank-ascending allreduce_sum (runtime.cpp:243-259). */
 static double dot_dist(const session_t* s, const int64_t* starts, const double* x, const double* y) {
     double acc = 0.0;
     for (int r = 0; r < s->cfg.nranks; ++r) {

@@ -9,10 +9,10 @@
 //     x fastest, diagonal 6 (26), off-diagonals -1, b = 1);
 //   * Notay's flexible PCG, PAPER.md:86-115 (Alg. 1) with SPEC.md:474-482,
 //     built only from the reference's own spmv_dist / dot_dist /
-//     vcycle_apply (dist.cpp:241-312, 412-421; cycle.cpp:126-152).
+//     vcycle_apply (dist.cpp:128-199, 412-421; cycle.cpp:86-112).
 // Everything else (setup_hierarchy, matching, Galerkin, V-cycle, halo SpMV)
 // is the unmodified reference code, run as p ranks on p threads by
-// spawn_ranks (runtime.cpp:230-290).  Compiled by oracle/Makefile into
+// spawn_ranks (runtime.cpp:92-152).  Compiled by oracle/Makefile into
 // oracle/_ref/libpairamg_ref.so; never linked into the product.
 #include <chrono>
 #include <cmath>

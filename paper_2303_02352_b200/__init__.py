@@ -35,8 +35,10 @@ EXPORTS = [
     "pairamg_get_setup_stats", "pairamg_set_kernel_timing", "pairamg_kernel_timing", "pairamg_launch_count",
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
     "pairamg_match_graph", "pairamg_mm_open", "pairamg_mm_rows", "pairamg_mm_copy_rows", "pairamg_mm_close",
-    "pairamg_mm_write", "pairamg_spgemm",
+    "pairamg_mm_write", "pairamg_spgemm", "pairamg_setup_warnings", "pairamg_setup_warning",
 ]
+
+STORAGE = {"auto": -1, "plain": 0, "dict": 1, "pat": 2, "sten": 3, "coded": 4}
 
 
 class PairamgError(RuntimeError):
@@ -49,10 +51,31 @@ class PairamgError(RuntimeError):
 
 
 class SetupConfig(C.Structure):  # amg.hpp:17-23
-    _fields_ = [("aggregation_exponent", C.c_int), ("coarse_size_target", C.c_int64), ("max_levels", C.c_int)]
+    """SetupConfig (amg.hpp:17-23).  ``replay`` = MatchingTrace::steps: a list
+    of global mate arrays, one per pairwise step (amg.cpp:182-197).  The B200
+    extensions: ``storage`` ("auto", "sten", "pat", "dict", "coded", "plain"),
+    ``replicate_rows`` and ``setup_overlap`` (include/pairamg_b200.h)."""
 
-    def __init__(self, aggregation_exponent=3, coarse_size_target=40, max_levels=40):
+    _fields_ = [("aggregation_exponent", C.c_int), ("coarse_size_target", C.c_int64), ("max_levels", C.c_int),
+                ("replay_steps", C.c_int), ("replay_mates", C.POINTER(C.POINTER(C.c_int64))),
+                ("replay_sizes", C.POINTER(C.c_int64)), ("storage", C.c_int), ("replicate_rows", C.c_int64),
+                ("setup_overlap", C.c_int)]
+
+    def __init__(self, aggregation_exponent=3, coarse_size_target=40, max_levels=40, replay=None,
+                 storage="auto", replicate_rows=2500000, setup_overlap=False):
         super().__init__(aggregation_exponent, coarse_size_target, max_levels)
+        self.storage = STORAGE[storage] if isinstance(storage, str) else int(storage)
+        self.replicate_rows = replicate_rows
+        self.setup_overlap = 1 if setup_overlap else 0
+        self._replay = None
+        if replay is not None:
+            arrs = [np.ascontiguousarray(m, np.int64) for m in replay]
+            ptrs = (C.POINTER(C.c_int64) * len(arrs))(*[a.ctypes.data_as(C.POINTER(C.c_int64)) for a in arrs])
+            sizes = (C.c_int64 * len(arrs))(*[len(a) for a in arrs])
+            self._replay = (arrs, ptrs, sizes)  # keep the buffers alive
+            self.replay_steps = len(arrs)
+            self.replay_mates = ptrs
+            self.replay_sizes = sizes
 
 
 class CycleConfig(C.Structure):  # cycle.hpp:7-12
@@ -73,7 +96,8 @@ class SolveConfig(C.Structure):
 class _SolveStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_relres", C.c_double),
                 ("rnorm0", C.c_double), ("t_solve_s", C.c_double), ("history", C.POINTER(C.c_double)),
-                ("history_cap", C.c_int)]
+                ("history_cap", C.c_int), ("t_h2d_s", C.c_double), ("t_d2h_s", C.c_double),
+                ("reductions_per_iter", C.c_int), ("halo_exchanges_per_iter", C.c_int)]
 
 
 class _SetupStats(C.Structure):
@@ -90,6 +114,10 @@ class SolveStats:
     rnorm0: float
     t_solve_s: float
     history: np.ndarray
+    t_h2d_s: float = 0.0
+    t_d2h_s: float = 0.0
+    reductions_per_iter: int = 0
+    halo_exchanges_per_iter: int = 0
 
 
 _lib = None
@@ -148,6 +176,8 @@ def lib() -> C.CDLL:
         "pairamg_mm_close": ([vp], st),
         "pairamg_mm_write": ([C.c_char_p, i64, i64, vp, vp, vp], st),
         "pairamg_spgemm": ([vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, C.POINTER(vp), C.POINTER(i64)], st),
+        "pairamg_setup_warnings": ([vp, C.POINTER(C.c_int)], st),
+        "pairamg_setup_warning": ([vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -337,7 +367,8 @@ class Solver:
                 u = np.zeros_like(b)
             _check(lib().pairamg_solve(self.h, _ptr(b), _ptr(u), C.byref(cycle), C.byref(solve_cfg), C.byref(st)))
         return SolveStats(st.iterations, bool(st.converged), st.final_relres, st.rnorm0, st.t_solve_s,
-                          hist[: st.iterations + 1].copy())
+                          hist[: st.iterations + 1].copy(), st.t_h2d_s, st.t_d2h_s, st.reductions_per_iter,
+                          st.halo_exchanges_per_iter)
 
     def vcycle(self, r, cycle: CycleConfig | None = None):
         cycle = cycle or CycleConfig()
@@ -412,6 +443,19 @@ class Solver:
         m = np.empty(n.value, np.int64)
         _check(lib().pairamg_matching_export(self.h, step, C.byref(n), _ptr(m)))
         return m
+
+    def warnings(self) -> list[str]:
+        """Hierarchy::warnings (amg.cpp:230-234) + validate_cycle_config's (cycle.cpp:7-13)."""
+        n = C.c_int()
+        _check(lib().pairamg_setup_warnings(self.h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            ln = C.c_size_t()
+            _check(lib().pairamg_setup_warning(self.h, i, None, 0, C.byref(ln)))
+            buf = C.create_string_buffer(ln.value + 1)
+            _check(lib().pairamg_setup_warning(self.h, i, buf, ln.value + 1, None))
+            out.append(buf.value.decode())
+        return out
 
     def setup_stats(self) -> dict:
         s = _SetupStats()

@@ -15,6 +15,12 @@ struct SetupConfig {  // SetupConfig (amg.hpp:17-23)
     int aggregation_exponent = 3;
     int64_t coarse_size_target = 40;
     int max_levels = 40;
+    // replay (MatchingTrace, amg.hpp:13-23): global mates per pairwise step
+    std::vector<const int64_t*> replay;
+    std::vector<int64_t> replay_sizes;
+    int storage = -1;                  // pairamg_storage (-1 auto)
+    int64_t replicate_rows = 2500000;  // nranks > 1: replicate coarse levels up to this size
+    bool setup_overlap = false;        // nranks > 1: P halo exchange on the comm stream
 };
 
 struct CycleConfig {  // CycleConfig (cycle.hpp:7-12)
@@ -74,7 +80,7 @@ struct Hierarchy {
 };
 
 // Replicate every level whose global size is <= max_rows (nranks > 1).
-void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows);
+void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows, int storage);
 // Padded allgather of per-rank segments (counts[r] elements each) into a
 // contiguous vector on `s` (graph-capturable).
 void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* sendbuf, double* recvbuf,

@@ -58,6 +58,19 @@ pb::SetupConfig setup_cfg(const pairamg_setup_config* c) {
         o.aggregation_exponent = c->aggregation_exponent;
         o.coarse_size_target = c->coarse_size_target;
         o.max_levels = c->max_levels;
+        if (c->replay_steps < 0) pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: replay_steps must be >= 0");
+        if (c->replay_steps > 0 && (!c->replay_mates || !c->replay_sizes))
+            pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: replay_steps > 0 needs replay_mates and replay_sizes");
+        for (int t = 0; t < c->replay_steps; ++t) {
+            o.replay.push_back(c->replay_mates[t]);
+            o.replay_sizes.push_back(c->replay_sizes[t]);
+        }
+        if (c->storage < PAIRAMG_STORAGE_AUTO || c->storage > PAIRAMG_STORAGE_CODED)
+            pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: unknown storage format " + std::to_string(c->storage));
+        o.storage = c->storage;
+        if (c->replicate_rows < 0) pb::fail(PAIRAMG_INVALID_ARGUMENT, "setup: replicate_rows must be >= 0");
+        o.replicate_rows = c->replicate_rows;
+        o.setup_overlap = c->setup_overlap != 0;
     }
     return o;
 }
@@ -166,9 +179,16 @@ __global__ void k_poisson_fill(int stencil, int64_t nx, int64_t ny, int64_t nz, 
 extern "C" {
 
 void pairamg_default_setup_config(pairamg_setup_config* c) {
+    std::memset(c, 0, sizeof *c);
     c->aggregation_exponent = 3;
     c->coarse_size_target = 40;
     c->max_levels = 40;
+    c->replay_steps = 0;
+    c->replay_mates = nullptr;
+    c->replay_sizes = nullptr;
+    c->storage = PAIRAMG_STORAGE_AUTO;
+    c->replicate_rows = 2500000;
+    c->setup_overlap = 0;
 }
 
 void pairamg_default_cycle_config(pairamg_cycle_config* c) {
@@ -319,16 +339,31 @@ pairamg_status pairamg_solve(pairamg_solver* s, const double* b, double* u, cons
         cudaStream_t st = sv.rt.stream();
         const int64_t n = sv.h.levels[0]->A.n;
         pb::DBuf<double> db(static_cast<size_t>(n), st), du(static_cast<size_t>(n), st);
+        // the copies are timed on the solver stream (events), apart from the solve
+        cudaEvent_t ev[4];
+        for (auto& e : ev) PB_CUDA(cudaEventCreate(&e));
+        PB_CUDA(cudaEventRecord(ev[0], st));
         if (n) {
             PB_CUDA(cudaMemcpyAsync(db.get(), b, 8 * n, cudaMemcpyHostToDevice, st));
             PB_CUDA(cudaMemcpyAsync(du.get(), u, 8 * n, cudaMemcpyHostToDevice, st));
         }
+        PB_CUDA(cudaEventRecord(ev[1], st));
         pairamg_solve_config sc;
         pairamg_default_solve_config(&sc);
         if (scfg) sc = *scfg;
         sv.solve(db.get(), du.get(), cycle_cfg(ccfg), sc.rtol, sc.max_iters, sc.precflag != 0, stats);
+        PB_CUDA(cudaEventRecord(ev[2], st));
         if (n) PB_CUDA(cudaMemcpyAsync(u, du.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+        PB_CUDA(cudaEventRecord(ev[3], st));
         PB_CUDA(cudaStreamSynchronize(st));
+        float h2d = 0.f, d2h = 0.f;
+        PB_CUDA(cudaEventElapsedTime(&h2d, ev[0], ev[1]));
+        PB_CUDA(cudaEventElapsedTime(&d2h, ev[2], ev[3]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (stats) {
+            stats->t_h2d_s = h2d * 1e-3;
+            stats->t_d2h_s = d2h * 1e-3;
+        }
     });
 }
 
@@ -481,6 +516,29 @@ pairamg_status pairamg_get_setup_stats(pairamg_solver* s, pairamg_setup_stats* o
         out->rc_messages = st.rc_messages;
         out->levels = sv.h.nl();
         out->opc = sv.h.opc;
+    });
+}
+
+pairamg_status pairamg_setup_warnings(pairamg_solver* s, int* count) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        if (!count) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null count");
+        *count = static_cast<int>(sv.warnings().size());
+    });
+}
+
+pairamg_status pairamg_setup_warning(pairamg_solver* s, int i, char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        pb::Solver& sv = S(s);
+        const std::vector<std::string> w = sv.warnings();
+        if (i < 0 || i >= static_cast<int>(w.size())) pb::fail(PAIRAMG_INVALID_ARGUMENT, "warning index out of range");
+        const std::string& m = w[static_cast<size_t>(i)];
+        if (len) *len = m.size();
+        if (buf && cap) {
+            const size_t k = std::min(cap - 1, m.size());
+            std::memcpy(buf, m.data(), k);
+            buf[k] = 0;
+        }
     });
 }
 

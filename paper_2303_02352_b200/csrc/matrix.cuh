@@ -5,7 +5,7 @@
 //                ([0,n) owned, [n, n+n_halo) halo slots), f64 values.  Each
 //                row keeps the reference's column order (ascending GLOBAL id,
 //                csr.hpp:10-11), so every per-row sum runs in the reference
-//                order (dist.cpp:277-300).
+//                order (dist.cpp:164-187).
 //   HaloPlan   : HaloPlan (dist.hpp:50-65): sorted global ids of the halo
 //                slots (recv_ids), per-peer receive ranges, per-peer send
 //                lists of owned local ids, a packed send buffer.
@@ -16,7 +16,7 @@
 //                contiguous 256 B / 128 B transaction and the lane's sum runs
 //                over its row in CSR order, bitwise equal to spmv_local.
 //                Interior and boundary rows get separate Sells so halo
-//                exchange overlaps interior rows (dist.cpp:303-311).
+//                exchange overlaps interior rows (dist.cpp:190-198).
 #pragma once
 
 #include <vector>
@@ -54,18 +54,6 @@ struct DevMatrix {
     int64_t n_boundary = 0;
 };
 
-// Shared-memory window plan of a DICT Sell (sell_win.cuh): the distinct
-// column offsets clustered into <= kWinMax contiguous windows per tile.
-constexpr int kWinMax = 12;
-struct SellWin {
-    bool ok = false;
-    int T = 0, nwin = 0, ntiles = 0, grid = 0;
-    int lo[kWinMax] = {}, len[kWinMax] = {}, soff[kWinMax] = {};
-    int r_soff = 0, d_soff = 0, q_soff = 0, c_soff = 0, stage = 0, al_r = 0, base0 = 0;
-    size_t smem = 0;                // dynamic shared memory per CTA (2 stages)
-    std::vector<ulonglong2> rec;   // 256 records {value bits, shared-memory base}
-};
-
 struct Sell {
     // PAT  : one byte per ROW naming its row pattern (the row's full sequence
     //        of (column - row, value) entries; <= 255 distinct patterns); the
@@ -88,9 +76,6 @@ struct Sell {
     DBuf<ulonglong2> dict;    // DICT: 256 records {value bits, column - row}; [255] = pad {0, 0}
     std::vector<ulonglong2> hdict;  // DICT: host copy, passed to the kernels as a __grid_constant__ parameter
     int ndict = 0;
-    DBuf<uint8_t> dcode;            // DICT: l1 diagonal code per SELL row (empty = read the l1 array)
-    std::vector<double> hdiag;      // DICT: the distinct l1 values, passed with the dictionary
-    SellWin win;                    // DICT: shared-memory window plan (contiguous row sets)
     DBuf<uint8_t> pid;        // PAT: pattern id per row (indexed by row id)
     DBuf<ulonglong2> ptab;    // PAT: pattern records {value bits, column - row}
     DBuf<int2> pmeta;         // PAT: {first record, length} per pattern
@@ -111,7 +96,7 @@ struct Sell {
 };
 
 // Operators of the SELL kernels (sell.cu)
-enum SellOp { kSpmv = 0, kJacobi = 1, kResid = 2, kJacobiZero = 3, kJacobiProl = 4 };
+enum SellOp { kSpmv = 0, kJacobi = 1, kResid = 2 };
 
 struct SellOpArgs {
     int op = kSpmv;
@@ -120,16 +105,13 @@ struct SellOpArgs {
     const double* r = nullptr;  // right-hand side
     const double* d = nullptr;  // l1 diagonal
     double omega = 1.0;
-    const int32_t* pcol = nullptr;  // kJacobiProl: prolongator of the coarser level
-    const double* pval = nullptr;
-    const double* e = nullptr;      // kJacobiProl: coarse correction
     int max_grid = 0;               // STEN: cap on CTAs (grid-stride), 0 = one CTA per row block
 };
 
 // ---- sparse.cu ----
 // Global-column CSR (int64 row_ptr / col, device) of the owned rows ->
 // DevMatrix with local columns and a halo plan (build_rows_to_receive +
-// exchange_requests + build_spmv_plan, dist.cpp:158-233).  Takes ownership
+// exchange_requests + build_spmv_plan, dist.cpp:45-120).  Takes ownership
 // of the buffers.
 void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gcol,
               DBuf<double>&& val, int64_t nnz);
@@ -141,13 +123,13 @@ void global_columns(const DevMatrix& M, int64_t* d_out, cudaStream_t s);
 // PAT is tried first (needs the level's l1 diagonal to verify the per-pattern
 // diagonal bitwise), then DICT, then PLAIN.
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& out, cudaStream_t s,
-                bool allow_dict = true, const double* l1 = nullptr);
+                int storage = -1, const double* l1 = nullptr);
 // One byte per value into <= 256 distinct values (exact bits); false (and
 // nothing built) when there are more.
 bool build_value_codes(const double* v, int64_t n, DBuf<uint8_t>& code, std::vector<double>& table, cudaStream_t s);
 double sell_bytes(const Sell& S);               // stored matrix bytes of the format
 double sell_op_bytes(const Sell& S, int op);    // algorithmic bytes of one launch (op, or -1 = spmv+dots)
-// l1_diagonal_dist (cycle.cpp:55-75); throws singular_smoother.
+// l1_diagonal_dist (cycle.cpp:15-35); throws singular_smoother.
 void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s);
 // x_halo[h] <- owner's x for every halo slot (pack, NCCL send/recv). On `s`.
 void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_halo, cudaStream_t s);

@@ -176,7 +176,7 @@ int p2p_prio() {
     static int prio = [] {
         int lo = 0, hi = 0;
         PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        return env_flag("PAIRAMG_P2P_PRIO", true) ? hi : lo;
+        return hi;
     }();
     return prio;
 }
@@ -218,7 +218,7 @@ HaloSrc p2p_halo_src(const HaloPlan& H, P2PHalo& P) {
     hs.staging = P.staging;
     hs.nhalo = H.n_halo;
     hs.ctr = P.ctr.get();
-    if (env_flag("PAIRAMG_FUSED_PUSH", true) && H.send_peers.size() <= 8) {
+    if (H.send_peers.size() <= 8) {
         hs.fused = true;
         hs.npeers = static_cast<int>(H.send_peers.size());
         for (int i = 0; i <= hs.npeers; ++i) hs.off[i] = H.send_off[static_cast<size_t>(i)];

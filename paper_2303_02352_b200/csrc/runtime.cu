@@ -28,7 +28,7 @@ Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
         static_assert(sizeof(uid.internal) == 128, "NCCL unique id size");
         std::memcpy(uid.internal, id, 128);
         PB_NCCL(ncclCommInitRank(&comm_, nranks, uid, rank));
-        if (env_flag("PAIRAMG_NCCL_WARMUP", true)) warmup();
+        warmup();
     }
 }
 
@@ -91,7 +91,7 @@ int64_t Runtime::allreduce_sum_i64(int64_t x) {
     if (nranks_ == 1) return x;
     stats_.allreduces += 1;
     int64_t acc = 0;
-    for (int64_t v : allgather_i64(x)) acc += v;  // rank-ascending (runtime.cpp:410-416)
+    for (int64_t v : allgather_i64(x)) acc += v;  // rank-ascending (runtime.cpp:265-280)
     stats_.allgathers -= 1;
     return acc;
 }

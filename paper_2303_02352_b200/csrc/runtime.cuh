@@ -7,7 +7,7 @@
 //   alltoallv                 -> counts by ncclAllGather, payload by grouped send/recv
 //   allreduce_sum             -> ncclAllGather + rank-ascending sum, which keeps the
 //                                reference's deterministic cross-rank order
-//                                (runtime.cpp:388-396)
+//                                (runtime.cpp:250-258)
 // CommStats (runtime.hpp:42-54) is kept as instrumentation.
 #pragma once
 

@@ -19,16 +19,10 @@
 // Operators (one warp per slice, one lane per row, CSR-order sums with
 // separately rounded multiply/add; the row's own operands are loaded before
 // the gather chain so their latency overlaps it):
-//   kSpmv        y = A x                                  (spmv_dist, dist.cpp:277-300)
-//   kJacobi      y = x + (omega*(r - A x))/d              (cycle.cpp:96-100)
-//   kResid       y = r - A x                              (cycle.cpp:141-143)
-//   kJacobiZero  zero-start sweep (cycle.cpp:89-93) fused into the next sweep,
-//                x1 = (omega*r)/d recomputed per gathered column
-//   kJacobiProl  prolongate_add (cycle.cpp:117-124) fused into the first post-sweep
+//   kSpmv        y = A x                                  (spmv_dist, dist.cpp:164-187)
+//   kJacobi      y = x + (omega*(r - A x))/d              (cycle.cpp:56-60)
+//   kResid       y = r - A x                              (cycle.cpp:101-103)
 //   spmv+dots    v = A w with the FCG dot triple (w.r, w.v, w.q) (Alg. 1 l.10-13)
-// The two fused operators trade stored bytes for per-entry recomputation; on
-// B200 they measured slower than the separate kernels and are
-// off by default (PAIRAMG_FUSE=1 enables them).
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -51,11 +45,8 @@ constexpr int kTableCap = 1024;
 constexpr ull kEmptyLo = 0x8000000000000000ULL;
 
 // STEN sweeps divide by the pattern's l1 diagonal through ddiv_recip
-// (common.cuh) with a host-computed reciprocal; PAIRAMG_FAST_DIV=0 divides.
-bool fast_div() {
-    static const bool on = env_flag("PAIRAMG_FAST_DIV", true);
-    return on;
-}
+// (common.cuh) with a host-computed reciprocal (bitwise the IEEE quotient).
+constexpr bool fast_div() { return true; }
 
 struct SellArgs {
     const int64_t* soff;  // PLAIN
@@ -72,18 +63,12 @@ struct SellArgs {
     const double* r;
     const double* d;
     double omega;
-    const int32_t* pcol;
-    const double* pval;
-    const double* e;
     const double* q;
     double* partials;
-    const uint8_t* dcode;  // DICT: l1 diagonal code per SELL row (DictParam::dg), or null
 };
 
 template <int OP>
 __device__ __forceinline__ double xval(const SellArgs& a, int c) {
-    if (OP == kJacobiZero) return ddiv(dmul(a.omega, __ldg(a.r + c)), __ldg(a.d + c));
-    if (OP == kJacobiProl) return dadd(__ldg(a.x + c), dmul(__ldg(a.pval + c), __ldg(a.e + __ldg(a.pcol + c))));
     return __ldg(a.x + c);
 }
 
@@ -123,7 +108,6 @@ constexpr int kFPlain = 0, kFDict = 1, kFCoded = 2;
 template <int F>
 struct DictParam {
     ulonglong2 e[256];
-    double dg[256];  // distinct l1 diagonal values (when SellArgs::dcode is set)
 };
 template <>
 struct DictParam<kFPlain> {
@@ -218,12 +202,9 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
     // own-row operands first: their latency overlaps the gather chain
     double xi = 0.0, ri = 0.0, di = 1.0;
     if (valid) {
-        if (OP == kJacobi || OP == kJacobiZero || OP == kJacobiProl) {
+        if (OP == kJacobi) {
             ri = a.r[row];
-            if constexpr (F != kFPlain)
-                di = a.dcode ? dp.dg[a.dcode[sr]] : a.d[row];
-            else
-                di = a.d[row];
+            di = a.d[row];
         }
         if (OP == kResid) ri = a.r[row];
         if (OP == kJacobi) xi = a.x[row];
@@ -235,7 +216,6 @@ __global__ void __launch_bounds__(kThreads) k_sell(SellArgs a, const __grid_cons
     } else if (OP == kResid) {
         a.y[row] = dsub(ri, sum);
     } else {
-        if (OP != kJacobi) xi = xval<OP>(a, row);
         a.y[row] = dadd(xi, ddiv(dmul(a.omega, dsub(ri, sum)), di));
     }
 }
@@ -285,9 +265,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_sell_spmv_dots(SellArgs a, cons
     }
 }
 
-#include "sell_win.cuh"
 #include "sell_sten.cuh"
-#include "sell_stenwin.cuh"
 
 // ------------------------------------------------------------------ PAT ---
 //
@@ -649,30 +627,6 @@ __global__ void k_sell_fill_dict(const int64_t* __restrict__ rp, const int32_t* 
     }
 }
 
-// l1 diagonal codes: key (0, value bits) in the same open-addressing table.
-__global__ void k_diag_insert(const double* __restrict__ l1, const int32_t* __restrict__ rows, int64_t row0,
-                              int64_t nrows, ull* table, unsigned* count, int* overflow) {
-    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (sr >= nrows || *reinterpret_cast<volatile int*>(overflow)) return;
-    const int64_t row = rows ? rows[sr] : row0 + sr;
-    table_find(table, 0, static_cast<ull>(__double_as_longlong(l1[row])), true, count, overflow);
-}
-
-__global__ void k_diag_fill(const double* __restrict__ l1, const int32_t* __restrict__ rows, int64_t row0,
-                            int64_t nrows, ull* table, const int* __restrict__ slot_code, uint8_t* __restrict__ dcode,
-                            int* bad) {
-    const int64_t sr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (sr >= nrows) return;
-    const int64_t row = rows ? rows[sr] : row0 + sr;
-    const int slot = table_find(table, 0, static_cast<ull>(__double_as_longlong(l1[row])), false, nullptr, nullptr);
-    const int c = slot < 0 ? -1 : slot_code[slot];
-    if (c < 0) {
-        atomicExch(bad, 1);
-        return;
-    }
-    dcode[sr] = static_cast<uint8_t>(c);
-}
-
 // Generic value codes (transfer operators): key (0, value bits).
 __global__ void k_val_insert(const double* __restrict__ v, int64_t n, ull* table, unsigned* count, int* overflow) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -699,167 +653,6 @@ void cub_call(F&& f, cudaStream_t s) {
     PB_CUDA(f(nullptr, bytes));
     DBuf<uint8_t> tmp(bytes ? bytes : 1, s);
     PB_CUDA(f(tmp.get(), bytes));
-}
-
-// Window plan (sell_win.cuh) from the dictionary's column offsets.
-void plan_windows(Sell& S, const std::vector<int32_t>& dcol, const std::vector<double>& dval) {
-    SellWin& P = S.win;
-    P = SellWin();
-    std::vector<int64_t> offs(dcol.begin(), dcol.end());
-    offs.push_back(0);  // pads read the row's own x
-    std::sort(offs.begin(), offs.end());
-    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
-    constexpr int64_t kWinGap = 8;
-    std::vector<std::pair<int64_t, int64_t>> win;  // [lo, hi]
-    for (int64_t o : offs) {
-        if (!win.empty() && o - win.back().second <= kWinGap)
-            win.back().second = o;
-        else
-            win.push_back({o, o});
-    }
-    if (win.size() > static_cast<size_t>(kWinMax)) return;
-    const int T = std::max(64, env_int("PAIRAMG_WIN_T", 512) / 64 * 64);
-    P.T = T;
-    P.nwin = static_cast<int>(win.size());
-    int off = 0;
-    std::vector<int> al(win.size());
-    for (size_t k = 0; k < win.size(); ++k) {
-        const int64_t lo = win[k].first, span = win[k].second - win[k].first;
-        al[k] = static_cast<int>((S.row0 + lo) & 1);
-        P.lo[k] = static_cast<int>(lo);
-        P.len[k] = static_cast<int>((al[k] + T + span + 1) & ~int64_t(1));
-        P.soff[k] = off;
-        off += P.len[k];
-    }
-    P.al_r = static_cast<int>(S.row0 & 1);
-    P.r_soff = off;
-    off += T + 2;
-    P.d_soff = off;
-    off += T + 2;
-    P.q_soff = off;
-    off += T + 2;
-    P.c_soff = off;
-    off += T * S.words / 2;
-    P.stage = off;
-    P.smem = static_cast<size_t>(2) * off * 8;
-    if (P.smem > static_cast<size_t>(kWinSmemCap)) return;
-    auto base_of = [&](int64_t o) {
-        for (size_t k = 0; k < win.size(); ++k)
-            if (o >= win[k].first && o <= win[k].second)
-                return P.soff[k] + al[k] + static_cast<int>(o - win[k].first);
-        return -1;
-    };
-    P.base0 = base_of(0);
-    P.rec.assign(256, make_ulonglong2(0ULL, static_cast<ull>(P.base0)));
-    for (size_t c = 0; c < dcol.size(); ++c) {
-        ull vb;
-        std::memcpy(&vb, &dval[c], 8);
-        P.rec[c] = make_ulonglong2(vb, static_cast<ull>(base_of(dcol[c])));
-    }
-    P.ntiles = static_cast<int>((S.nslices * 32 + T - 1) / T);
-    int per_sm = 0;
-    const void* fns[] = {reinterpret_cast<const void*>(&k_win<kSpmv>), reinterpret_cast<const void*>(&k_win<kJacobi>),
-                         reinterpret_cast<const void*>(&k_win<kResid>), reinterpret_cast<const void*>(&k_win<-1>)};
-    for (const void* f : fns) {
-        // one ceiling for every Sell (the attribute is per function, last write wins)
-        PB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemCap));
-        int nb = 0;
-        PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kWinThreads, P.smem));
-        per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
-    }
-    if (per_sm < 1) return;
-    P.grid = std::min(P.ntiles, kSmCount * per_sm);
-    P.ok = true;
-}
-
-WinArgs win_args_of(const Sell& S) {
-    const SellWin& P = S.win;
-    WinArgs a{};
-    a.code = S.code.get();
-    a.words = S.words;
-    a.row0 = static_cast<int>(S.row0);
-    a.nrows = static_cast<int>(S.nrows);
-    a.nslices = static_cast<int>(S.nslices);
-    a.ntiles = P.ntiles;
-    a.T = P.T;
-    a.xlen = S.xlen;
-    a.nwin = P.nwin;
-    for (int k = 0; k < kWinMax; ++k) {
-        a.lo[k] = P.lo[k];
-        a.len[k] = P.len[k];
-        a.soff[k] = P.soff[k];
-    }
-    a.r_soff = P.r_soff;
-    a.d_soff = P.d_soff;
-    a.q_soff = P.q_soff;
-    a.c_soff = P.c_soff;
-    a.stage = P.stage;
-    a.al_r = P.al_r;
-    a.base0 = P.base0;
-    return a;
-}
-
-DictParam<kFDict> win_param(const Sell& S) {
-    DictParam<kFDict> dp;
-    for (int i = 0; i < 256; ++i) {
-        dp.e[i] = S.win.rec[i];
-        dp.dg[i] = 1.0;
-    }
-    return dp;
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-bool use_win(const Sell& S, const SellOpArgs& o) {
-    if (!S.win.ok || S.format != Sell::kDict) return false;
-    if (o.op != kSpmv && o.op != kJacobi && o.op != kResid) return false;
-    return aligned16(o.x) && (o.op == kSpmv || aligned16(o.r)) && (o.op != kJacobi || aligned16(o.d));
-}
-
-// Replace the 8-byte l1 diagonal stream of a DICT Sell by a 1-byte code per
-// row into <= 256 distinct values (exact bits) passed with the dictionary.
-void try_diag_codes(const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
-    const int32_t* rl = S.rows.empty() ? nullptr : rows;
-    DBuf<ull> table(2 * kTableCap, s);
-    DBuf<unsigned> cnt(1, s);
-    DBuf<int> flags(2, s);
-    cnt.zero(s);
-    flags.zero(s);
-    k_table_init<<<kTableCap / 256, 256, 0, s>>>(table.get());
-    k_diag_insert<<<blocks_for(S.nrows, 256), 256, 0, s>>>(l1, rl, S.row0, S.nrows, table.get(), cnt.get(),
-                                                            flags.get());
-    PB_CHECK_LAUNCH();
-    int over = 0;
-    std::vector<ull> h(2 * kTableCap);
-    PB_CUDA(cudaMemcpyAsync(&over, flags.get(), 4, cudaMemcpyDeviceToHost, s));
-    PB_CUDA(cudaMemcpyAsync(h.data(), table.get(), 16 * kTableCap, cudaMemcpyDeviceToHost, s));
-    PB_CUDA(cudaStreamSynchronize(s));
-    if (over) return;
-    std::vector<std::pair<ull, int>> vals;  // (value bits, slot), ascending -> deterministic codes
-    for (int i = 0; i < kTableCap; ++i)
-        if (!(h[2 * i] == kEmptyLo && h[2 * i + 1] == 0)) vals.push_back({h[2 * i + 1], i});
-    if (vals.empty() || vals.size() > 256) return;
-    std::sort(vals.begin(), vals.end());
-    std::vector<int> slot_code(kTableCap, -1);
-    S.hdiag.assign(256, 1.0);
-    for (size_t c = 0; c < vals.size(); ++c) {
-        slot_code[vals[c].second] = static_cast<int>(c);
-        std::memcpy(&S.hdiag[c], &vals[c].first, 8);
-    }
-    DBuf<int> dsc(kTableCap, s);
-    PB_CUDA(cudaMemcpyAsync(dsc.get(), slot_code.data(), 4 * kTableCap, cudaMemcpyHostToDevice, s));
-    S.dcode.alloc(static_cast<size_t>(S.nslices * 32), s);
-    PB_CUDA(cudaMemsetAsync(S.dcode.get(), 0, S.nslices * 32, s));
-    k_diag_fill<<<blocks_for(S.nrows, 256), 256, 0, s>>>(l1, rl, S.row0, S.nrows, table.get(), dsc.get(),
-                                                          S.dcode.get(), flags.get() + 1);
-    PB_CHECK_LAUNCH();
-    int bad = 0;
-    PB_CUDA(cudaMemcpyAsync(&bad, flags.get() + 1, 4, cudaMemcpyDeviceToHost, s));
-    PB_CUDA(cudaStreamSynchronize(s));
-    if (bad) {
-        S.dcode.reset();
-        S.hdiag.clear();
-    }
 }
 
 bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, const double* l1, cudaStream_t s) {
@@ -924,8 +717,6 @@ bool try_dict(const DevMatrix& M, const int32_t* rows, Sell& S, const double* l1
     PB_CUDA(cudaStreamSynchronize(s));
     if (bad) fail(PAIRAMG_INTERNAL, "sell: dictionary encoding lost an entry");
     S.format = Sell::kDict;
-    if (l1 && env_flag("PAIRAMG_DIAG_CODE", false)) try_diag_codes(rows, S, l1, s);
-    if (S.rows.empty() && env_flag("PAIRAMG_WIN", false)) plan_windows(S, dcol, dval);
     return true;
 }
 
@@ -1086,7 +877,7 @@ bool try_pattern(const DevMatrix& M, const int32_t* rows, Sell& S, const double*
             PB_CUDA(cudaStreamSynchronize(s));
         }
         meta.push_back(make_int2(static_cast<int>(rec.size()), static_cast<int>(len)));
-        // l1 diagonal of the pattern in CSR order (cycle.cpp:60-67): a_ii + sum |a_ij|
+        // l1 diagonal of the pattern in CSR order (cycle.cpp:20-27): a_ii + sum |a_ij|
         double acc = 0.0;
         for (int64_t k = 0; k < len; ++k) {
             const int64_t delta = static_cast<int64_t>(c[k]) - row;
@@ -1156,7 +947,7 @@ StenArgs sten_args_of(const Sell& S, int block_rows = 256) {
     a.safe_lo = static_cast<int>(lo);
     a.safe_hi = static_cast<int>(hi);
     a.nblk = static_cast<int>((S.nrows + block_rows - 1) / block_rows);
-    a.pf_blocks = env_int("PAIRAMG_PF_BLOCKS", 16 * kSmCount) * 256 / block_rows;
+    a.pf_blocks = 16 * kSmCount * 256 / block_rows;
     a.offmax = S.sten_offmax;
     return a;
 }
@@ -1167,8 +958,7 @@ bool sten_center(const Sell& S) { return S.sten_L > 0 && S.sten_off[static_cast<
 // Every main record but the centre (L/2, the fixed-length kernels' diagonal)
 // is exactly -1.0: the row sums subtract instead of multiplying (bitwise equal).
 int sten_neg1(const Sell& S) {
-    static const bool on = env_flag("PAIRAMG_STEN_NEG1", true);
-    if (!on || S.sten_L <= 0) return 0;
+    if (S.sten_L <= 0) return 0;
     for (int k = 0; k < S.sten_L; ++k)
         if (k != S.sten_L / 2 && S.sten_val[k] != -1.0) return 0;
     return 1;
@@ -1204,113 +994,11 @@ StenParamW sten_param_w(const Sell& S) {
     return p;
 }
 
-// Shared-memory window plan of a contiguous STEN row set (k_stenwin):
-// offsets closer than T/2 share a window.  Stored in S.win (rec[k].y = the
-// shared-memory base of main record k).
-constexpr int kStenWinT = 512;
-constexpr int kStenWinSmemCap = 96 * 1024;
-
-void plan_sten_windows(Sell& S) {
-    SellWin& P = S.win;
-    P = SellWin();
-    if (S.format != Sell::kSten || !S.rows.empty() || S.nrows == 0 || !sten_center(S) ||
-        (S.sten_L != 7 && S.sten_L != 27) || !env_flag("PAIRAMG_STEN_WIN", false))
-        return;
-    const int T = kStenWinT;
-    std::vector<int64_t> offs(S.sten_off.begin(), S.sten_off.end());
-    std::sort(offs.begin(), offs.end());
-    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
-    std::vector<std::pair<int64_t, int64_t>> win;
-    for (int64_t o : offs) {
-        if (!win.empty() && o - win.back().second <= T / 2)
-            win.back().second = o;
-        else
-            win.push_back({o, o});
-    }
-    if (win.size() > static_cast<size_t>(kWinMax)) return;
-    P.T = T;
-    P.nwin = static_cast<int>(win.size());
-    int off = 0;
-    std::vector<int> al(win.size());
-    for (size_t k = 0; k < win.size(); ++k) {
-        const int64_t lo = win[k].first, span = win[k].second - win[k].first;
-        al[k] = static_cast<int>((S.row0 + lo) & 1);
-        P.lo[k] = static_cast<int>(lo);
-        P.len[k] = static_cast<int>((al[k] + T + span + 1) & ~int64_t(1));
-        P.soff[k] = off;
-        off += P.len[k];
-    }
-    P.al_r = static_cast<int>(S.row0 & 1);
-    P.r_soff = off;
-    off += T + 2;
-    P.stage = off;
-    P.smem = static_cast<size_t>(2) * off * 8;
-    if (P.smem > static_cast<size_t>(kStenWinSmemCap)) return;
-    P.rec.assign(static_cast<size_t>(S.sten_L), make_ulonglong2(0ULL, 0ULL));
-    for (int k = 0; k < S.sten_L; ++k) {
-        const int64_t o = S.sten_off[static_cast<size_t>(k)];
-        for (size_t w = 0; w < win.size(); ++w)
-            if (o >= win[w].first && o <= win[w].second)
-                P.rec[static_cast<size_t>(k)].y = static_cast<ull>(P.soff[w] + al[w] + (o - win[w].first));
-    }
-    P.ntiles = static_cast<int>((S.nrows + T - 1) / T);
-    int per_sm = 0;
-    const void* fns[] = {reinterpret_cast<const void*>(&k_stenwin<kSpmv, 7>),
-                         reinterpret_cast<const void*>(&k_stenwin<kJacobi, 7>),
-                         reinterpret_cast<const void*>(&k_stenwin<kResid, 7>),
-                         reinterpret_cast<const void*>(&k_stenwin<kSpmv, 27>),
-                         reinterpret_cast<const void*>(&k_stenwin<kJacobi, 27>),
-                         reinterpret_cast<const void*>(&k_stenwin<kResid, 27>)};
-    for (const void* f : fns) {
-        PB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStenWinSmemCap));
-        int nb = 0;
-        PB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 256, P.smem));
-        per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
-    }
-    if (per_sm < 1) return;
-    P.grid = std::min(P.ntiles, kSmCount * per_sm);
-    P.ok = true;
-}
-
-template <int OP>
-bool launch_stenwin(const Sell& S, const StenArgs& a0, cudaStream_t s) {
-    const SellWin& P = S.win;
-    if (!P.ok || S.format != Sell::kSten) return false;
-    StenWinArgs a{};
-    a.row0 = static_cast<int>(S.row0);
-    a.nrows = static_cast<int>(S.nrows);
-    a.ntiles = P.ntiles;
-    a.T = P.T;
-    a.xlen = S.xlen;
-    a.nwin = P.nwin;
-    for (int k = 0; k < P.nwin; ++k) {
-        a.lo[k] = P.lo[k];
-        a.len[k] = P.len[k];
-        a.soff[k] = P.soff[k];
-    }
-    a.r_soff = P.r_soff;
-    a.stage = P.stage;
-    a.al_r = P.al_r;
-    for (int k = 0; k < S.sten_L; ++k) a.base[k] = static_cast<int>(P.rec[static_cast<size_t>(k)].y);
-    a.pid = S.pid.get();
-    a.x = a0.x;
-    a.y = a0.y;
-    a.r = a0.r;
-    a.omega = a0.omega;
-    const StenParam p = sten_param(S);
-    if (S.sten_L == 7)
-        launch_k<2>(k_stenwin<OP, 7>, P.grid, 256, P.smem, s, a, p);
-    else
-        launch_k<2>(k_stenwin<OP, 27>, P.grid, 256, P.smem, s, a, p);
-    return true;
-}
-
 // Two rows per thread for the 7-record main pattern (k_sten2): +10% bandwidth.
 // 27 records: only the SpMV+dots kernel gains (122 vs 132 us; sweeps lose).
 bool sten_rpt2(const Sell& S, bool dots = false) {
-    if (!sten_center(S) || S.nrows < env_int("PAIRAMG_STEN_RPT_MIN_ROWS", 0)) return false;
-    if (S.sten_L == 7) return env_int("PAIRAMG_STEN_RPT", 2) == 2;
-    return S.sten_L == 27 && env_int("PAIRAMG_STEN_RPT27", dots ? 2 : 1) == 2;
+    if (!sten_center(S)) return false;
+    return S.sten_L == 7 || (S.sten_L == 27 && dots);
 }
 
 inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nblk; }
@@ -1318,7 +1006,6 @@ inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nb
 // cap > 0: at most `cap` CTAs, grid-striding over the logical blocks.
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
-    if (!ROWS && cap == 0 && launch_stenwin<OP>(S, a0, s)) return;
     const StenParam p = sten_param(S);
     if (sten_rpt2(S)) {
         StenArgs a = sten_args_of(S, 512);
@@ -1400,7 +1087,6 @@ SellArgs args_of(const Sell& S) {
     a.rows = S.rows.empty() ? nullptr : S.rows.get();
     a.row0 = static_cast<int>(S.row0);
     a.nslices = S.nslices;
-    a.dcode = S.dcode.empty() ? nullptr : S.dcode.get();
     a.nrows = S.nrows;
     return a;
 }
@@ -1409,7 +1095,6 @@ template <int F = kFDict>
 DictParam<F> dict_param(const Sell& S) {
     DictParam<F> dp;
     for (int i = 0; i < 256; ++i) dp.e[i] = i < static_cast<int>(S.hdict.size()) ? S.hdict[i] : make_ulonglong2(0ULL, 0ULL);
-    for (int i = 0; i < 256; ++i) dp.dg[i] = i < static_cast<int>(S.hdiag.size()) ? S.hdiag[i] : 1.0;
     return dp;
 }
 DictParam<kFCoded> coded_param(const Sell& S) { return dict_param<kFCoded>(S); }
@@ -1580,14 +1265,17 @@ bool build_sten_wide(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sel
     return false;
 }
 
-void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, bool allow_dict,
+void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, int storage,
                 const double* l1) {
     sell_prologue(M, rows, nrows, S, s);
 
-    // Format choice (measured on B200): DICT keeps 32 registers
-    // and full occupancy, best for short rows; PAT removes the per-entry code
-    // stream, best once rows are long (27-point: 187 vs 198 us per L0 sweep).
-    if (allow_dict) {
+    // Format choice (measured on B200): STEN whenever the rows
+    // nest into one main pattern; else DICT keeps 32 registers and full
+    // occupancy, best for short rows; PAT removes the per-entry code stream,
+    // best once rows are long (27-point: 187 vs 198 us per L0 sweep); CODED
+    // for few distinct values with irregular offsets; PLAIN otherwise.  A
+    // forced format (pairamg_setup_config::storage) falls back to PLAIN.
+    if (storage != Sell::kPlain) {
         int maxlen = 0;
         {
             DBuf<int64_t> mx(1, s);
@@ -1598,20 +1286,29 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
             PB_CUDA(cudaStreamSynchronize(s));
             maxlen = static_cast<int>(h);
         }
-        const int pref = env_int("PAIRAMG_SELL_PAT", -1);  // 1 force PAT, 0 never, -1 auto
-        const bool want_pat = pref == 1 || (pref == -1 && maxlen > 16);
-        if (env_flag("PAIRAMG_SELL_STEN", true) && maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
-            if (try_sten(S)) {
-                plan_sten_windows(S);
-                return;
+        if (storage < 0) {
+            const bool want_pat = maxlen > 16;
+            if (maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
+                if (try_sten(S) || want_pat) return;
+                reset_pat(S);
             }
-            if (want_pat) return;
-            reset_pat(S);
+            if (want_pat && try_pattern(M, rows, S, l1, s)) return;
+            if (try_dict(M, rows, S, l1, s)) return;
+            if (!want_pat && try_pattern(M, rows, S, l1, s)) return;
+            if (try_coded(M, rows, S, s)) return;
+        } else if (storage == Sell::kSten) {
+            if (maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
+                if (try_sten(S)) return;
+                reset_pat(S);
+            }
+        } else if (storage == Sell::kPat) {
+            if (try_pattern(M, rows, S, l1, s)) return;
+        } else if (storage == Sell::kDict) {
+            if (try_dict(M, rows, S, l1, s)) return;
+        } else if (storage == Sell::kCoded) {
+            if (try_coded(M, rows, S, s)) return;
         }
-        if (want_pat && try_pattern(M, rows, S, l1, s)) return;
-        if (env_flag("PAIRAMG_SELL_PAIRS", true) && try_dict(M, rows, S, l1, s)) return;
-        if (pref != 0 && !want_pat && try_pattern(M, rows, S, l1, s)) return;
-        if (env_flag("PAIRAMG_SELL_CODED", true) && try_coded(M, rows, S, s)) return;
+        sell_prologue(M, rows, nrows, S, s);
     }
     S.format = Sell::kPlain;
     slice_widths(M, rows, S, s);
@@ -1640,7 +1337,7 @@ double sell_op_bytes(const Sell& S, int op) {
     const double n = static_cast<double>(S.nrows), mat = sell_bytes(S);
     switch (op) {
         case kSpmv: return mat + 16.0 * n;                                             // x, y
-        case kJacobi: return mat + (S.format == Sell::kPat || S.format == Sell::kSten ? 24.0 : S.dcode.empty() ? 32.0 : 25.0) * n;  // x, r, (d), y
+        case kJacobi: return mat + (S.format == Sell::kPat || S.format == Sell::kSten ? 24.0 : 32.0) * n;  // x, r, (d), y
         case kResid: return mat + 24.0 * n;                                            // x, r, y
         default: return mat + 32.0 * n;                                                // spmv+dots: w, r, q, v
     }
@@ -1664,7 +1361,7 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
             case kSpmv: PB_STEN(kSpmv) break;
             case kJacobi: PB_STEN(kJacobi) break;
             case kResid: PB_STEN(kResid) break;
-            default: fail(PAIRAMG_INTERNAL, "sell_apply: fused operators need PAIRAMG_SELL_STEN=0 PAIRAMG_SELL_PAT=0");
+            default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
         }
 #undef PB_STEN
         PB_CHECK_LAUNCH();
@@ -1687,25 +1384,9 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
             case kSpmv: PB_PAT(kSpmv) break;
             case kJacobi: PB_PAT(kJacobi) break;
             case kResid: PB_PAT(kResid) break;
-            default: fail(PAIRAMG_INTERNAL, "sell_apply: fused operators need PAIRAMG_SELL_PAT=0");
+            default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
         }
 #undef PB_PAT
-        PB_CHECK_LAUNCH();
-        return;
-    }
-    if (use_win(S, o)) {
-        WinArgs w = win_args_of(S);
-        w.x = o.x;
-        w.y = o.y;
-        w.r = o.r;
-        w.d = o.d;
-        w.omega = o.omega;
-        const DictParam<kFDict> dp = win_param(S);
-        switch (o.op) {
-            case kSpmv: k_win<kSpmv><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
-            case kJacobi: k_win<kJacobi><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
-            default: k_win<kResid><<<S.win.grid, kWinThreads, S.win.smem, s>>>(w, dp); break;
-        }
         PB_CHECK_LAUNCH();
         return;
     }
@@ -1715,15 +1396,10 @@ void sell_apply(const Sell& S, const SellOpArgs& o, cudaStream_t s) {
     a.r = o.r;
     a.d = o.d;
     a.omega = o.omega;
-    a.pcol = o.pcol;
-    a.pval = o.pval;
-    a.e = o.e;
     switch (o.op) {
         case kSpmv: launch_op<kSpmv>(S, a, s); break;
         case kJacobi: launch_op<kJacobi>(S, a, s); break;
         case kResid: launch_op<kResid>(S, a, s); break;
-        case kJacobiZero: launch_op<kJacobiZero>(S, a, s); break;
-        case kJacobiProl: launch_op<kJacobiProl>(S, a, s); break;
         default: fail(PAIRAMG_INTERNAL, "sell_apply: bad op");
     }
 }
@@ -1732,7 +1408,7 @@ bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, doub
     // <= 8 records: with 27 the remote (DSMEM) gathers outweigh the saved
     // launches (measured 1.28 vs 1.25 ms/iter at 27-point 192^3)
     if (S.format != Sell::kSten || !S.rows.empty() || S.row0 != 0 || S.nrows != S.xlen || nu < 1 ||
-        S.nrows > int64_t(kCoarseCta) * kCoarseRows || S.sten_L > env_int("PAIRAMG_COARSE_CLUSTER_L", 8))
+        S.nrows > int64_t(kCoarseCta) * kCoarseRows || S.sten_L > 8)
         return false;
     const int R = static_cast<int>((S.nrows + kCoarseCta - 1) / kCoarseCta);
     StenArgs a = sten_args_of(S);
@@ -1762,8 +1438,7 @@ bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, doub
 }
 
 bool sell_split_ok(const Sell& I, const Sell& B) {
-    return I.format == Sell::kSten && B.format == Sell::kSten && I.rows.empty() && I.nrows > 0 && B.nrows > 0 &&
-           env_flag("PAIRAMG_HALO_SPLIT", true);
+    return I.format == Sell::kSten && B.format == Sell::kSten && I.rows.empty() && I.nrows > 0 && B.nrows > 0;
 }
 
 namespace {
@@ -1809,7 +1484,7 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
             P.h.send_idx = hs->send_idx;
         }
     }
-    P.h.bnd_last = env_flag("PAIRAMG_BND_LAST", true) ? 1 : 0;
+    P.h.bnd_last = 1;
     P.grid = P.h.npush + P.h.nblk_a + P.h.nblk_b;
     return P;
 }
@@ -1882,7 +1557,6 @@ int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* 
 
 int sell_dots_grid(const Sell& S, int cap) {
     if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256), cap);
-    if (S.format == Sell::kDict && S.win.ok) return S.win.grid;
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
@@ -1917,17 +1591,6 @@ int sell_spmv_dots(const Sell& S, const double* w, double* v, const double* r, c
             k_pat_spmv_dots<true><<<grid, kThreads, 0, s>>>(p);
         else
             k_pat_spmv_dots<false><<<grid, kThreads, 0, s>>>(p);
-        PB_CHECK_LAUNCH();
-        return grid;
-    }
-    if (S.format == Sell::kDict && S.win.ok && aligned16(w) && aligned16(r) && aligned16(q)) {
-        WinArgs wa = win_args_of(S);
-        wa.x = w;
-        wa.y = v;
-        wa.r = r;
-        wa.q = q;
-        wa.partials = partials;
-        k_win<-1><<<grid, kWinThreads, S.win.smem, s>>>(wa, win_param(S));
         PB_CHECK_LAUNCH();
         return grid;
     }

@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_con
 
 // ---------------------------------------------------------------------------
 // The coarsest level's whole smoothing (zero start + nu-1 l1-Jacobi sweeps,
-// cycle.cpp:126-133) in ONE launch of one thread-block cluster: every CTA
+// cycle.cpp:86-93) in ONE launch of one thread-block cluster: every CTA
 // owns R consecutive rows, keeps its slice of the iterate in shared memory
 // (ping-pong), gathers neighbours from the owning CTA's shared memory
 // (distributed shared memory) and the cluster barrier separates the sweeps.

@@ -10,7 +10,7 @@
 //     k_galerkin_*         galerkin_product R*(A*P) (amg.cpp:110-142) as ONE fused
 //                          kernel per coarse row: the A*P row products and the R*C
 //                          accumulation in the reference's exact summation order
-//                          (csr.cpp:363-429), two-phase (symbolic count, numeric fill)
+//                          (csr.cpp:206-272), two-phase (symbolic count, numeric fill)
 //     k_wnext              w_{k+1} = R w_k (amg.cpp:244-247)
 //   per level: k_compose (compose_prolongators, amg.cpp:79-85), composed Galerkin,
 //   R = P^T (transpose_block, amg.cpp:87-108), l1 diagonal, halo plan, SELL copy.
@@ -284,7 +284,7 @@ __global__ void k_pext(const int32_t* __restrict__ pcol, const double* __restric
 // order (fine row t of R's row ascending, then A's row in CSR order), each
 // (gc = P column of a_ij's column, v = a_ij * p_j, r_t).  Per distinct coarse
 // column:  C_t = first v, then + later v of fine row t (A*P entry,
-// csr.cpp:302-317);  A_c = first r_t*C_t, then + later ones (R*C entry).
+// csr.cpp:145-160);  A_c = first r_t*C_t, then + later ones (R*C entry).
 struct GalerkinArgs {
     const int64_t* rp;
     const int32_t* col;
@@ -714,7 +714,7 @@ void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* 
     PB_CHECK_LAUNCH();
 }
 
-void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows) {
+void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows, int storage) {
     h.rep_level = -1;
     h.rep.clear();
     if (rt.nranks() == 1) return;
@@ -726,7 +726,6 @@ void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows) {
             break;
         }
     if (kr < 0) return;
-    const bool dict = env_flag("PAIRAMG_SELL_DICT", true);
     for (int k = kr; k < h.nl(); ++k) {
         Level& D = *h.levels[k];
         auto R = std::make_unique<Level>();
@@ -754,7 +753,7 @@ void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows) {
         R->A.val = std::move(gval);
         R->l1.alloc(static_cast<size_t>(ng), s);
         l1_diagonal(R->A, R->l1.get(), s);
-        build_sell(R->A, nullptr, ng, R->sell_all, s, dict, R->l1.get());
+        build_sell(R->A, nullptr, ng, R->sell_all, s, storage, R->l1.get());
         R->x.alloc(static_cast<size_t>(ng), s);
         R->xt.alloc(static_cast<size_t>(ng), s);
         R->x.zero(s);
@@ -782,6 +781,55 @@ void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows) {
     h.rep_recv.alloc(static_cast<size_t>(std::max<int64_t>(h.rep_max * rt.nranks(), 1)), s);
     h.rep_level = kr;
     PB_CUDA(cudaStreamSynchronize(s));
+}
+
+// SetupConfig::replay (amg.cpp:182-197): the owned block of a recorded
+// global matching, checked as the reference checks it -- a mate outside
+// [h_own, k_own) crosses the partition (amg.cpp:187-189), a non-mutual or
+// self mate is an invalid matching (build_pairwise_prolongator, amg.cpp:54-57).
+static __global__ void k_replay_local(const int64_t* __restrict__ gm, int64_t n, int64_t h_own,
+                               int64_t* __restrict__ mate, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t g = gm[i];
+    if (g == -1) {
+        mate[i] = -1;
+    } else if (g < h_own || g >= h_own + n) {
+        atomicOr(bad, 1);
+        mate[i] = -1;
+    } else {
+        mate[i] = g - h_own;
+    }
+}
+
+static __global__ void k_replay_check(const int64_t* __restrict__ mate, int64_t n, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t j = mate[i];
+    if (j != -1 && (j == i || mate[j] != i)) atomicOr(bad, 2);
+}
+
+static void replay_matching(const SetupConfig& cfg, size_t step, int64_t fine_n, int64_t h_own, int64_t n, int64_t* mate,
+                     cudaStream_t s) {
+    if (step >= cfg.replay.size()) fail(PAIRAMG_CONTRACT_VIOLATION, "setup: matching trace exhausted");
+    if (!cfg.replay[step] || cfg.replay_sizes[step] != fine_n)
+        fail(PAIRAMG_CONTRACT_VIOLATION, "setup: replayed matching of step " + std::to_string(step) + " has " +
+                                             std::to_string(cfg.replay_sizes[step]) + " entries, the level has " +
+                                             std::to_string(fine_n) + " rows");
+    if (!n) return;
+    DBuf<int64_t> gm(static_cast<size_t>(n), s);
+    DBuf<int> bad(1, s);
+    bad.zero(s);
+    PB_CUDA(cudaMemcpyAsync(gm.get(), cfg.replay[step] + h_own, 8 * n, cudaMemcpyHostToDevice, s));
+    LAUNCH(k_replay_local, n, gm.get(), n, h_own, mate, bad.get());
+    int hb = 0;
+    PB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (hb & 1) fail(PAIRAMG_CONTRACT_VIOLATION, "setup: replayed matching crosses the rank partition");
+    LAUNCH(k_replay_check, n, mate, n, bad.get());
+    PB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+    PB_CUDA(cudaStreamSynchronize(s));
+    if (hb & 2) fail(PAIRAMG_CONTRACT_VIOLATION, "build_pairwise_prolongator: invalid matching");
 }
 
 void suitor_match_device(const int64_t* rp, const int32_t* col, const double* w, int64_t n, int64_t* mate,
@@ -820,6 +868,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
     }
     h.levels.push_back(std::move(L0));
 
+    size_t trace_step = 0;
     while (h.nl() < cfg.max_levels && h.levels.back()->A.n_global > cfg.coarse_size_target) {
         Level& Lf = *h.levels.back();
         const int level_index = h.nl();
@@ -842,17 +891,22 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             PB_CUDA(cudaStreamSynchronize(s));
             const auto tm = Clock::now();
             const int64_t msg0 = rt.stats().total_messages();
-            DBuf<double> diag(static_cast<size_t>(n), s), gw(static_cast<size_t>(A_pair->nnz), s);
-            DBuf<ull> clamped(1, s);
-            clamped.zero(s);
-            LAUNCH(k_diag, n, A_pair->rp.get(), A_pair->col.get(), A_pair->val.get(), n, diag.get());
-            LAUNCH(k_weights, n, A_pair->rp.get(), A_pair->col.get(), A_pair->val.get(), n, w_pair.get(),
-                   diag.get(), gw.get(), clamped.get());
-            DBuf<ull> slot(static_cast<size_t>(2 * n), s);
-            slot.zero(s);
-            LAUNCH(k_suitor, n, A_pair->rp.get(), A_pair->col.get(), gw.get(), n, slot.get());
             DBuf<int64_t> mate(static_cast<size_t>(n), s);
-            LAUNCH(k_mate, n, slot.get(), n, mate.get());
+            if (!cfg.replay.empty()) {
+                replay_matching(cfg, trace_step, fine_n, part[rank], n, mate.get(), s);
+            } else {
+                DBuf<double> diag(static_cast<size_t>(n), s), gw(static_cast<size_t>(A_pair->nnz), s);
+                DBuf<ull> clamped(1, s);
+                clamped.zero(s);
+                LAUNCH(k_diag, n, A_pair->rp.get(), A_pair->col.get(), A_pair->val.get(), n, diag.get());
+                LAUNCH(k_weights, n, A_pair->rp.get(), A_pair->col.get(), A_pair->val.get(), n, w_pair.get(),
+                       diag.get(), gw.get(), clamped.get());
+                DBuf<ull> slot(static_cast<size_t>(2 * n), s);
+                slot.zero(s);
+                LAUNCH(k_suitor, n, A_pair->rp.get(), A_pair->col.get(), gw.get(), n, slot.get());
+                LAUNCH(k_mate, n, slot.get(), n, mate.get());
+            }
+            ++trace_step;
             DBuf<int64_t> pos(static_cast<size_t>(n + 1), s);
             LAUNCH(k_leader, n + 1, mate.get(), n, pos.get());
             cub_call([&](void* t, size_t& b) {
@@ -890,7 +944,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             DBuf<int64_t> pc;
             DBuf<double> pv;
             PExt px;
-            if (pair_galerkin && env_flag("PAIRAMG_SETUP_OVERLAP", false))
+            if (pair_galerkin && cfg.setup_overlap)
                 extend_p_begin(rt, *A_pair, agg.get(), pval.get(), cpart[rank], pc, pv, px);
 
             // ---- R, w_next, composition ----
@@ -953,7 +1007,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             DBuf<int64_t> pc;
             DBuf<double> pv;
             PExt px;
-            const bool ov = env_flag("PAIRAMG_SETUP_OVERLAP", false);
+            const bool ov = cfg.setup_overlap;
             if (ov) extend_p_begin(rt, Lf.A, comp_col.get(), comp_val.get(), part[rank], pc, pv, px);
             DBuf<int64_t> rrp;
             DBuf<int32_t> rcol;
@@ -990,24 +1044,21 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         L.l1.alloc(static_cast<size_t>(n), s);
         l1_diagonal(L.A, L.l1.get(), s);
         if (L.A.halo.n_halo > 0) {
-            build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, env_flag("PAIRAMG_SELL_DICT", true),
-                       L.l1.get());
+            build_sell(L.A, L.A.interior_rows.get(), n - L.A.n_boundary, L.sell_int, s, cfg.storage, L.l1.get());
             // boundary rows: STEN too when the faces' halo offsets nest into
             // one main pattern (slab partitions), else PAT/DICT/PLAIN
-            build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s,
-                       env_flag("PAIRAMG_SELL_DICT", true) && env_flag("PAIRAMG_BND_FORMATS", true), L.l1.get());
+            build_sell(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bnd, s, cfg.storage, L.l1.get());
             // an interior rank's two faces reach different halo slots: with
             // 27 points their merged pattern has 36 records -> wide STEN for
             // the split launch (boundary blocks take up to 64)
-            if (L.sell_bnd.format != Sell::kSten && env_flag("PAIRAMG_SELL_STEN", true) &&
-                env_flag("PAIRAMG_STEN_WIDE", true))
+            if (L.sell_bnd.format != Sell::kSten && (cfg.storage < 0 || cfg.storage == Sell::kSten))
                 build_sten_wide(L.A, L.A.boundary_rows.get(), L.A.n_boundary, L.sell_bndw, s, L.l1.get());
             // whole level incl. halo columns, for the exchange-then-compute
             // schedule (slab partitions keep constant halo column offsets,
             // so DICT/PAT usually still apply)
-            build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true), L.l1.get());
+            build_sell(L.A, nullptr, n, L.sell_all, s, cfg.storage, L.l1.get());
         } else {
-            build_sell(L.A, nullptr, n, L.sell_all, s, env_flag("PAIRAMG_SELL_DICT", true), L.l1.get());
+            build_sell(L.A, nullptr, n, L.sell_all, s, cfg.storage, L.l1.get());
         }
         L.x.alloc(static_cast<size_t>(next), s);
         L.xt.alloc(static_cast<size_t>(next), s);
@@ -1023,7 +1074,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
     h.opc = opc;
     {
         const auto tc = Clock::now();
-        replicate_coarse_levels(rt, h, env_int("PAIRAMG_REPLICATE_ROWS", 2500000));
+        replicate_coarse_levels(rt, h, cfg.replicate_rows, cfg.storage);
         h.stats.t_spmm_comm += since(tc);
     }
     PB_CUDA(cudaStreamSynchronize(s));

@@ -1,6 +1,6 @@
 // solve.cu -- the solve path: the symmetric V-cycle (vcycle_apply,
-// cycle.cpp:126-152) with l1-Jacobi sweeps (cycle.cpp:77-102), local
-// restriction / prolongation (cycle.cpp:104-124), and Notay's flexible CG
+// cycle.cpp:86-112) with l1-Jacobi sweeps (cycle.cpp:37-62), local
+// restriction / prolongation (cycle.cpp:64-84), and Notay's flexible CG
 // (Alg. 1) with one fused dot-triple reduction and one
 // fused four-vector update per iteration.  One whole FCG iteration (all
 // levels, halos, reductions) is captured once into a CUDA graph and
@@ -20,7 +20,7 @@ namespace {
 
 constexpr int kRedThreads = 256;
 
-// x = (omega*r)/d : the zero-start sweep (cycle.cpp:89-93)
+// x = (omega*r)/d : the zero-start sweep (cycle.cpp:49-53)
 __global__ void k_zero_start(const double* r, const double* d,
                              double* x, int64_t n, double omega) {
     pdl_begin();
@@ -28,7 +28,7 @@ __global__ void k_zero_start(const double* r, const double* d,
     if (i < n) x[i] = ddiv(dmul(omega, r[i]), d[i]);
 }
 
-// restrict_to_coarse (cycle.cpp:104-115): rc_c = 0.0 + sum R_ci res_i, fine ascending
+// restrict_to_coarse (cycle.cpp:64-75): rc_c = 0.0 + sum R_ci res_i, fine ascending
 __global__ void k_restrict(const int64_t* rrp, const int32_t* rcol,
                            const double* rval, const double* res,
                            double* rc, int64_t nc) {
@@ -40,7 +40,7 @@ __global__ void k_restrict(const int64_t* rrp, const int32_t* rcol,
     rc[c] = s;
 }
 
-// prolongate_add (cycle.cpp:117-124): x_i = x_i + p_i * e_agg(i)
+// prolongate_add (cycle.cpp:77-84): x_i = x_i + p_i * e_agg(i)
 __global__ void k_prolong(const int32_t* pcol, const double* pval,
                           const double* e, double* x, int64_t n) {
     pdl_begin();
@@ -103,7 +103,7 @@ CodeTab code_tab(const std::vector<double>& v) {
 // FCG vector updates (Alg. 1 lines 16-19), op order shared with the oracle:
 //   d = w - c d ; q = v - c q ; u = u + a d ; r = r - a q ;  plus |r|^2 partials.
 // ZS: also forms the next V-cycle's level-0 zero-start sweep from the new
-// residual, x1 = (omega*r)/d (cycle.cpp:89-93), while r is in registers; d
+// residual, x1 = (omega*r)/d (cycle.cpp:49-53), while r is in registers; d
 // is the pattern's l1 diagonal (STEN level 0: one byte per row) or the l1
 // array.
 template <bool ZS>
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kRedThreads)
     }
 }
 
-// Cross-rank sums in rank order (runtime.cpp:388-396), then the FCG scalar
+// Cross-rank sums in rank order (runtime.cpp:250-258), then the FCG scalar
 // recurrences (Alg. 1 lines 4-5, 14; breakdown check SPEC.md:478).
 __global__ void k_fcg_scalars(const double* g, int p, FcgState* st) {
     pdl_begin();
@@ -296,6 +296,15 @@ __global__ void k_norm_final(const double* g, int p, FcgState* st, int init) {
     }
 }
 
+// validate_cycle_config (cycle.cpp:7-13): negative sweep counts are an
+// error, pre != post a warning (the preconditioner is then not symmetric).
+std::string check_cycle(const CycleConfig& cc) {
+    if (cc.pre_sweeps < 0 || cc.post_sweeps < 0 || cc.coarsest_sweeps < 0)
+        fail(PAIRAMG_INVALID_ARGUMENT, "cycle config: sweep counts must be >= 0");
+    if (cc.pre_sweeps != cc.post_sweeps) return "pre_sweeps != post_sweeps: the V-cycle preconditioner is not symmetric";
+    return {};
+}
+
 int red_grid(int64_t n) {
     const int64_t want = (n + kRedThreads - 1) / kRedThreads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
@@ -304,10 +313,11 @@ int red_grid(int64_t n) {
 }  // namespace
 
 Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
-    fuse = env_flag("PAIRAMG_FUSE", false);
+    // spmv_dist's overlap flag (dist.cpp:128-199): interior rows while the
+    // halo is in flight (default, as every reference call site) or exchange first
     overlap = env_flag("PAIRAMG_OVERLAP", true);
-    bnd_on_comm = env_flag("PAIRAMG_BND_ON_COMM", true);
-    halo_grid_ = kSmCount * env_int("PAIRAMG_HALO_CTAS_PER_SM", 4);
+    p2p_ = env_flag("PAIRAMG_P2P", true);
+    halo_grid_ = kSmCount * 4;
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     PB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_state_), sizeof(FcgState)));
@@ -332,22 +342,6 @@ void Solver::destroy_graph() {
     graph_ = nullptr;
     if (loop_graph_) cudaGraphExecDestroy(loop_graph_);
     loop_graph_ = nullptr;
-}
-
-// Multi-rank solves run the device-side loop only when nothing in the
-// iteration goes through NCCL (a conditional graph body with NCCL kernels
-// hung): NVLink halos on every distributed level, the P2P dot allgather and
-// the P2P replicated-rhs gather.
-bool Solver::nccl_free_iteration() {
-    if (rt.nranks() == 1) return true;
-    if (!env_flag("PAIRAMG_GRAPH_LOOP_MR", false) || !dots_gather_.ok) return false;  // measured no faster at N=2
-    if (h.rep_level >= 0 && !rep_gather_.ok) return false;
-    const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
-    for (int k = 0; k < nd; ++k) {
-        const Level& L = *h.levels[static_cast<size_t>(k)];
-        if (L.A.halo.has_traffic() && !L.p2p.ok) return false;
-    }
-    return true;
 }
 
 void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters) {
@@ -390,16 +384,16 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
     destroy_graph();
     ready = false;
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
-    if (rt.nranks() > 1 && env_flag("PAIRAMG_P2P", true) && env_flag("PAIRAMG_P2P_DOTS", true))
+    if (rt.nranks() > 1 && p2p_)
         p2p_gather_setup(rt, dots_gather_, 4, s_);  // collective
-    if (rt.nranks() > 1 && env_flag("PAIRAMG_P2P", true)) {  // collective: every rank, every distributed level
+    if (rt.nranks() > 1 && p2p_) {  // collective: every rank, every distributed level
         const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
         for (int k = 0; k < nd; ++k) p2p_setup(rt, h.levels[static_cast<size_t>(k)]->A.halo, h.levels[static_cast<size_t>(k)]->p2p, s_);
     }
     p2p_seg_destroy(rep_gather_);
-    if (rt.nranks() > 1 && h.rep_level >= 0 && env_flag("PAIRAMG_P2P", true) && env_flag("PAIRAMG_P2P_REP", true))
+    if (rt.nranks() > 1 && h.rep_level >= 0 && p2p_)
         p2p_seg_setup(rt, rep_gather_, h.rep[0]->A.n, s_);  // collective
-    if (env_flag("PAIRAMG_TRANSFER_CODES", true)) {
+    {  // byte codes of the transfer values (<= 256 distinct per level)
         auto codes = [&](Level& L) {
             if (L.pval.empty()) return;
             build_value_codes(L.pval.get(), static_cast<int64_t>(L.pval.size()), L.pcode, L.ptab, s_);
@@ -496,27 +490,8 @@ void Solver::end_time(int kc) {
     tcount_[kc] = idx + 1;
 }
 
-void Solver::hrec(cudaEvent_t e, cudaStream_t st) {
-    if (capturing(st))
-        PB_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
-    else
-        PB_CUDA(cudaEventRecord(e, st));
-}
-
 void Solver::collect_times() {
     if (!timing) return;
-    if (hcount_ > 0) {  // PAIRAMG_HALO_TRACE summary (rank, averages in us from the compute-stream start)
-        double acc[4] = {0, 0, 0, 0};
-        for (int i = 0; i < hcount_; ++i)
-            for (int j = 1; j < 5; ++j) {
-                float ms = 0.f;
-                PB_CUDA(cudaEventElapsedTime(&ms, htrace_[static_cast<size_t>(i)][0], htrace_[static_cast<size_t>(i)][j]));
-                acc[j - 1] += ms * 1e3 / hcount_;
-            }
-        std::fprintf(stderr, "halo trace rank %d (%d sweeps): comm start %.1f  exchange done %.1f  boundary done %.1f  interior done %.1f us\n",
-                     rt.rank(), hcount_, acc[0], acc[1], acc[2], acc[3]);
-        hcount_ = 0;
-    }
     for (int kc = 0; kc < kNumClasses; ++kc)
         for (int i = 0; i < tcount_[kc]; ++i) {
             float ms = 0.f;
@@ -552,17 +527,6 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         end_time(kc);
         return;
     }
-    const bool trace = timing && kc == 0 && L.A.halo.n_halo > 0 && bnd_on_comm && env_flag("PAIRAMG_HALO_TRACE", false);
-    std::array<cudaEvent_t, 5>* tr = nullptr;
-    if (trace) {
-        while (static_cast<int>(htrace_.size()) <= hcount_) {
-            std::array<cudaEvent_t, 5> ev;
-            for (auto& e : ev) PB_CUDA(cudaEventCreate(&e));
-            htrace_.push_back(ev);
-        }
-        tr = &htrace_[static_cast<size_t>(hcount_++)];
-        hrec((*tr)[0], s_);
-    }
     if (L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) &&
         (o.op == kSpmv || o.op == kJacobi || o.op == kResid)) {
         // push this rank's boundary values into the neighbours, then one
@@ -575,39 +539,28 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         return;
     }
     if (L.A.halo.has_traffic()) {
-        if (o.op == kJacobiZero || o.op == kJacobiProl)
-            fail(PAIRAMG_INTERNAL, "fused sweeps need a level without halo traffic");
         // The boundary rows run on the (high-priority) communication stream
         // right behind the halo receive, concurrently with the interior rows:
         // the compute stream only joins at the end, no second launch on it.
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
-        if (tr) hrec((*tr)[1], rt.comm_stream());
         exchange(L, o.x, rt.comm_stream());
-        if (tr) hrec((*tr)[2], rt.comm_stream());
-        if (L.A.halo.n_halo > 0 && bnd_on_comm) {
+        if (L.A.halo.n_halo > 0) {
             sell_apply(L.sell_bnd, o, rt.comm_stream());
             launches_ += 1;
         }
-        if (tr) hrec((*tr)[3], rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += L.A.halo.send_off.back() ? 1 : 0;
     }
-    if (L.A.halo.n_halo > 0 && bnd_on_comm) {
+    if (L.A.halo.n_halo > 0) {
         // capped grid: the interior kernel leaves SM slots to the pack/NCCL/
         // boundary kernels (else they only run once every interior CTA has
         // been dispatched; measured: halo done at 91 us of an 89 us interior)
         SellOpArgs oi = o;
         oi.max_grid = halo_grid_;
         sell_apply(L.sell_int, oi, s_);
-        if (tr) hrec((*tr)[4], s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         launches_ += 1;
-    } else if (L.A.halo.n_halo > 0) {
-        sell_apply(L.sell_int, o, s_);
-        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        sell_apply(L.sell_bnd, o, s_);
-        launches_ += 2;
     } else {
         if (L.A.halo.has_traffic()) PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         sell_apply(L.sell_all, o, s_);
@@ -627,12 +580,6 @@ static SellOpArgs jacobi_args(int op, const double* x, double* y, const double* 
     return o;
 }
 
-bool Solver::fusable(int k) {
-    const Level& L = lvl(k);
-    return fuse && !L.A.halo.has_traffic() && (L.sell_all.format == Sell::kDict || L.sell_all.format == Sell::kPlain ||
-                                                  L.sell_all.format == Sell::kCoded);
-}
-
 void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& xc, double*& xo, double omega,
                     bool l0) {
     Level& L = lvl(k);
@@ -645,10 +592,6 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
     if (zero_start && k == 0 && zs_pending_) {  // x1 already formed by the previous update / the solve prologue
         zs_pending_ = false;
         sweep = 1;
-    } else if (zero_start && nu >= 2 && fusable(k)) {
-        // sweeps 1+2 in one pass: x1 = (omega*r)/d is formed at every gathered column
-        apply(k, jacobi_args(kJacobiZero, nullptr, xc, rhs, L.l1.get(), omega), l0 ? 4 : -1);
-        sweep = 2;
     } else if (zero_start) {
         begin_time(-1);
         if (n) launch_k<4>(k_zero_start, blocks_for(n, 256), 256, 0, s_, rhs, L.l1.get(), xc, n, omega);
@@ -717,17 +660,7 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     vcycle_enqueue(k + 1, crhs, e, cc);
     begin_time(lc);
     if (gather) e += h.rep_offsets[static_cast<size_t>(rt.rank())];
-    int post = cc.post_sweeps;
-    if (post >= 1 && fusable(k)) {
-        // prolongate_add fused into the first post-sweep: x_j + p_j*e_agg(j) on the fly
-        SellOpArgs o = jacobi_args(kJacobiProl, xc, xo, rhs, L.l1.get(), cc.relax_weight);
-        o.pcol = T.pcol.get();
-        o.pval = T.pval.get();
-        o.e = e;
-        apply(k, o, l0 ? 5 : -1);
-        std::swap(xc, xo);
-        --post;
-    } else {
+    {
         const bool v4 = L.A.n >= 4 && (reinterpret_cast<uintptr_t>(xc) & 15) == 0;  // 16-byte aligned buffers
         if (L.A.n && !T.pcode.empty() && v4) {
             const int64_t n4 = L.A.n / 4;  // the < 4 tail rows by the scalar kernel
@@ -747,7 +680,7 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
         PB_CHECK_LAUNCH();
         launches_ += 1;
     }
-    smooth(k, false, post, rhs, xc, xo, cc.relax_weight, l0);
+    smooth(k, false, cc.post_sweeps, rhs, xc, xo, cc.relax_weight, l0);
     end_time(lc);
     out = xc;
 }
@@ -800,7 +733,7 @@ void Solver::reduce_norm_enqueue(bool init) {
 // that produced its right-hand side (and by the solve prologue for the first).
 bool Solver::zs_fused(const CycleConfig& cc, bool precflag) {
     const int nu0 = h.nl() == 1 ? cc.coarsest_sweeps : cc.pre_sweeps;
-    return precflag && nu0 >= 1 && !fusable(0) && env_flag("PAIRAMG_ZS_FUSE", true);
+    return precflag && nu0 >= 1;
 }
 
 ZeroStart Solver::zero_start_args(const CycleConfig& cc) {
@@ -845,7 +778,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.split_bnd(), w, v_.get(), r_.get(), q_.get(), partials_.get(),
                                           max_blocks_, hs, s_);
         launches_ += hs.fused ? 1 : 2;
-    } else if (L0.A.halo.n_halo > 0 && bnd_on_comm) {  // boundary rows behind the halo, on the comm stream
+    } else if (L0.A.halo.n_halo > 0) {  // boundary rows behind the halo, on the comm stream
         const int g1 = sell_dots_grid(L0.sell_int, halo_grid_);
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
@@ -866,16 +799,8 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         launches_ += 1;
     }
-    if ((L0.A.halo.has_traffic() && !overlap) || (L0.A.halo.n_halo > 0 && bnd_on_comm) ||
-        (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.split_bnd()))) {
+    if ((L0.A.halo.has_traffic() && !overlap) || L0.A.halo.n_halo > 0) {
         // done above
-    } else if (L0.A.halo.n_halo > 0) {
-        const int g1 = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
-        PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        const int g2 = sell_spmv_dots(L0.sell_bnd, w, v_.get(), r_.get(), q_.get(), partials_.get() + 3 * g1,
-                                      max_blocks_, s_);
-        dots_grid_ = g1 + g2;
-        launches_ += 2;
     } else {
         if (L0.A.halo.has_traffic()) PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
@@ -901,8 +826,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
                    bool precflag, pairamg_solve_stats* st) {
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "solve: setup not run");
     if (rtol <= 0.0 || max_iters < 1) fail(PAIRAMG_INVALID_ARGUMENT, "solve: need rtol > 0 and max_iters >= 1");
-    if (cc.pre_sweeps < 0 || cc.post_sweeps < 0 || cc.coarsest_sweeps < 0)
-        fail(PAIRAMG_INVALID_ARGUMENT, "cycle config: sweep counts must be >= 0");
+    cycle_warning = check_cycle(cc);
     Level& L0 = *h.levels[0];
     for (auto& kt : ktime) kt = KernelClassTiming{};
     // Algorithmic bytes per level-0 launch of the stored format (matrix
@@ -910,7 +834,6 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     const double n0 = static_cast<double>(n_);
     const double mat = L0.A.halo.n_halo > 0 ? sell_bytes(L0.sell_int) + sell_bytes(L0.sell_bnd)
                                             : sell_bytes(L0.sell_all);
-    const double nc1 = h.nl() > 1 ? static_cast<double>(h.levels[1]->A.n) : 0.0;
     auto op_bytes = [&](int op) {
         return L0.A.halo.n_halo > 0 ? sell_op_bytes(L0.sell_int, op) + sell_op_bytes(L0.sell_bnd, op)
                                     : sell_op_bytes(L0.sell_all, op);
@@ -921,8 +844,6 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     // 6 vectors read, 4 written; + the fused zero-start: pattern byte (or l1) read, x1 written
     const bool zs = zs_fused(cc, precflag);
     ktime[3].bytes_per_launch = (80.0 + (zs ? (zero_start_args(cc).pid ? 9.0 : 16.0) : 0.0)) * n0;
-    ktime[4].bytes_per_launch = mat + 24.0 * n0;              // r, d read; y written
-    ktime[5].bytes_per_launch = mat + 44.0 * n0 + 8.0 * nc1;  // x, p, pcol, r, d read, e; y written
 
     cudaEvent_t e0, e1;
     PB_CUDA(cudaEventCreate(&e0));
@@ -982,7 +903,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             graph_prec_ = precflag;
             graph_timing_ = timing;
         }
-        const bool device_loop = loop_ok && !timing && env_flag("PAIRAMG_GRAPH_LOOP", true) && nccl_free_iteration();
+        const bool device_loop = loop_ok && !timing && rt.nranks() == 1 && env_flag("PAIRAMG_GRAPH_LOOP", true);
         if (device_loop) {
             // the whole iteration loop as ONE graph launch: a conditional WHILE
             // node re-runs the captured iteration until k_loop_ctl clears it
@@ -1032,8 +953,15 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     }
 }
 
+std::vector<std::string> Solver::warnings() const {
+    std::vector<std::string> w = h.warnings;
+    if (!cycle_warning.empty()) w.push_back(cycle_warning);
+    return w;
+}
+
 void Solver::vcycle(const double* d_r, double* d_x, const CycleConfig& cc) {
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "vcycle: setup not run");
+    cycle_warning = check_cycle(cc);
     if (n_) PB_CUDA(cudaMemcpyAsync(r_.get(), d_r, 8 * n_, cudaMemcpyDeviceToDevice, s_));
     double* out = nullptr;
     const bool t = timing;

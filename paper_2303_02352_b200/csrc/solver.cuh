@@ -30,12 +30,11 @@ struct FcgState {
     int status;                      // 0 ok, 1 breakdown
 };
 
-// Timed kernel classes (level 0): 0 plain l1-Jacobi sweep, 1 residual,
-// 2 SpMV + dot triple, 3 FCG vector update, 4 fused zero-start sweep,
-// 5 fused prolongation sweep; kLevelClass + k: level k's own V-cycle work
-// (everything between entering level k and leaving it, minus level k+1's
-// cycle; two intervals per V-cycle), for k < kTimedLevels.
-constexpr int kLevelClass = 6;
+// Timed kernel classes (level 0): 0 l1-Jacobi sweep, 1 residual,
+// 2 SpMV + dot triple, 3 FCG vector update; kLevelClass + k: level k's own
+// V-cycle work (everything between entering level k and leaving it, minus
+// level k+1's cycle; two intervals per V-cycle), for k < kTimedLevels.
+constexpr int kLevelClass = 4;
 constexpr int kTimedLevels = 16;
 constexpr int kNumClasses = kLevelClass + kTimedLevels;
 
@@ -57,20 +56,23 @@ public:
                bool precflag, pairamg_solve_stats* st);
     void vcycle(const double* d_r, double* d_x, const CycleConfig& cc);
     void spmv(int level, const double* d_x, double* d_y);
+    // Hierarchy::warnings plus validate_cycle_config's (cycle.cpp:7-13) for
+    // the cycle configuration of the last solve / V-cycle.
+    std::vector<std::string> warnings() const;
 
     Runtime& rt;
     Hierarchy h;
     bool ready = false;
     bool timing = false;
-    bool fuse = true;     // fused zero-start / prolongation sweeps on halo-free levels
     bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
     bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
-    bool bnd_on_comm = true;  // halo boundary rows computed on the comm stream behind the receive
+    bool p2p_ = true;         // NVLink direct-store exchanges (else NCCL)
     int halo_grid_ = 0;       // CTA cap of interior kernels on halo levels (0 = uncapped)
     P2PGather dots_gather_;   // NVLink allgather of the per-iteration dot partials
     P2PSegGather rep_gather_; // NVLink gather of the first replicated level's right-hand side
     std::array<KernelClassTiming, kNumClasses> ktime{};
     int64_t last_launches = 0;
+    std::string cycle_warning;
 
 private:
     // enqueue helpers (host-side pointer bookkeeping; graph-capturable)
@@ -79,7 +81,6 @@ private:
     void apply(int k, const SellOpArgs& o, int kclass);
     void apply_on(Level& L, const SellOpArgs& o, int kclass);
     void exchange(Level& L, const double* x, cudaStream_t st);
-    bool fusable(int k);
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
@@ -93,7 +94,6 @@ private:
     void begin_time(int kclass);
     void end_time(int kclass);
     void collect_times();
-    bool nccl_free_iteration();
     void destroy_graph();
 
     cudaStream_t s_;
@@ -124,11 +124,6 @@ private:
     std::array<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>, kNumClasses> tev_{};
     std::array<int, kNumClasses> tcount_{};
     std::array<int, kNumClasses> topen_{};
-    // PAIRAMG_HALO_TRACE (timing mode): per level-0 halo sweep, events at
-    // {compute start, comm start, exchange done, boundary done, interior done}
-    std::vector<std::array<cudaEvent_t, 5>> htrace_;
-    int hcount_ = 0;
-    void hrec(cudaEvent_t e, cudaStream_t st);
     int64_t launches_ = 0;
 };
 

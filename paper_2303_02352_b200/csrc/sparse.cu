@@ -1,9 +1,9 @@
 // sparse.cu -- distributed sparse primitives on one rank's device data:
-// localization + halo plans (dist.cpp:158-233), halo exchange (the sends /
-// receives of spmv_dist, dist.cpp:255-275), SELL-32 construction, the
-// SELL apply kernels (spmv_dist row loop dist.cpp:277-300, the l1-Jacobi
-// update cycle.cpp:96-100, the V-cycle residual cycle.cpp:141-143) and the
-// l1 diagonal (cycle.cpp:55-75).
+// localization + halo plans (dist.cpp:45-120), halo exchange (the sends /
+// receives of spmv_dist, dist.cpp:142-162), SELL-32 construction, the
+// SELL apply kernels (spmv_dist row loop dist.cpp:164-187, the l1-Jacobi
+// update cycle.cpp:56-60, the V-cycle residual cycle.cpp:101-103) and the
+// l1 diagonal (cycle.cpp:15-35).
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -88,7 +88,7 @@ __global__ void k_pack_pair(const int32_t* __restrict__ idx, int64_t m, const in
     }
 }
 
-// l1_diagonal_dist (cycle.cpp:55-75): d_i = a_ii + sum_{j != i} |a_ij| in CSR order.
+// l1_diagonal_dist (cycle.cpp:15-35): d_i = a_ii + sum_{j != i} |a_ij| in CSR order.
 __global__ void k_l1(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                      const double* __restrict__ val, int64_t n, double* __restrict__ d,
                      unsigned long long* __restrict__ zero_row) {
@@ -147,7 +147,7 @@ void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gco
         fail(PAIRAMG_INVALID_ARGUMENT, "local nnz exceeds int32 column-slot range; use more ranks");
     const int64_t b = M.row_begin, e = M.starts[r + 1];
 
-    // build_rows_to_receive (dist.cpp:158-168): sorted unique off-range ids.
+    // build_rows_to_receive (dist.cpp:45-55): sorted unique off-range ids.
     HaloPlan& H = M.halo;
     {
         DBuf<int64_t> off(static_cast<size_t>(std::max<int64_t>(nnz, 1)), s);
@@ -195,7 +195,7 @@ void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gco
     M.val = std::move(val);
     gcol.reset();
 
-    // exchange_requests (dist.cpp:180-204): tell owners what we need.
+    // exchange_requests (dist.cpp:67-91): tell owners what we need.
     H.recv_peers.clear();
     H.recv_off.assign(1, 0);
     H.send_peers.clear();
@@ -235,7 +235,7 @@ void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gco
             PB_CUDA(cudaMemcpyAsync(H.send_idx.get(), sidx.data(), 4 * sidx.size(), cudaMemcpyHostToDevice, s));
     }
 
-    // boundary / interior rows (build_spmv_plan, dist.cpp:222-231)
+    // boundary / interior rows (build_spmv_plan, dist.cpp:109-118)
     M.n_boundary = 0;
     M.boundary_rows.reset();
     M.interior_rows.reset();

@@ -80,7 +80,7 @@ s.set_kernel_timing(False)
 sizes = s.level_sizes()
 lines = [f"rank {rank}: timed solve {r.t_solve_s * 1e3 / r.iterations:.3f} ms/iter"]
 for k in range(min(len(sizes), 16)):
-    t = s.kernel_timing(6 + k)
+    t = s.kernel_timing(4 + k)
     if t["launches"]:
         lines.append(f"  level {k} rows {sizes[k][0]:>10d}: {t['ms'] / r.iterations * 1e3:8.1f} us/iter own work")
 for k, name in enumerate(["L0 sweep", "L0 resid", "L0 spmv+dots", "update", "L0 zs-sweep", "L0 prolong-sweep"]):

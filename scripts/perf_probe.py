@@ -33,7 +33,7 @@ def run(stencil, nd, reps=2):
     s.set_kernel_timing(True)
     u = torch.zeros(n, dtype=torch.float64, device="cuda")
     st2 = s.solve(b, u)
-    kt = [s.kernel_timing(k) for k in range(6)]
+    kt = [s.kernel_timing(k) for k in range(4)]
     print(f"{stencil}pt {nd}^3 gen={tg:.3f}s setup={ts:.3f}s ({ {k: round(v, 4) if isinstance(v, float) else v for k, v in st_.items()} }) "
           f"levels={s.level_sizes()} iters={st.iterations} relres={st.final_relres:.3e} solve={st.t_solve_s*1e3:.2f}ms "
           f"ms/iter={st.t_solve_s*1e3/st.iterations:.3f} launches={s.launch_count()}")

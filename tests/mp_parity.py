@@ -44,7 +44,8 @@ def main():
         b0, b1 = int(starts[rank]), int(starts[rank + 1])
         rp, ci, va = pb.poisson(st, nx, ny, nz, b0, b1)
         s = pb.Solver(rt)
-        s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, target, 40))
+        s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, target, 40, setup_overlap=os.environ.get(
+            "PAIRAMG_MP_SETUP_OVERLAP") == "1"))
         mine = {"levels": [s.level(k) for k in range(s.num_levels)],
                 "P": [s.prolongator(k) for k in range(1, s.num_levels)],
                 "M": [s.matching(t) for t in range(s.num_matchings)],

@@ -47,7 +47,7 @@ def test_every_declared_symbol_exported(lib):
 def test_status_names(lib):
     import paper_2303_02352_b200 as pb
 
-    assert pb.lib().pairamg_abi_version() == 1
+    assert pb.lib().pairamg_abi_version() == 2
     for i, name in enumerate(pb.ERROR_NAMES):
         assert lib.pairamg_status_name(i).decode() == name
 

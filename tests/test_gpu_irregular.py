@@ -47,22 +47,17 @@ def runtime():
     return pb.Runtime(0, 0, 1)
 
 
-FORMATS = {
-    "auto": {},
-    "pat": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "1"},
-    "dict": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0"},
-    "plain": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_DICT": "0"},
-    "coded": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0", "PAIRAMG_SELL_PAIRS": "0"},
-}
+# pairamg_setup_config::storage; a forced format falls back to PLAIN where it cannot encode the rows
+FORMATS = ["auto", "pat", "dict", "plain", "coded"]
 
 
-def check_pair(runtime, rp, ci, va, target, s_exp=3, all_levels=False):
+def check_pair(runtime, rp, ci, va, target, s_exp=3, all_levels=False, storage="auto"):
     import paper_2303_02352_b200 as pb
 
     orc = oracle.Oracle("restatement", csr=(rp, ci, va), nranks=1, coarse_size_target=target,
                         aggregation_exponent=s_exp, matching_mode=1).setup()
     s = pb.Solver(runtime)
-    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(s_exp, target, 40))
+    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(s_exp, target, 40, storage=storage))
     assert s.level_sizes() == orc.level_sizes()
     for k in range(orc.num_levels):
         for name, x, y in zip(["row_ptr", "col", "val", "w", "l1"], s.level(k), orc.level(k)):
@@ -80,24 +75,20 @@ def check_pair(runtime, rp, ci, va, target, s_exp=3, all_levels=False):
     return fmts if all_levels else fmts[0]
 
 
-@pytest.mark.parametrize("fmt", sorted(FORMATS))
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("seed", [0, 1])
-def test_random_spd(runtime, fmt, seed, monkeypatch):
-    for k, v in FORMATS[fmt].items():
-        monkeypatch.setenv(k, v)
+def test_random_spd(runtime, fmt, seed):
     rng = np.random.default_rng(100 + seed)
     rp, ci, va, _ = random_spd(300 + 50 * seed, 0.03, rng)
     # random values: DICT/PAT/STEN do not apply and the builder must fall back
     # to PLAIN whatever is requested
-    assert check_pair(runtime, rp, ci, va, target=20, s_exp=2) == "plain"
+    assert check_pair(runtime, rp, ci, va, target=20, s_exp=2, storage=fmt) == "plain"
 
 
-@pytest.mark.parametrize("fmt", sorted(FORMATS))
-def test_variable_coefficient_poisson(runtime, fmt, monkeypatch):
-    for k, v in FORMATS[fmt].items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("fmt", FORMATS)
+def test_variable_coefficient_poisson(runtime, fmt):
     rp, ci, va = varcoef7(12, np.random.default_rng(5))
-    check_pair(runtime, rp, ci, va, target=200)
+    check_pair(runtime, rp, ci, va, target=200, storage=fmt)
 
 
 def test_scaled_poisson_keeps_sten(runtime):
@@ -123,10 +114,8 @@ def test_odd_grid_coarse_levels_coded(runtime):
 
 
 @pytest.mark.parametrize("fmt", ["auto", "coded"])
-def test_random_pattern_few_values(runtime, fmt, monkeypatch):
+def test_random_pattern_few_values(runtime, fmt):
     """Random sparsity with quantised values: CODED at level 0."""
-    for k, v in FORMATS[fmt].items():
-        monkeypatch.setenv(k, v)
     rng = np.random.default_rng(7)
     n = 400
     A = np.zeros((n, n))
@@ -141,5 +130,6 @@ def test_random_pattern_few_values(runtime, fmt, monkeypatch):
         ci.extend(nz.tolist())
         va.extend(A[i, nz].tolist())
         rp.append(len(ci))
-    fmts = check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=20, s_exp=2, all_levels=True)
+    fmts = check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=20, s_exp=2, all_levels=True,
+                      storage=fmt)
     assert fmts[0] == "coded", fmts

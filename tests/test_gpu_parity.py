@@ -37,7 +37,7 @@ def runtime():
     return pb.Runtime(0, 0, 1)
 
 
-def build_pair(runtime, stencil, nx, ny, nz, target=None):
+def build_pair(runtime, stencil, nx, ny, nz, target=None, storage="auto"):
     import paper_2303_02352_b200 as pb
 
     nd = max(nx, ny, nz)
@@ -46,7 +46,7 @@ def build_pair(runtime, stencil, nx, ny, nz, target=None):
                         coarse_size_target=target, matching_mode=1).setup()
     rp, ci, va = orc.input_csr()
     s = pb.Solver(runtime)
-    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(3, target, 40))
+    s.setup(len(rp) - 1, [0, len(rp) - 1], rp, ci, va, cfg=pb.SetupConfig(3, target, 40, storage=storage))
     return orc, s
 
 
@@ -83,21 +83,14 @@ def test_spmv_and_vcycle_bitexact(runtime, case):
     np.testing.assert_array_equal(bits(s.vcycle(r)), bits(orc.vcycle(r)))
 
 
-FORMATS = {  # solve-time storage of every level (csrc/sell.cu): all must be bit-identical
-    "sten": {"PAIRAMG_SELL_STEN": "1"},
-    "pat": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "1"},
-    "dict": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0"},
-    "plain": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_DICT": "0"},
-    "coded": {"PAIRAMG_SELL_STEN": "0", "PAIRAMG_SELL_PAT": "0", "PAIRAMG_SELL_PAIRS": "0"},
-}
+# solve-time storage of every level (csrc/sell.cu, pairamg_setup_config::storage): all must be bit-identical
+FORMATS = ["sten", "pat", "dict", "plain", "coded"]
 
 
-@pytest.mark.parametrize("fmt", sorted(FORMATS))
+@pytest.mark.parametrize("fmt", FORMATS)
 @pytest.mark.parametrize("case", [CASES[1], CASES[3], CASES[4]], ids=lambda c: f"{c[0]}pt-{c[1]}x{c[2]}x{c[3]}")
-def test_storage_formats_bitexact(runtime, case, fmt, monkeypatch):
-    for k, v in FORMATS[fmt].items():
-        monkeypatch.setenv(k, v)
-    orc, s = build_pair(runtime, *case)
+def test_storage_formats_bitexact(runtime, case, fmt):
+    orc, s = build_pair(runtime, *case, storage=fmt)
     assert s.level_storage(0) == fmt
     rng = np.random.default_rng(11)
     for k in range(orc.num_levels):

@@ -13,14 +13,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-ALT = {"PAIRAMG_FUSED_PUSH": "0", "PAIRAMG_SETUP_OVERLAP": "1", "PAIRAMG_GRAPH_LOOP_MR": "1"}
+ALT = {"PAIRAMG_MP_SETUP_OVERLAP": "1"}
 
 
 @pytest.mark.parametrize("world,overlap", [(2, 1), (2, 0), (2, 2), (4, 1)])
 def test_distributed_parity(world, overlap):
     """overlap=0: exchange-then-compute over the whole level (one Sell with halo columns);
-    overlap=2: the non-default paths (separate push launch, setup exchange
-    overlapped with R / composition, device-side FCG loop across ranks)."""
+    overlap=2: setup exchange overlapped with R / composition (setup_overlap)."""
     if gpu_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
