@@ -167,6 +167,15 @@ int pairamg_abi_version(void);
 /* ---- runtime (spawn_ranks / RankCtx, runtime.hpp:71-136) ---- */
 /* 128-byte NCCL unique id, to be broadcast to every rank by the caller. */
 pairamg_status pairamg_comm_unique_id(uint8_t id[128]);
+/* spawn_ranks analogue (runtime.cpp:92-152): a 128-byte id for ranks that are
+ * threads of ONE process.  Passed to pairamg_runtime_create by every rank
+ * thread, it joins them through an in-process hub instead of NCCL: host
+ * collectives meet in shared memory (with the reference's deadlock timeout,
+ * PAIRAMG_DEADLOCK), device data moves by peer copies and the solve-path
+ * exchanges by the same P2P store/flag kernels as across processes.  Ranks
+ * may share one GPU (device argument equal), e.g. to run a multi-rank setup
+ * and solve on a single B200. */
+pairamg_status pairamg_comm_local_id(uint8_t id[128]);
 /* nranks == 1: id may be NULL and no communicator is created. */
 pairamg_status pairamg_runtime_create(int device, int rank, int nranks, const uint8_t* id,
                                       pairamg_runtime** out);

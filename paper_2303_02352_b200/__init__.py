@@ -28,6 +28,7 @@ ERROR_NAMES = [
 EXPORTS = [
     "pairamg_default_setup_config", "pairamg_default_cycle_config", "pairamg_default_solve_config",
     "pairamg_status_name", "pairamg_last_error", "pairamg_abi_version", "pairamg_comm_unique_id",
+    "pairamg_comm_local_id",
     "pairamg_runtime_create", "pairamg_runtime_destroy", "pairamg_solver_create", "pairamg_solver_destroy",
     "pairamg_setup", "pairamg_setup_device", "pairamg_solve", "pairamg_solve_device", "pairamg_vcycle",
     "pairamg_spmv", "pairamg_hierarchy_info", "pairamg_level_info", "pairamg_level_storage", "pairamg_level_export",
@@ -143,6 +144,7 @@ def lib() -> C.CDLL:
         "pairamg_last_error": ([], C.c_char_p),
         "pairamg_abi_version": ([], C.c_int),
         "pairamg_comm_unique_id": ([vp], st),
+        "pairamg_comm_local_id": ([vp], st),
         "pairamg_runtime_create": ([C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)], st),
         "pairamg_runtime_destroy": ([vp], st),
         "pairamg_solver_create": ([vp, C.POINTER(vp)], st),
@@ -206,6 +208,52 @@ def unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().pairamg_comm_unique_id(buf))
     return bytes(buf)
+
+
+def local_id() -> bytes:
+    """Join id for ranks that are threads of this process (pairamg_comm_local_id)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().pairamg_comm_local_id(buf))
+    return bytes(buf)
+
+
+def spawn_ranks(nranks: int, program, devices=None, timeout: float = 900.0):
+    """spawn_ranks (runtime.hpp:113-136): run ``program(rt)`` on ``nranks``
+    threads of this process, one Runtime each (LOCAL transport; all on GPU 0
+    unless ``devices`` lists one per rank).  Returns the per-rank results in
+    rank order; the first rank failure is re-raised as "rank r: ..." like the
+    reference (runtime.cpp:139-151).  Ranks sharing a GPU need
+    CUDA_MODULE_LOADING=EAGER in the environment before CUDA is initialised."""
+    import threading
+
+    uid = local_id()
+    devices = devices or [0] * nranks
+    out, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        rt = None
+        try:
+            rt = Runtime(devices[r], r, nranks, uid)
+            out[r] = program(rt)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+        finally:
+            if rt is not None:
+                rt.close()
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    if any(t.is_alive() for t in ts):
+        raise PairamgError(7, "spawn_ranks: a rank thread did not finish (deadlock)")
+    for r, e in enumerate(err):
+        if e is not None:
+            if isinstance(e, PairamgError):
+                raise PairamgError(e.status, f"rank {r}: {e}") from e
+            raise RuntimeError(f"rank {r}: {e}") from e
+    return out
 
 
 def read_matrix_market(path: str, row_begin: int = 0, row_end: int | None = None):

@@ -224,6 +224,13 @@ const char* pairamg_status_name(pairamg_status s) {
 const char* pairamg_last_error(void) { return g_err.c_str(); }
 int pairamg_abi_version(void) { return PAIRAMG_B200_ABI_VERSION; }
 
+pairamg_status pairamg_comm_local_id(uint8_t id[128]) {
+    return guarded([&] {
+        if (!id) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null id");
+        pb::make_local_id(id);
+    });
+}
+
 pairamg_status pairamg_comm_unique_id(uint8_t id[128]) {
     return guarded([&] {
         ncclUniqueId uid;

@@ -84,8 +84,35 @@ __global__ void __launch_bounds__(256) k_p2p_pull(const double* staging, const u
     }
 }
 
+// A device buffer as another rank can map it: a CUDA IPC handle across
+// processes, the raw pointer between the threads of one process (LOCAL
+// runtimes; same or peer-enabled device).
+struct SharedBuf {
+    cudaIpcMemHandle_t h;
+    void* raw;
+};
+
+bool export_buf(const Runtime& rt, void* p, SharedBuf& out) {
+    out.raw = p;
+    if (rt.local()) return true;
+    return cudaIpcGetMemHandle(&out.h, p) == cudaSuccess;
+}
+
+bool import_buf(const Runtime& rt, const SharedBuf& in, void** out, std::vector<void*>& opened) {
+    if (rt.local()) {
+        *out = in.raw;
+        return true;
+    }
+    if (cudaIpcOpenMemHandle(out, in.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    opened.push_back(*out);
+    return true;
+}
+
 struct Blob {
-    cudaIpcMemHandle_t staging, flags;
+    SharedBuf staging, flags;
     int64_t n_halo;
     int32_t nrecv;
     int32_t recv_rank[kMaxPeers];
@@ -116,8 +143,7 @@ void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s) {
         local_ok = cudaMalloc(&P.staging, 16 * static_cast<size_t>(std::max<int64_t>(H.n_halo, 1))) == cudaSuccess &&
                    cudaMalloc(&P.flags, 8 * static_cast<size_t>(rt.nranks())) == cudaSuccess &&
                    cudaMemset(P.flags, 0, 8 * static_cast<size_t>(rt.nranks())) == cudaSuccess &&
-                   cudaIpcGetMemHandle(&mine.staging, P.staging) == cudaSuccess &&
-                   cudaIpcGetMemHandle(&mine.flags, P.flags) == cudaSuccess;
+                   export_buf(rt, P.staging, mine.staging) && export_buf(rt, P.flags, mine.flags);
         cudaGetLastError();
     }
     mine.n_halo = local_ok ? H.n_halo : -1;  // -1: this rank cannot take part
@@ -139,18 +165,10 @@ void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s) {
                 if (q.recv_rank[k] == rt.rank()) off = q.recv_off[k];
             void* st = nullptr;
             void* fl = nullptr;
-            if (off < 0 || cudaIpcOpenMemHandle(&st, q.staging, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            if (off < 0 || !import_buf(rt, q.staging, &st, P.opened) || !import_buf(rt, q.flags, &fl, P.opened)) {
                 ok = false;
-                cudaGetLastError();
                 break;
             }
-            P.opened.push_back(st);
-            if (cudaIpcOpenMemHandle(&fl, q.flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                ok = false;
-                cudaGetLastError();
-                break;
-            }
-            P.opened.push_back(fl);
             P.peer_staging.push_back(static_cast<double*>(st) + off);
             P.peer_stride.push_back(q.n_halo);
             P.peer_flag.push_back(static_cast<unsigned long long*>(fl) + rt.rank());
@@ -293,15 +311,14 @@ void p2p_gather_setup(Runtime& rt, P2PGather& G, int kmax, cudaStream_t s) {
     G.rank = rt.rank();
     G.kmax = kmax;
     struct GBlob {
-        cudaIpcMemHandle_t mail, flags;
+        SharedBuf mail, flags;
         int32_t ok;
     } mine;
     std::memset(&mine, 0, sizeof mine);
     const size_t mbytes = 8 * 2 * static_cast<size_t>(G.nranks) * kmax;
     mine.ok = cudaMalloc(&G.mail, mbytes) == cudaSuccess && cudaMalloc(&G.flags, 8 * G.nranks) == cudaSuccess &&
               cudaMemset(G.flags, 0, 8 * G.nranks) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.mail, G.mail) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.flags, G.flags) == cudaSuccess;
+              export_buf(rt, G.mail, mine.mail) && export_buf(rt, G.flags, mine.flags);
     cudaGetLastError();
     const std::vector<uint8_t> all = rt.allgather_bytes(&mine, sizeof mine);
     std::vector<GBlob> blobs(static_cast<size_t>(G.nranks));
@@ -316,14 +333,11 @@ void p2p_gather_setup(Runtime& rt, P2PGather& G, int kmax, cudaStream_t s) {
         }
         void* m = nullptr;
         void* f = nullptr;
-        if (cudaIpcOpenMemHandle(&m, blobs[static_cast<size_t>(r)].mail, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-            cudaIpcOpenMemHandle(&f, blobs[static_cast<size_t>(r)].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
+        if (!import_buf(rt, blobs[static_cast<size_t>(r)].mail, &m, G.opened) ||
+            !import_buf(rt, blobs[static_cast<size_t>(r)].flags, &f, G.opened)) {
             ok = false;
             break;
         }
-        G.opened.push_back(m);
-        G.opened.push_back(f);
         G.peer_mail.push_back(static_cast<double*>(m));
         G.peer_flags.push_back(static_cast<unsigned long long*>(f));
     }
@@ -419,14 +433,13 @@ void p2p_seg_setup(Runtime& rt, P2PSegGather& G, int64_t total, cudaStream_t s) 
     G.rank = rt.rank();
     G.total = total;
     struct SBlob {
-        cudaIpcMemHandle_t buf, flags;
+        SharedBuf buf, flags;
         int32_t ok;
     } mine;
     std::memset(&mine, 0, sizeof mine);
     mine.ok = cudaMalloc(&G.buf, 8 * static_cast<size_t>(std::max<int64_t>(total, 1))) == cudaSuccess &&
               cudaMalloc(&G.flags, 8 * G.nranks) == cudaSuccess && cudaMemset(G.flags, 0, 8 * G.nranks) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.buf, G.buf) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.flags, G.flags) == cudaSuccess;
+              export_buf(rt, G.buf, mine.buf) && export_buf(rt, G.flags, mine.flags);
     cudaGetLastError();
     const std::vector<uint8_t> all = rt.allgather_bytes(&mine, sizeof mine);
     std::vector<SBlob> blobs(static_cast<size_t>(G.nranks));
@@ -441,14 +454,11 @@ void p2p_seg_setup(Runtime& rt, P2PSegGather& G, int64_t total, cudaStream_t s) 
         }
         void* m = nullptr;
         void* f = nullptr;
-        if (cudaIpcOpenMemHandle(&m, blobs[static_cast<size_t>(r)].buf, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-            cudaIpcOpenMemHandle(&f, blobs[static_cast<size_t>(r)].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
+        if (!import_buf(rt, blobs[static_cast<size_t>(r)].buf, &m, G.opened) ||
+            !import_buf(rt, blobs[static_cast<size_t>(r)].flags, &f, G.opened)) {
             ok = false;
             break;
         }
-        G.opened.push_back(m);
-        G.opened.push_back(f);
         G.peer_buf.push_back(static_cast<double*>(m));
         G.peer_flags.push_back(static_cast<unsigned long long*>(f));
     }

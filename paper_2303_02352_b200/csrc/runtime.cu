@@ -1,9 +1,132 @@
-// runtime.cu -- NCCL-backed rank runtime (see runtime.cuh).
+// runtime.cu -- NCCL-backed and in-process (LOCAL) rank runtimes (see runtime.cuh).
 #include "runtime.cuh"
 
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <string>
+
+#include <cuda.h>
+#include <unistd.h>
 
 namespace pb {
+
+// ---- LOCAL transport: the in-process hub (spawn_ranks, runtime.cpp:92-152) ----
+
+namespace {
+constexpr char kLocalMagic[16] = "PAIRAMG-LOCAL-1";
+}
+
+bool is_local_id(const uint8_t* id) { return id && std::memcmp(id, kLocalMagic, sizeof kLocalMagic) == 0; }
+
+void make_local_id(uint8_t id[128]) {
+    static std::atomic<uint64_t> seq{0};
+    std::memset(id, 0, 128);
+    std::memcpy(id, kLocalMagic, sizeof kLocalMagic);
+    const uint64_t v[3] = {static_cast<uint64_t>(getpid()), seq.fetch_add(1) + 1, std::random_device{}()};
+    std::memcpy(id + 16, v, sizeof v);
+}
+
+struct LocalHub {
+    int nranks = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    int joined = 0;
+    bool aborted = false;
+    std::string why;
+    std::vector<const void*> slot;
+
+    // Generation barrier with the reference's deadlock semantics: a peer
+    // that never arrives (or left) fails the wait instead of hanging.
+    void wait_all(int rank) {
+        static const int timeout_s = env_int("PAIRAMG_LOCAL_TIMEOUT_S", 600);
+        std::unique_lock<std::mutex> lk(m);
+        if (aborted) fail(PAIRAMG_DEADLOCK, "rank " + std::to_string(rank) + ": " + why);
+        const uint64_t g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(timeout_s), [&] { return gen != g || aborted; })) {
+            aborted = true;
+            why = "collective timed out after " + std::to_string(timeout_s) + " s (a peer rank never arrived)";
+            cv.notify_all();
+        }
+        if (gen == g) fail(PAIRAMG_DEADLOCK, "rank " + std::to_string(rank) + ": " + why);
+    }
+    void abort(const std::string& w) {
+        std::lock_guard<std::mutex> lk(m);
+        if (!aborted) {
+            aborted = true;
+            why = w;
+        }
+        cv.notify_all();
+    }
+};
+
+namespace {
+std::mutex g_hubs_m;
+std::map<std::string, std::weak_ptr<LocalHub>> g_hubs;
+
+std::shared_ptr<LocalHub> join_hub(const uint8_t* id, int nranks) {
+    const std::string key(reinterpret_cast<const char*>(id), 128);
+    std::lock_guard<std::mutex> lk(g_hubs_m);
+    std::shared_ptr<LocalHub> h = g_hubs[key].lock();
+    if (!h) {
+        h = std::make_shared<LocalHub>();
+        h->nranks = nranks;
+        h->slot.assign(static_cast<size_t>(nranks), nullptr);
+        g_hubs[key] = h;
+    }
+    if (h->nranks != nranks) fail(PAIRAMG_INVALID_ARGUMENT, "runtime: ranks of one local id disagree on nranks");
+    if (++h->joined == nranks) g_hubs.erase(key);  // every rank holds it now
+    return h;
+}
+}  // namespace
+
+// Lazy kernel loading (CUDA 12 default) may synchronise the context at a
+// kernel's first launch; with several ranks in one context, a rank spinning
+// on a peer's halo flag would then deadlock the peer's first launch.
+static bool lazy_module_loading() {
+    using Fn = CUresult (*)(CUmoduleLoadingMode*);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &p, cudaEnableDefault, &q) != cudaSuccess || !p) {
+        cudaGetLastError();
+        return true;  // unknown: assume the default (lazy)
+    }
+    CUmoduleLoadingMode m = CU_MODULE_LAZY_LOADING;
+    if (reinterpret_cast<Fn>(p)(&m) != CUDA_SUCCESS) return true;
+    return m == CU_MODULE_LAZY_LOADING;
+}
+
+const std::vector<const void*>& Runtime::hub_gather(const void* mine) {
+    {
+        std::lock_guard<std::mutex> lk(hub_->m);
+        hub_->slot[static_cast<size_t>(rank_)] = mine;
+    }
+    hub_->wait_all(rank_);
+    return hub_->slot;
+}
+
+void Runtime::hub_release() { hub_->wait_all(rank_); }
+
+void Runtime::barrier() {
+    if (nranks_ == 1) return;
+    if (hub_) {
+        hub_->wait_all(rank_);
+        return;
+    }
+    allreduce_sum_i64(0);
+}
 
 Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
     : device_(device), rank_(rank), nranks_(nranks) {
@@ -23,12 +146,37 @@ Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
     uint64_t threshold = UINT64_MAX;
     PB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     if (nranks > 1) {
-        if (!id) fail(PAIRAMG_INVALID_ARGUMENT, "runtime: NCCL unique id required for nranks > 1");
-        ncclUniqueId uid;
-        static_assert(sizeof(uid.internal) == 128, "NCCL unique id size");
-        std::memcpy(uid.internal, id, 128);
-        PB_NCCL(ncclCommInitRank(&comm_, nranks, uid, rank));
-        warmup();
+        if (!id) fail(PAIRAMG_INVALID_ARGUMENT, "runtime: a unique id (NCCL or local) is required for nranks > 1");
+        if (is_local_id(id)) {
+            hub_ = join_hub(id, nranks);
+            const std::vector<int64_t> devs = allgather_i64(device);
+            for (int r = 0; r < nranks; ++r) {
+                const int d = static_cast<int>(devs[static_cast<size_t>(r)]);
+                if (r != rank && d == device) shared_device_ = true;
+                if (d != device) {  // peer copies and stores between the ranks' GPUs
+                    int can = 0;
+                    PB_CUDA(cudaDeviceCanAccessPeer(&can, device, d));
+                    if (can) {
+                        const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+                        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) PB_CUDA(e);
+                        cudaGetLastError();
+                    }
+                }
+            }
+            if (shared_device_ && lazy_module_loading()) {
+                hub_->abort("lazy module loading with ranks sharing a GPU");
+                fail(PAIRAMG_INVALID_ARGUMENT,
+                     "runtime: ranks sharing one GPU need CUDA_MODULE_LOADING=EAGER (set before the process "
+                     "initialises CUDA): with lazy loading, a rank's first launch of a kernel can wait for a "
+                     "context synchronisation that a peer rank's halo wait blocks");
+            }
+        } else {
+            ncclUniqueId uid;
+            static_assert(sizeof(uid.internal) == 128, "NCCL unique id size");
+            std::memcpy(uid.internal, id, 128);
+            PB_NCCL(ncclCommInitRank(&comm_, nranks, uid, rank));
+            warmup();
+        }
     }
 }
 
@@ -53,6 +201,7 @@ void Runtime::warmup() {
 
 Runtime::~Runtime() {
     cudaSetDevice(device_);
+    if (hub_) hub_->abort("rank " + std::to_string(rank_) + " destroyed its runtime");
     if (comm_) ncclCommDestroy(comm_);
     if (stream_) cudaStreamDestroy(stream_);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
@@ -64,6 +213,12 @@ std::vector<int64_t> Runtime::allgather_i64(int64_t x) {
     stats_.allgathers += 1;
     stats_.collective_messages += nranks_ - 1;
     stats_.collective_bytes += 8 * (nranks_ - 1);
+    if (hub_) {
+        const auto& p = hub_gather(&x);
+        for (int r = 0; r < nranks_; ++r) out[static_cast<size_t>(r)] = *static_cast<const int64_t*>(p[static_cast<size_t>(r)]);
+        hub_release();
+        return out;
+    }
     DBuf<int64_t> d(static_cast<size_t>(nranks_) + 1, stream_);
     PB_CUDA(cudaMemcpyAsync(d.get() + nranks_, &x, 8, cudaMemcpyHostToDevice, stream_));
     PB_NCCL(ncclAllGather(d.get() + nranks_, d.get(), 1, ncclInt64, comm_, stream_));
@@ -79,6 +234,12 @@ std::vector<uint8_t> Runtime::allgather_bytes(const void* data, size_t n) {
         return out;
     }
     stats_.allgathers += 1;
+    if (hub_) {
+        const auto& p = hub_gather(data);
+        for (int r = 0; r < nranks_; ++r) std::memcpy(out.data() + r * n, p[static_cast<size_t>(r)], n);
+        hub_release();
+        return out;
+    }
     DBuf<uint8_t> d(static_cast<size_t>(nranks_ + 1) * n, stream_);
     PB_CUDA(cudaMemcpyAsync(d.get() + nranks_ * n, data, n, cudaMemcpyHostToDevice, stream_));
     PB_NCCL(ncclAllGather(d.get() + nranks_ * n, d.get(), n, ncclUint8, comm_, stream_));
@@ -105,6 +266,20 @@ std::vector<std::vector<int64_t>> Runtime::alltoallv_i64(
     out[rank_] = chunks[rank_];
     if (p == 1) return out;
     stats_.alltoallvs += 1;
+    if (hub_) {
+        const auto& ptr = hub_gather(&chunks);
+        for (int q = 0; q < p; ++q) {
+            if (q == rank_) continue;
+            const auto& theirs = *static_cast<const std::vector<std::vector<int64_t>>*>(ptr[static_cast<size_t>(q)]);
+            out[static_cast<size_t>(q)] = theirs[static_cast<size_t>(rank_)];
+            if (!chunks[static_cast<size_t>(q)].empty()) {
+                stats_.collective_messages += 1;
+                stats_.collective_bytes += 8 * static_cast<int64_t>(chunks[static_cast<size_t>(q)].size());
+            }
+        }
+        hub_release();
+        return out;
+    }
     // counts matrix by allgather (row r = what rank r sends to each rank)
     std::vector<int64_t> mine(p);
     for (int d = 0; d < p; ++d) mine[d] = static_cast<int64_t>(chunks[d].size());
@@ -163,7 +338,71 @@ void Runtime::allgather_f64(const double* send, double* recv, size_t count, cuda
         PB_CUDA(cudaMemcpyAsync(recv, send, count * 8, cudaMemcpyDeviceToDevice, s));
         return;
     }
+    if (hub_) fail(PAIRAMG_INTERNAL, "allgather_f64: LOCAL runtimes use the P2P gathers on the solve path");
     PB_NCCL(ncclAllGather(send, recv, count, ncclDouble, comm_, s));
+}
+
+void Runtime::allgather_dev(const void* send, void* recv, size_t bytes) {
+    if (nranks_ == 1) {
+        if (bytes) PB_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, stream_));
+        PB_CUDA(cudaStreamSynchronize(stream_));
+        return;
+    }
+    stats_.allgathers += 1;
+    if (hub_) {
+        PB_CUDA(cudaStreamSynchronize(stream_));
+        const auto& p = hub_gather(send);
+        for (int r = 0; r < nranks_; ++r)
+            if (bytes)
+                PB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + r * bytes, p[static_cast<size_t>(r)], bytes,
+                                        cudaMemcpyDefault, stream_));
+        PB_CUDA(cudaStreamSynchronize(stream_));
+        hub_release();
+        return;
+    }
+    PB_NCCL(ncclAllGather(send, recv, bytes, ncclChar, comm_, stream_));
+    PB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+namespace {
+struct ExchangeView {
+    const std::vector<int>* to;
+    const std::vector<const void*>* bufs;
+    const std::vector<size_t>* bytes;
+};
+}  // namespace
+
+void Runtime::exchange_dev(const std::vector<int>& send_to, const std::vector<const void*>& sends,
+                           const std::vector<size_t>& send_bytes, const std::vector<int>& recv_from,
+                           const std::vector<void*>& recvs, const std::vector<size_t>& recv_bytes, cudaStream_t s) {
+    for (size_t i = 0; i < send_to.size(); ++i) {
+        stats_.p2p_messages += 1;
+        stats_.p2p_bytes += static_cast<int64_t>(send_bytes[i]);
+    }
+    if (hub_) {
+        PB_CUDA(cudaStreamSynchronize(s));
+        const ExchangeView mine{&send_to, &sends, &send_bytes};
+        const auto& p = hub_gather(&mine);
+        for (size_t i = 0; i < recv_from.size(); ++i) {
+            const ExchangeView& q = *static_cast<const ExchangeView*>(p[static_cast<size_t>(recv_from[i])]);
+            size_t k = 0;
+            while (k < q.to->size() && (*q.to)[k] != rank_) ++k;
+            if (k == q.to->size() || (*q.bytes)[k] != recv_bytes[i])
+                fail(PAIRAMG_INTERNAL, "exchange: unmatched send/recv between ranks " + std::to_string(recv_from[i]) +
+                                           " and " + std::to_string(rank_));
+            if (recv_bytes[i])
+                PB_CUDA(cudaMemcpyAsync(recvs[i], (*q.bufs)[k], recv_bytes[i], cudaMemcpyDefault, s));
+        }
+        PB_CUDA(cudaStreamSynchronize(s));
+        hub_release();
+        return;
+    }
+    PB_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < send_to.size(); ++i)
+        if (send_bytes[i]) PB_NCCL(ncclSend(sends[i], send_bytes[i], ncclChar, send_to[i], comm_, s));
+    for (size_t i = 0; i < recv_from.size(); ++i)
+        if (recv_bytes[i]) PB_NCCL(ncclRecv(recvs[i], recv_bytes[i], ncclChar, recv_from[i], comm_, s));
+    PB_NCCL(ncclGroupEnd());
 }
 
 }  // namespace pb

@@ -684,7 +684,7 @@ SegInfo seg_info(const std::vector<int64_t>& counts) {
     return si;
 }
 
-// Setup-time allgatherv of a device array (padded ncclAllGather + unpad).
+// Setup-time allgatherv of a device array (padded allgather + unpad).
 template <typename T>
 int64_t allgatherv(Runtime& rt, const T* d_local, int64_t count, DBuf<T>& out) {
     cudaStream_t s = rt.stream();
@@ -693,7 +693,7 @@ int64_t allgatherv(Runtime& rt, const T* d_local, int64_t count, DBuf<T>& out) {
     const int64_t total = si.off[si.p - 1] + si.cnt[si.p - 1];
     DBuf<T> send(static_cast<size_t>(std::max<int64_t>(si.max, 1)), s), recv(static_cast<size_t>(std::max<int64_t>(si.max * si.p, 1)), s);
     if (count) PB_CUDA(cudaMemcpyAsync(send.get(), d_local, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
-    PB_NCCL(ncclAllGather(send.get(), recv.get(), sizeof(T) * si.max, ncclChar, rt.nccl(), s));
+    rt.allgather_dev(send.get(), recv.get(), sizeof(T) * si.max);
     out.alloc(static_cast<size_t>(total), s);
     if (si.max) k_unpad<T><<<blocks_for(si.max * si.p, 256), 256, 0, s>>>(recv.get(), si, out.get());
     PB_CHECK_LAUNCH();
@@ -709,7 +709,7 @@ void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* 
     SegInfo si = seg_info(counts);
     (void)offsets;
     if (count) PB_CUDA(cudaMemcpyAsync(sendbuf, d_local, 8 * count, cudaMemcpyDeviceToDevice, s));
-    PB_NCCL(ncclAllGather(sendbuf, recvbuf, static_cast<size_t>(maxcount), ncclDouble, rt.nccl(), s));
+    rt.allgather_f64(sendbuf, recvbuf, static_cast<size_t>(maxcount), s);
     if (maxcount) k_unpad<double><<<blocks_for(maxcount * si.p, 256), 256, 0, s>>>(recvbuf, si, d_out);
     PB_CHECK_LAUNCH();
 }

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kRedThreads)
              const double* v, double* q, double* r, int64_t n,
              const FcgState* st, double* partials, ZeroStart z) {
     pdl_begin();
+    if (st->stop) return;  // multi-rank: r_k already met the stopping test (k_fcg_scalars4)
     const double c = st->c, a = st->a;
     double rr = 0.0;
     // 16-byte vector accesses (all vectors are 256-byte aligned), scalar tail
@@ -268,6 +269,64 @@ __global__ void k_fcg_scalars(const double* g, int p, FcgState* st) {
     st->rho = rho_new;
 }
 
+// Multi-rank form with ONE cross-rank exchange per iteration (
+// SURVEY.md 8c item 2): g holds every rank's (w.r, w.v, w.q, |r_k|^2_local)
+// where r_k is the residual this iteration's V-cycle was applied to.  The
+// stopping test of r_k is evaluated here, one V-cycle late: when it holds
+// (or k = max_iters) the update is skipped (st->stop) and the solve ends with
+// u_k -- the same iterate and count as testing right after update k.
+__global__ void k_fcg_scalars4(const double* g, int p, FcgState* st, double rtol, int max_iters, double* hist) {
+    pdl_begin();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double al = 0.0, be = 0.0, ga = 0.0, rr = 0.0;
+    for (int r = 0; r < p; ++r) {
+        al = dadd(al, g[4 * r + 0]);
+        be = dadd(be, g[4 * r + 1]);
+        ga = dadd(ga, g[4 * r + 2]);
+        rr = dadd(rr, g[4 * r + 3]);
+    }
+    st->rr = rr;
+    const double rel = ddiv(__dsqrt_rn(rr), __dsqrt_rn(st->rr0));
+    if (hist && st->it <= max_iters) hist[st->it] = rel;
+    if (rel < rtol || st->it >= max_iters) {
+        st->stop = 1;
+        return;
+    }
+    st->stop = 0;
+    st->alpha = al;
+    st->beta = be;
+    st->gamma = ga;
+    double rho_new, c;
+    if (st->it == 0) {
+        rho_new = be;
+        c = 0.0;
+    } else {
+        rho_new = dsub(be, ddiv(dmul(ga, ga), st->rho));
+        c = ddiv(ga, st->rho);
+    }
+    if (rho_new == 0.0 || !isfinite(rho_new)) st->status = 1;
+    st->c = c;
+    st->a = ddiv(al, rho_new);
+    st->rho = rho_new;
+    st->it += 1;  // the update of this iteration runs
+}
+
+// Local |r_{k+1}|^2 of the update's block partials into out (no exchange:
+// it travels with the next iteration's dot triple).
+__global__ void __launch_bounds__(kRedThreads) k_rr_local(const double* partials, int G, double* out) {
+    pdl_begin();
+    __shared__ double red[kRedThreads];
+    double s = 0.0;
+    for (int g = threadIdx.x; g < G; g += kRedThreads) s = dadd(s, partials[g]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = dadd(red[threadIdx.x], red[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
 // Device-side stopping test of the graph loop (same operations as the host
 // loop: rel = sqrt(rr)/sqrt(rr0); stop on rel < rtol, max_iters or breakdown).
 __global__ void k_loop_ctl(const FcgState* st, double rtol, int max_iters, double* hist,
@@ -290,6 +349,7 @@ __global__ void k_norm_final(const double* g, int p, FcgState* st, int init) {
         st->rr0 = rr;
         st->it = 0;
         st->status = 0;
+        st->stop = 0;
         st->rho = 0.0;
     } else {
         st->it += 1;
@@ -316,7 +376,8 @@ Solver::Solver(Runtime& r) : rt(r), s_(r.stream()) {
     // spmv_dist's overlap flag (dist.cpp:128-199): interior rows while the
     // halo is in flight (default, as every reference call site) or exchange first
     overlap = env_flag("PAIRAMG_OVERLAP", true);
-    p2p_ = env_flag("PAIRAMG_P2P", true);
+    // LOCAL runtimes (thread ranks) exchange solve-path data by P2P stores only
+    p2p_ = rt.local() || env_flag("PAIRAMG_P2P", true);
     halo_grid_ = kSmCount * 4;
     PB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -511,10 +572,19 @@ void Solver::apply(int k, const SellOpArgs& o, int kc) { apply_on(lvl(k), o, kc)
 // level's P2P plan is up, else NCCL send/recv.
 void Solver::exchange(Level& L, const double* x, cudaStream_t st) {
     double* halo = const_cast<double*>(x) + L.A.n;
-    if (L.p2p.ok)
+    if (L.p2p.ok) {
         p2p_exchange(L.A.halo, L.p2p, x, halo, st);
+        rt.stats().halo_exchanges += 1;
+    }
     else
         halo_exchange(rt, L.A.halo, x, halo, st);
+}
+
+// One launch for interior + boundary rows whose boundary blocks wait for the
+// neighbours' pushes.  Not when ranks share a GPU (LOCAL runtime): a grid
+// whose last blocks wait on a peer's kernel could hold every SM slot.
+bool Solver::split_launch(const Level& L) const {
+    return L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) && !rt.shared_device();
 }
 
 void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
@@ -527,11 +597,11 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         end_time(kc);
         return;
     }
-    if (L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) &&
-        (o.op == kSpmv || o.op == kJacobi || o.op == kResid)) {
+    if (split_launch(L)) {
         // push this rank's boundary values into the neighbours, then one
         // launch whose boundary blocks wait for theirs (no comm stream)
         const HaloSrc hs = p2p_halo_src(L.A.halo, L.p2p);
+        rt.stats().halo_exchanges += 1;
         if (!hs.fused) p2p_push(L.A.halo, L.p2p, o.x, s_);
         sell_apply_split(L.sell_int, L.split_bnd(), o, hs, s_);
         launches_ += hs.fused ? 1 : 2;
@@ -685,10 +755,9 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     out = xc;
 }
 
-void Solver::reduce_dots_enqueue() {
+void Solver::reduce_dots_enqueue(bool fused_norm) {
     const int p = rt.nranks();
     // partial count G is encoded by the producer; it is fixed for the level
-    Level& L0 = *h.levels[0];
     const int G = dots_grid_;  // partial triples written by the SpMV+dots launches
     if (G > kStage) {  // two fixed-order stages: kStage blocks over contiguous chunks, then one block
         launch_k(k_reduce_chunks, kStage, kRedThreads, 0, s_, partials_.get(), G, 3, stage_.get());
@@ -700,14 +769,20 @@ void Solver::reduce_dots_enqueue() {
     }
     PB_CHECK_LAUNCH();
     const double* g = local_.get();
+    const int K = fused_norm ? 4 : 3;  // local_[3] = |r_k|^2 of this rank (k_rr_local / prologue)
     if (p > 1) {
+        rt.stats().device_reductions += 1;
         if (dots_gather_.ok)
-            p2p_allgather(dots_gather_, local_.get(), gathered_.get(), 3, s_);
+            p2p_allgather(dots_gather_, local_.get(), gathered_.get(), K, s_);
         else
-            rt.allgather_f64(local_.get(), gathered_.get(), 3, s_);
+            rt.allgather_f64(local_.get(), gathered_.get(), static_cast<size_t>(K), s_);
         g = gathered_.get();
+        launches_ += 1;
     }
-    launch_k(k_fcg_scalars, 1, 32, 0, s_, g, p, state_.get());
+    if (fused_norm)
+        launch_k(k_fcg_scalars4, 1, 32, 0, s_, g, p, state_.get(), cap_rtol_, cap_maxit_, hist_.get());
+    else
+        launch_k(k_fcg_scalars, 1, 32, 0, s_, g, p, state_.get());
     PB_CHECK_LAUNCH();
     launches_ += 2;
 }
@@ -718,6 +793,7 @@ void Solver::reduce_norm_enqueue(bool init) {
     PB_CHECK_LAUNCH();
     const double* g = local_.get() + 3;
     if (p > 1) {
+        rt.stats().device_reductions += 1;
         if (dots_gather_.ok)
             p2p_allgather(dots_gather_, local_.get() + 3, gathered_.get() + 3 * p, 1, s_);
         else
@@ -772,8 +848,9 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         exchange(L0, w, s_);
         dots_grid_ = sell_spmv_dots(L0.sell_all, w, v_.get(), r_.get(), q_.get(), partials_.get(), max_blocks_, s_);
         launches_ += 2;
-    } else if (L0.p2p.ok && L0.A.halo.n_halo > 0 && sell_split_ok(L0.sell_int, L0.split_bnd())) {
+    } else if (split_launch(L0)) {
         const HaloSrc hs = p2p_halo_src(L0.A.halo, L0.p2p);
+        rt.stats().halo_exchanges += 1;
         if (!hs.fused) p2p_push(L0.A.halo, L0.p2p, w, s_);
         dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.split_bnd(), w, v_.get(), r_.get(), q_.get(), partials_.get(),
                                           max_blocks_, hs, s_);
@@ -807,7 +884,8 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
         launches_ += 1;
     }
     end_time(2);
-    reduce_dots_enqueue();
+    const bool fused_norm = rt.nranks() > 1;
+    reduce_dots_enqueue(fused_norm);
     begin_time(3);
     zs_pending_ = false;
     if (zs)
@@ -819,7 +897,13 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     PB_CHECK_LAUNCH();
     end_time(3);
     launches_ += 1;
-    reduce_norm_enqueue(false);
+    if (fused_norm) {
+        launch_k(k_rr_local, 1, kRedThreads, 0, s_, partials_.get(), red_grid(n_), local_.get() + 3);
+        PB_CHECK_LAUNCH();
+        launches_ += 1;
+    } else {
+        reduce_norm_enqueue(false);
+    }
 }
 
 void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double rtol, int max_iters,
@@ -885,17 +969,25 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     std::vector<double> hist{1.0};
     if (rnorm0 != 0.0) {
         // (re)capture the iteration graph
+        const bool mr = rt.nranks() > 1;  // stopping test inside the graph (k_fcg_scalars4)
         if (!graph_ || graph_cc_.pre_sweeps != cc.pre_sweeps || graph_cc_.post_sweeps != cc.post_sweeps ||
             graph_cc_.coarsest_sweeps != cc.coarsest_sweeps || graph_cc_.relax_weight != cc.relax_weight ||
-            graph_prec_ != precflag || graph_timing_ != timing) {
+            graph_prec_ != precflag || graph_timing_ != timing ||
+            (mr && (cap_rtol_ != rtol || cap_maxit_ != max_iters))) {
             destroy_graph();
+            cap_rtol_ = rtol;
+            cap_maxit_ = max_iters;
+            if (mr) hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
             tcount_.fill(0);
             cudaGraph_t g;
             const int64_t l0 = launches_;
+            const CommStats c0 = rt.stats();
             PB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
             iteration_enqueue(cc, precflag);
             PB_CUDA(cudaStreamEndCapture(s_, &g));
             per_iter_launches_ = launches_ - l0;
+            reductions_per_iter_ = static_cast<int>(rt.stats().device_reductions - c0.device_reductions);
+            halos_per_iter_ = static_cast<int>(rt.stats().halo_exchanges - c0.halo_exchanges);
             launches_ = l0;
             PB_CUDA(cudaGraphInstantiate(&graph_, g, 0));
             PB_CUDA(cudaGraphDestroy(g));
@@ -918,6 +1010,23 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             PB_CUDA(cudaMemcpy(dh.data(), hist_.get(), 8 * (it + 1), cudaMemcpyDeviceToHost));
             for (int i = 1; i <= it; ++i) hist.push_back(dh[static_cast<size_t>(i)]);
             rel = dh[static_cast<size_t>(it)];
+        } else if (mr) {
+            // one launch per iteration; launch j tests r_j (k_fcg_scalars4) and
+            // updates to r_{j+1} unless that test already stopped the solve
+            while (true) {
+                PB_CUDA(cudaGraphLaunch(graph_, s_));
+                launches_ += per_iter_launches_;
+                PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
+                PB_CUDA(cudaStreamSynchronize(s_));
+                collect_times();
+                if (h_state_->status)
+                    fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(h_state_->it));
+                const int j = h_state_->stop ? h_state_->it : h_state_->it - 1;
+                rel = std::sqrt(h_state_->rr) / rnorm0;
+                if (j >= 1) hist.push_back(rel);
+                it = j;
+                if (h_state_->stop) break;
+            }
         } else {
             while (true) {
                 PB_CUDA(cudaGraphLaunch(graph_, s_));
@@ -948,6 +1057,10 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
         st->final_relres = rel;
         st->rnorm0 = rnorm0;
         st->t_solve_s = ms * 1e-3;
+        st->t_h2d_s = 0.0;
+        st->t_d2h_s = 0.0;
+        st->reductions_per_iter = reductions_per_iter_;
+        st->halo_exchanges_per_iter = halos_per_iter_;
         if (st->history)
             for (int i = 0; i < st->history_cap && i < static_cast<int>(hist.size()); ++i) st->history[i] = hist[i];
     }

@@ -28,6 +28,7 @@ struct FcgState {
     double rr, rr0;                  // |r_{i+1}|^2, |r_0|^2
     int it;                          // iterations completed
     int status;                      // 0 ok, 1 breakdown
+    int stop;                        // multi-rank: r_it met the stopping test, no update
 };
 
 // Timed kernel classes (level 0): 0 l1-Jacobi sweep, 1 residual,
@@ -81,13 +82,14 @@ private:
     void apply(int k, const SellOpArgs& o, int kclass);
     void apply_on(Level& L, const SellOpArgs& o, int kclass);
     void exchange(Level& L, const double* x, cudaStream_t st);
+    bool split_launch(const Level& L) const;
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
     bool zs_fused(const CycleConfig& cc, bool precflag);
     ZeroStart zero_start_args(const CycleConfig& cc);
     bool zs_pending_ = false;  // level-0 x1 of the next V-cycle is already formed
-    void reduce_dots_enqueue();
+    void reduce_dots_enqueue(bool fused_norm);
     void reduce_norm_enqueue(bool init_rr0);
     void ensure_vectors();
     void ensure_events(int kclass, int idx);
@@ -118,6 +120,9 @@ private:
     DBuf<double> hist_;
     void ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters);
     int64_t per_iter_launches_ = 0;
+    int reductions_per_iter_ = 0, halos_per_iter_ = 0;  // cross-rank exchanges per FCG iteration
+    double cap_rtol_ = 0.0;  // stopping test captured into the multi-rank iteration graph
+    int cap_maxit_ = 0;
     std::vector<cudaEvent_t> ev_pool_;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     // per-class event pairs recorded in the captured iteration

@@ -274,23 +274,31 @@ void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s) {
 
 void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_halo, cudaStream_t s) {
     if (!H.has_traffic()) return;
+    rt.stats().halo_exchanges += 1;
     const int64_t nsend = H.send_off.back();
     if (nsend) {
         k_pack<<<blocks_for(nsend, 256), 256, 0, s>>>(H.send_idx.get(), nsend, x_owned, H.send_buf.get());
         PB_CHECK_LAUNCH();
     }
-    PB_NCCL(ncclGroupStart());
-    for (size_t i = 0; i < H.send_peers.size(); ++i) {
-        const int64_t c = H.send_off[i + 1] - H.send_off[i];
-        PB_NCCL(ncclSend(H.send_buf.get() + H.send_off[i], static_cast<size_t>(c), ncclDouble, H.send_peers[i],
-                         rt.nccl(), s));
-        rt.stats().p2p_messages += 1;
-        rt.stats().p2p_bytes += 8 * c;
+    if (rt.local()) {
+        cudaStreamCaptureStatus cs;
+        PB_CUDA(cudaStreamIsCapturing(s, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            fail(PAIRAMG_INTERNAL, "halo_exchange: LOCAL runtimes exchange solve-path halos by P2P stores");
     }
-    for (size_t i = 0; i < H.recv_peers.size(); ++i)
-        PB_NCCL(ncclRecv(x_halo + H.recv_off[i], static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]),
-                         ncclDouble, H.recv_peers[i], rt.nccl(), s));
-    PB_NCCL(ncclGroupEnd());
+    std::vector<int> to(H.send_peers.begin(), H.send_peers.end()), from(H.recv_peers.begin(), H.recv_peers.end());
+    std::vector<const void*> sb;
+    std::vector<void*> rb;
+    std::vector<size_t> sn, rn;
+    for (size_t i = 0; i < H.send_peers.size(); ++i) {
+        sb.push_back(H.send_buf.get() + H.send_off[i]);
+        sn.push_back(8 * static_cast<size_t>(H.send_off[i + 1] - H.send_off[i]));
+    }
+    for (size_t i = 0; i < H.recv_peers.size(); ++i) {
+        rb.push_back(x_halo + H.recv_off[i]);
+        rn.push_back(8 * static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]));
+    }
+    rt.exchange_dev(to, sb, sn, from, rb, rn, s);
 }
 
 void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_t* a_halo,
@@ -303,20 +311,38 @@ void halo_exchange_pair(Runtime& rt, HaloPlan& H, const int64_t* a_owned, int64_
                                                            H.send_buf_i64.get(), H.send_buf.get());
         PB_CHECK_LAUNCH();
     }
-    PB_NCCL(ncclGroupStart());
+    // ids then values to every peer (two messages per peer, one exchange)
+    std::vector<int> to, from;
+    std::vector<const void*> sb;
+    std::vector<void*> rb;
+    std::vector<size_t> sn, rn;
     for (size_t i = 0; i < H.send_peers.size(); ++i) {
         const size_t c = static_cast<size_t>(H.send_off[i + 1] - H.send_off[i]);
-        PB_NCCL(ncclSend(H.send_buf_i64.get() + H.send_off[i], c, ncclInt64, H.send_peers[i], rt.nccl(), s));
-        PB_NCCL(ncclSend(H.send_buf.get() + H.send_off[i], c, ncclDouble, H.send_peers[i], rt.nccl(), s));
-        rt.stats().p2p_messages += 1;
-        rt.stats().p2p_bytes += 16 * static_cast<int64_t>(c);
+        to.push_back(H.send_peers[i]);
+        sb.push_back(H.send_buf_i64.get() + H.send_off[i]);
+        sn.push_back(8 * c);
     }
     for (size_t i = 0; i < H.recv_peers.size(); ++i) {
         const size_t c = static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]);
-        PB_NCCL(ncclRecv(a_halo + H.recv_off[i], c, ncclInt64, H.recv_peers[i], rt.nccl(), s));
-        PB_NCCL(ncclRecv(b_halo + H.recv_off[i], c, ncclDouble, H.recv_peers[i], rt.nccl(), s));
+        from.push_back(H.recv_peers[i]);
+        rb.push_back(a_halo + H.recv_off[i]);
+        rn.push_back(8 * c);
     }
-    PB_NCCL(ncclGroupEnd());
+    rt.exchange_dev(to, sb, sn, from, rb, rn, s);
+    to.clear(), from.clear(), sb.clear(), rb.clear(), sn.clear(), rn.clear();
+    for (size_t i = 0; i < H.send_peers.size(); ++i) {
+        const size_t c = static_cast<size_t>(H.send_off[i + 1] - H.send_off[i]);
+        to.push_back(H.send_peers[i]);
+        sb.push_back(H.send_buf.get() + H.send_off[i]);
+        sn.push_back(8 * c);
+    }
+    for (size_t i = 0; i < H.recv_peers.size(); ++i) {
+        const size_t c = static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]);
+        from.push_back(H.recv_peers[i]);
+        rb.push_back(b_halo + H.recv_off[i]);
+        rn.push_back(8 * c);
+    }
+    rt.exchange_dev(to, sb, sn, from, rb, rn, s);
 }
 
 }  // namespace pb

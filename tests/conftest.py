@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# Multi-rank tests run their ranks as threads sharing cuda:0 (pb.spawn_ranks,
+# tests/test_local_ranks.py); that needs every kernel loaded up front -- set
+# before anything initialises CUDA in this process (runtime.cu explains why).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -1,0 +1,148 @@
+"""Multi-rank parity on ONE GPU: ranks are threads of this process
+(pb.spawn_ranks -> the LOCAL runtime, the reference's own spawn_ranks model,
+runtime.cpp:92-152), every rank on cuda:0.
+
+The distributed code paths are the ones the multi-GPU runs take -- halo
+plans (localize / exchange_requests), the P halo exchange of the Galerkin
+product (spmm_dist), per-step coarse partitions (allgather_partition), coarse
+replication, the P2P flag-protocol halo exchange and dot allgather of the
+solve -- with raw pointers instead of CUDA IPC handles.  Every hierarchy
+array, SpMV and V-cycle must equal the oracle at the same partition count bit
+for bit (tests/mp_parity.py), as must the replayed reference matchings on odd
+grids split across ranks.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.mp_parity import CASES, bits, check_case, rank_program
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}pt-{c[1]}x{c[2]}x{c[3]}")
+def test_local_ranks_parity(case, world):
+    import paper_2303_02352_b200 as pb
+
+    allp = pb.spawn_ranks(world, lambda rt: rank_program(rt, case))
+    check_case(case, world, allp)
+
+
+@pytest.mark.parametrize("mode", ["exchange_first", "setup_overlap", "no_replication"])
+def test_local_ranks_schedules(mode, monkeypatch):
+    """The non-default schedules: exchange-then-compute SpMV (spmv_dist overlap=false,
+    dist.cpp:186-190), P's halo exchange overlapped with R / composition, and every
+    level distributed (no coarse replication)."""
+    import paper_2303_02352_b200 as pb
+
+    case = (7, 20, 17, 23)
+    if mode == "exchange_first":
+        monkeypatch.setenv("PAIRAMG_OVERLAP", "0")
+    kw = {"setup_overlap": mode == "setup_overlap", "replicate_rows": 0 if mode == "no_replication" else 2500000}
+    allp = pb.spawn_ranks(2, lambda rt: rank_program(rt, case, **kw))
+    check_case(case, 2, allp)
+
+
+@pytest.mark.parametrize("case,world", [((7, 45, 45, 45), 2), ((7, 33, 31, 29), 3), ((27, 15, 15, 16), 2)],
+                         ids=lambda x: str(x))
+def test_local_ranks_replay_reference(case, world):
+    """Odd grids, several ranks: the UNMODIFIED reference's matchings (oracle/_ref at
+    the same p) replayed through SetupConfig::replay give its hierarchy bit for bit."""
+    import paper_2303_02352_b200 as pb
+
+    st, nx, ny, nz = case
+    n = nx * ny * nz
+    target = 40 * nx
+    ref = oracle.Oracle("reference", stencil=st, nx=nx, ny=ny, nz=nz, nranks=world,
+                        coarse_size_target=target).setup()
+    trace = ref.matchings()
+    starts = pb.uniform_partition(n, world)
+
+    def prog(rt):
+        b0, b1 = int(starts[rt.rank]), int(starts[rt.rank + 1])
+        rp, ci, va = pb.poisson(st, nx, ny, nz, b0, b1)
+        s = pb.Solver(rt)
+        s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, target, 40, replay=trace))
+        out = {"levels": [s.level(k) for k in range(s.num_levels)], "sizes": s.level_sizes(),
+               "vcycle": s.vcycle(np.cos(0.11 * np.arange(n))[b0:b1])}
+        s.close()
+        return out
+
+    allp = pb.spawn_ranks(world, prog)
+    assert [tuple(x) for x in allp[0]["sizes"]] == [tuple(x) for x in ref.level_sizes()]
+    for k in range(ref.num_levels):
+        want = ref.level(k)
+        for i, name in enumerate(["row_ptr", "col", "val", "w", "l1"]):
+            if i == 0:
+                continue  # row_ptr is local per rank; cols/vals/w/l1 concatenate
+            got = np.concatenate([allp[r]["levels"][k][i] for r in range(world)])
+            assert np.array_equal(bits(got), bits(want[i])), f"level {k} {name}"
+    g = np.concatenate([allp[r]["vcycle"] for r in range(world)])
+    assert np.array_equal(bits(g), bits(ref.vcycle(np.cos(0.11 * np.arange(n)))))
+
+
+def test_local_replay_crossing_partition():
+    """A replayed mate owned by another rank is a contract violation (amg.cpp:187-189)."""
+    import paper_2303_02352_b200 as pb
+
+    nx = 8
+    n = nx ** 3
+    starts = pb.uniform_partition(n, 2)
+    bad = np.full(n, -1, np.int64)
+    bad[0], bad[n - 1] = n - 1, 0  # pairs rows of rank 0 and rank 1
+
+    def prog(rt):
+        b0, b1 = int(starts[rt.rank]), int(starts[rt.rank + 1])
+        rp, ci, va = pb.poisson(7, nx, nx, nx, b0, b1)
+        s = pb.Solver(rt)
+        try:
+            s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, 40, 40, replay=[bad]))
+        except pb.PairamgError as e:
+            return e.code, str(e)
+        finally:
+            s.close()
+        return "ok", ""
+
+    out = pb.spawn_ranks(2, prog)
+    assert all(c == "contract_violation" and "crosses the rank partition" in m for c, m in out), out
+
+
+def test_local_deadlock_is_reported():
+    """A rank that leaves while its peers sit in a collective turns the wait into
+    PAIRAMG_DEADLOCK instead of a hang (the reference's timed receive)."""
+    import paper_2303_02352_b200 as pb
+
+    def prog(rt):
+        if rt.rank == 1:
+            return "left"
+        s = pb.Solver(rt)
+        rp, ci, va = pb.poisson(7, 6, 6, 6, 0, 108)
+        try:
+            s.setup(216, [0, 108, 216], rp, ci, va)
+        except pb.PairamgError as e:
+            return e.code
+        finally:
+            s.close()
+        return "ok"
+
+    out = pb.spawn_ranks(2, prog)
+    assert out == ["deadlock", "left"], out
+
+
+def test_lazy_loading_refused_for_shared_gpu():
+    """Ranks sharing a GPU under lazy module loading would risk the documented
+    lazy-loading deadlock: pairamg_runtime_create refuses with a clear message."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import paper_2303_02352_b200 as pb\n"
+            "try:\n"
+            "    pb.spawn_ranks(2, lambda rt: 0)\n"
+            "except pb.PairamgError as e:\n"
+            "    print('REFUSED', e.code, 'EAGER' in str(e))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_MODULE_LOADING="LAZY")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, env=env, timeout=300)
+    assert "REFUSED invalid_argument True" in r.stdout, r.stdout + r.stderr
