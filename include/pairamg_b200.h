@@ -142,6 +142,7 @@ typedef struct pairamg_solve_stats {
      * SPEC.md:477) and halo exchanges per iteration, from CommStats deltas. */
     int reductions_per_iter;
     int halo_exchanges_per_iter;
+    double halo_bytes_per_iter; /* halo values this rank receives per iteration (8 B each) */
 } pairamg_solve_stats;
 
 /* SetupStats (amg.hpp:40-47) plus the hierarchy summary. */
@@ -281,6 +282,19 @@ pairamg_status pairamg_poisson_host(int stencil, int64_t nx, int64_t ny, int64_t
 pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny,
                                       int64_t nz, int64_t row_begin, int64_t row_end,
                                       int64_t* d_row_ptr, int64_t* d_col, double* d_val);
+/* Variable-coefficient workload (no reference counterpart; exercises the
+ * general storage paths): same sparsity as the Poisson operator, cell
+ * coefficients k_c = 1 + (hash(seed, c) mod levels) for levels > 0 (a few
+ * distinct entry values) or continuous in [0.5, 1.5) for levels = 0 (all
+ * distinct); couplings -(k_i + k_j)/2, diagonal = sum over the stencil
+ * directions of (k_i + k_j)/2 with k_i across the Dirichlet boundary. */
+pairamg_status pairamg_varcoef_host(int stencil, int64_t nx, int64_t ny, int64_t nz, int levels,
+                                    uint64_t seed, int64_t row_begin, int64_t row_end,
+                                    int64_t* row_ptr, int64_t* col, double* val);
+pairamg_status pairamg_varcoef_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny,
+                                      int64_t nz, int levels, uint64_t seed, int64_t row_begin,
+                                      int64_t row_end, int64_t* d_row_ptr, int64_t* d_col,
+                                      double* d_val);
 
 /* ---- MatrixMarket ingest / distribute (mm_io.cpp:26-110, csr.cpp:24-54,
  *      dist.cpp:349-363) ---- */

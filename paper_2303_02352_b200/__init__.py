@@ -37,6 +37,7 @@ EXPORTS = [
     "pairamg_solver_stream", "pairamg_poisson_nnz", "pairamg_poisson_host", "pairamg_poisson_device",
     "pairamg_match_graph", "pairamg_mm_open", "pairamg_mm_rows", "pairamg_mm_copy_rows", "pairamg_mm_close",
     "pairamg_mm_write", "pairamg_spgemm", "pairamg_setup_warnings", "pairamg_setup_warning",
+    "pairamg_varcoef_host", "pairamg_varcoef_device",
 ]
 
 STORAGE = {"auto": -1, "plain": 0, "dict": 1, "pat": 2, "sten": 3, "coded": 4}
@@ -98,7 +99,8 @@ class _SolveStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_relres", C.c_double),
                 ("rnorm0", C.c_double), ("t_solve_s", C.c_double), ("history", C.POINTER(C.c_double)),
                 ("history_cap", C.c_int), ("t_h2d_s", C.c_double), ("t_d2h_s", C.c_double),
-                ("reductions_per_iter", C.c_int), ("halo_exchanges_per_iter", C.c_int)]
+                ("reductions_per_iter", C.c_int), ("halo_exchanges_per_iter", C.c_int),
+                ("halo_bytes_per_iter", C.c_double)]
 
 
 class _SetupStats(C.Structure):
@@ -119,6 +121,7 @@ class SolveStats:
     t_d2h_s: float = 0.0
     reductions_per_iter: int = 0
     halo_exchanges_per_iter: int = 0
+    halo_bytes_per_iter: float = 0.0
 
 
 _lib = None
@@ -171,6 +174,8 @@ def lib() -> C.CDLL:
         "pairamg_poisson_nnz": ([C.c_int, i64, i64, i64, i64, i64], i64),
         "pairamg_poisson_host": ([C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
         "pairamg_poisson_device": ([vp, C.c_int, i64, i64, i64, i64, i64, vp, vp, vp], st),
+        "pairamg_varcoef_host": ([C.c_int, i64, i64, i64, C.c_int, C.c_uint64, i64, i64, vp, vp, vp], st),
+        "pairamg_varcoef_device": ([vp, C.c_int, i64, i64, i64, C.c_int, C.c_uint64, i64, i64, vp, vp, vp], st),
         "pairamg_match_graph": ([vp, i64, vp, vp, vp, vp], st),
         "pairamg_mm_open": ([C.c_char_p, C.POINTER(vp), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
         "pairamg_mm_rows": ([vp, i64, i64, C.POINTER(i64)], st),
@@ -323,6 +328,21 @@ def poisson(stencil: int, nx: int, ny: int, nz: int, row_begin: int = 0, row_end
     return rp, ci, va
 
 
+def varcoef(stencil: int, nx: int, ny: int, nz: int, levels: int = 2, seed: int = 1, row_begin: int = 0,
+            row_end: int | None = None):
+    """Owned rows of the variable-coefficient operator (pairamg_varcoef_host):
+    Poisson sparsity, couplings -(k_i + k_j)/2 from hashed cell coefficients."""
+    L = lib()
+    if row_end is None:
+        row_end = nx * ny * nz
+    nnz = L.pairamg_poisson_nnz(stencil, nx, ny, nz, row_begin, row_end)
+    rp = np.empty(row_end - row_begin + 1, np.int64)
+    ci = np.empty(nnz, np.int64)
+    va = np.empty(nnz, np.float64)
+    _check(L.pairamg_varcoef_host(stencil, nx, ny, nz, levels, seed, row_begin, row_end, _ptr(rp), _ptr(ci), _ptr(va)))
+    return rp, ci, va
+
+
 def uniform_partition(n: int, p: int) -> np.ndarray:
     """Partition::uniform (runtime.cpp:13-22)."""
     return np.array([(n // p) * r + min(n % p, r) for r in range(p + 1)], np.int64)
@@ -416,7 +436,7 @@ class Solver:
             _check(lib().pairamg_solve(self.h, _ptr(b), _ptr(u), C.byref(cycle), C.byref(solve_cfg), C.byref(st)))
         return SolveStats(st.iterations, bool(st.converged), st.final_relres, st.rnorm0, st.t_solve_s,
                           hist[: st.iterations + 1].copy(), st.t_h2d_s, st.t_d2h_s, st.reductions_per_iter,
-                          st.halo_exchanges_per_iter)
+                          st.halo_exchanges_per_iter, st.halo_bytes_per_iter)
 
     def vcycle(self, r, cycle: CycleConfig | None = None):
         cycle = cycle or CycleConfig()

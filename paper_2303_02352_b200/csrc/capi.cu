@@ -144,21 +144,53 @@ __host__ __device__ inline int row_len(int stencil, int64_t nx, int64_t ny, int6
     return stencil == 27 ? ax * ay * az : 1 + (ax - 1) + (ay - 1) + (az - 1);
 }
 
+// Variable-coefficient operator (a workload for the general storage paths,
+// no reference counterpart): cell coefficient k_c from a hash of (seed, c) --
+// 1 + (h mod levels) for levels > 0 (few distinct entry values), else a
+// continuous value in [0.5, 1.5) (every value distinct).  Coupling of
+// neighbours i, j: -(k_i + k_j)/2; diagonal: the sum over all stencil
+// directions of (k_i + k_j)/2, with k_i for directions leaving the grid
+// (Dirichlet), in direction order -- an SPD M-matrix.  levels < 0 = Poisson.
+struct Coef {
+    int levels = -1;
+    uint64_t seed = 0;
+};
+
+__host__ __device__ inline double cell_coef(int64_t c, const Coef& cf) {
+    uint64_t z = cf.seed + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(c + 1);  // splitmix64
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    if (cf.levels > 0) return 1.0 + static_cast<double>(z % static_cast<uint64_t>(cf.levels));
+    return 0.5 + static_cast<double>(z >> 11) * 0x1p-53;
+}
+
 __host__ __device__ inline void fill_row(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t row,
-                                         int64_t* col, double* val) {
+                                         int64_t* col, double* val, Coef cf = Coef()) {
     const int64_t i = row % nx, j = (row / nx) % ny, k = row / (nx * ny);
-    int o = 0;
+    const bool var = cf.levels >= 0;
+    const double ki = var ? cell_coef(row, cf) : 0.0;
+    double diag = 0.0;
+    int o = 0, od = 0;
     for (int dk = -1; dk <= 1; ++dk)
         for (int dj = -1; dj <= 1; ++dj)
             for (int di = -1; di <= 1; ++di) {
                 const int man = (di != 0) + (dj != 0) + (dk != 0);
                 if (stencil == 7 && man > 1) continue;
                 const int64_t ii = i + di, jj = j + dj, kk = k + dk;
-                if (ii < 0 || ii >= nx || jj < 0 || jj >= ny || kk < 0 || kk >= nz) continue;
+                const bool in = !(ii < 0 || ii >= nx || jj < 0 || jj >= ny || kk < 0 || kk >= nz);
+                if (var && man > 0) {
+                    const double c = in ? (ki + cell_coef(ii + nx * (jj + ny * kk), cf)) * 0.5 : ki;
+                    diag = diag + c;
+                    if (in) val[o] = -c;
+                }
+                if (!in) continue;
                 col[o] = ii + nx * (jj + ny * kk);
-                val[o] = man == 0 ? (stencil == 27 ? 26.0 : 6.0) : -1.0;
+                if (man == 0) od = o;
+                if (!var) val[o] = man == 0 ? (stencil == 27 ? 26.0 : 6.0) : -1.0;
                 ++o;
             }
+    if (var) val[od] = diag;
 }
 
 __global__ void k_poisson_len(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t m,
@@ -169,9 +201,40 @@ __global__ void k_poisson_len(int stencil, int64_t nx, int64_t ny, int64_t nz, i
 }
 
 __global__ void k_poisson_fill(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t m,
-                               const int64_t* __restrict__ rp, int64_t* __restrict__ col, double* __restrict__ val) {
+                               const int64_t* __restrict__ rp, int64_t* __restrict__ col, double* __restrict__ val,
+                               Coef cf) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r < m) fill_row(stencil, nx, ny, nz, b + r, col + rp[r], val + rp[r]);
+    if (r < m) fill_row(stencil, nx, ny, nz, b + r, col + rp[r], val + rp[r], cf);
+}
+
+void generate_host(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t e, int64_t* row_ptr,
+                   int64_t* col, double* val, Coef cf) {
+    if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
+    if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
+    row_ptr[0] = 0;
+    for (int64_t r = b; r < e; ++r) {
+        fill_row(stencil, nx, ny, nz, r, col + row_ptr[r - b], val + row_ptr[r - b], cf);
+        row_ptr[r - b + 1] = row_ptr[r - b] + row_len(stencil, nx, ny, nz, r);
+    }
+}
+
+void generate_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t e,
+                     int64_t* d_rp, int64_t* d_col, double* d_val, Coef cf) {
+    if (!rt) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null runtime");
+    if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
+    if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
+    PB_CUDA(cudaSetDevice(rt->rt->device()));
+    cudaStream_t st = rt->rt->stream();
+    const int64_t m = e - b;
+    k_poisson_len<<<pb::blocks_for(m + 1, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp);
+    PB_CHECK_LAUNCH();
+    size_t bytes = 0;
+    PB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, d_rp, d_rp, m + 1, st));
+    pb::DBuf<uint8_t> tmp(bytes ? bytes : 1, st);
+    PB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, d_rp, d_rp, m + 1, st));
+    if (m) k_poisson_fill<<<pb::blocks_for(m, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp, d_col, d_val, cf);
+    PB_CHECK_LAUNCH();
+    PB_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -607,35 +670,34 @@ int64_t pairamg_poisson_nnz(int stencil, int64_t nx, int64_t ny, int64_t nz, int
 
 pairamg_status pairamg_poisson_host(int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b, int64_t e,
                                     int64_t* row_ptr, int64_t* col, double* val) {
-    return guarded([&] {
-        if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
-        if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
-        row_ptr[0] = 0;
-        for (int64_t r = b; r < e; ++r) {
-            fill_row(stencil, nx, ny, nz, r, col + row_ptr[r - b], val + row_ptr[r - b]);
-            row_ptr[r - b + 1] = row_ptr[r - b] + row_len(stencil, nx, ny, nz, r);
-        }
-    });
+    return guarded([&] { generate_host(stencil, nx, ny, nz, b, e, row_ptr, col, val, Coef()); });
 }
 
 pairamg_status pairamg_poisson_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny, int64_t nz, int64_t b,
                                       int64_t e, int64_t* d_rp, int64_t* d_col, double* d_val) {
+    return guarded([&] { generate_device(rt, stencil, nx, ny, nz, b, e, d_rp, d_col, d_val, Coef()); });
+}
+
+pairamg_status pairamg_varcoef_host(int stencil, int64_t nx, int64_t ny, int64_t nz, int levels, uint64_t seed,
+                                    int64_t b, int64_t e, int64_t* row_ptr, int64_t* col, double* val) {
     return guarded([&] {
-        if (!rt) pb::fail(PAIRAMG_INVALID_ARGUMENT, "null runtime");
-        if (stencil != 7 && stencil != 27) pb::fail(PAIRAMG_INVALID_ARGUMENT, "stencil must be 7 or 27");
-        if (b < 0 || e < b || e > nx * ny * nz) pb::fail(PAIRAMG_INVALID_ARGUMENT, "row range");
-        PB_CUDA(cudaSetDevice(rt->rt->device()));
-        cudaStream_t st = rt->rt->stream();
-        const int64_t m = e - b;
-        k_poisson_len<<<pb::blocks_for(m + 1, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp);
-        PB_CHECK_LAUNCH();
-        size_t bytes = 0;
-        PB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, d_rp, d_rp, m + 1, st));
-        pb::DBuf<uint8_t> tmp(bytes ? bytes : 1, st);
-        PB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, d_rp, d_rp, m + 1, st));
-        if (m) k_poisson_fill<<<pb::blocks_for(m, 256), 256, 0, st>>>(stencil, nx, ny, nz, b, m, d_rp, d_col, d_val);
-        PB_CHECK_LAUNCH();
-        PB_CUDA(cudaStreamSynchronize(st));
+        if (levels < 0) pb::fail(PAIRAMG_INVALID_ARGUMENT, "varcoef: levels must be >= 0");
+        Coef cf;
+        cf.levels = levels;
+        cf.seed = seed;
+        generate_host(stencil, nx, ny, nz, b, e, row_ptr, col, val, cf);
+    });
+}
+
+pairamg_status pairamg_varcoef_device(pairamg_runtime* rt, int stencil, int64_t nx, int64_t ny, int64_t nz, int levels,
+                                      uint64_t seed, int64_t b, int64_t e, int64_t* d_rp, int64_t* d_col,
+                                      double* d_val) {
+    return guarded([&] {
+        if (levels < 0) pb::fail(PAIRAMG_INVALID_ARGUMENT, "varcoef: levels must be >= 0");
+        Coef cf;
+        cf.levels = levels;
+        cf.seed = seed;
+        generate_device(rt, stencil, nx, ny, nz, b, e, d_rp, d_col, d_val, cf);
     });
 }
 

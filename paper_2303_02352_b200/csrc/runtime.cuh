@@ -50,6 +50,7 @@ struct CommStats {
     // captured graph replays exactly what was counted while capturing)
     int64_t device_reductions = 0;  // FCG dot / norm allgathers
     int64_t halo_exchanges = 0;     // halo exchanges of x (any transport)
+    int64_t halo_bytes = 0;         // halo values received by those exchanges (8 B each)
     int64_t total_messages() const { return p2p_messages + collective_messages; }
 };
 

@@ -575,6 +575,7 @@ void Solver::exchange(Level& L, const double* x, cudaStream_t st) {
     if (L.p2p.ok) {
         p2p_exchange(L.A.halo, L.p2p, x, halo, st);
         rt.stats().halo_exchanges += 1;
+        rt.stats().halo_bytes += 8 * L.A.halo.n_halo;
     }
     else
         halo_exchange(rt, L.A.halo, x, halo, st);
@@ -602,6 +603,7 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         // launch whose boundary blocks wait for theirs (no comm stream)
         const HaloSrc hs = p2p_halo_src(L.A.halo, L.p2p);
         rt.stats().halo_exchanges += 1;
+        rt.stats().halo_bytes += 8 * L.A.halo.n_halo;
         if (!hs.fused) p2p_push(L.A.halo, L.p2p, o.x, s_);
         sell_apply_split(L.sell_int, L.split_bnd(), o, hs, s_);
         launches_ += hs.fused ? 1 : 2;
@@ -716,6 +718,10 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     PB_CHECK_LAUNCH();
     launches_ += 1;
     const double* crhs = C.rhs.get();
+    if (gather) {  // the replicated level's right-hand side: every rank's segment to every rank
+        rt.stats().halo_exchanges += 1;
+        rt.stats().halo_bytes += 8 * (C.A.n - T.A.n);
+    }
     if (gather && rep_gather_.ok) {  // NVLink stores of the restricted rhs into every rank's copy
         p2p_seg_gather(rep_gather_, T.rhs.get(), T.A.n, h.rep_offsets[static_cast<size_t>(rt.rank())], s_);
         crhs = rep_gather_.buf;
@@ -851,6 +857,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
     } else if (split_launch(L0)) {
         const HaloSrc hs = p2p_halo_src(L0.A.halo, L0.p2p);
         rt.stats().halo_exchanges += 1;
+        rt.stats().halo_bytes += 8 * L0.A.halo.n_halo;
         if (!hs.fused) p2p_push(L0.A.halo, L0.p2p, w, s_);
         dots_grid_ = sell_spmv_dots_split(L0.sell_int, L0.split_bnd(), w, v_.get(), r_.get(), q_.get(), partials_.get(),
                                           max_blocks_, hs, s_);
@@ -988,6 +995,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             per_iter_launches_ = launches_ - l0;
             reductions_per_iter_ = static_cast<int>(rt.stats().device_reductions - c0.device_reductions);
             halos_per_iter_ = static_cast<int>(rt.stats().halo_exchanges - c0.halo_exchanges);
+            halo_bytes_per_iter_ = static_cast<double>(rt.stats().halo_bytes - c0.halo_bytes);
             launches_ = l0;
             PB_CUDA(cudaGraphInstantiate(&graph_, g, 0));
             PB_CUDA(cudaGraphDestroy(g));
@@ -1061,6 +1069,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
         st->t_d2h_s = 0.0;
         st->reductions_per_iter = reductions_per_iter_;
         st->halo_exchanges_per_iter = halos_per_iter_;
+        st->halo_bytes_per_iter = halo_bytes_per_iter_;
         if (st->history)
             for (int i = 0; i < st->history_cap && i < static_cast<int>(hist.size()); ++i) st->history[i] = hist[i];
     }

@@ -121,6 +121,7 @@ private:
     void ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters);
     int64_t per_iter_launches_ = 0;
     int reductions_per_iter_ = 0, halos_per_iter_ = 0;  // cross-rank exchanges per FCG iteration
+    double halo_bytes_per_iter_ = 0.0;
     double cap_rtol_ = 0.0;  // stopping test captured into the multi-rank iteration graph
     int cap_maxit_ = 0;
     std::vector<cudaEvent_t> ev_pool_;

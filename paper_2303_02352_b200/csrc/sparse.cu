@@ -275,6 +275,7 @@ void l1_diagonal(const DevMatrix& M, double* d_out, cudaStream_t s) {
 void halo_exchange(Runtime& rt, HaloPlan& H, const double* x_owned, double* x_halo, cudaStream_t s) {
     if (!H.has_traffic()) return;
     rt.stats().halo_exchanges += 1;
+    rt.stats().halo_bytes += 8 * H.n_halo;
     const int64_t nsend = H.send_off.back();
     if (nsend) {
         k_pack<<<blocks_for(nsend, 256), 256, 0, s>>>(H.send_idx.get(), nsend, x_owned, H.send_buf.get());
