@@ -132,6 +132,14 @@ def problem_dims(args, world: int):
     return nd, nd, nd, 40 * nd
 
 
+def slab(n: int, world: int, rank: int):
+    """Row-block partition (Partition::uniform) and this rank's block."""
+    import paper_2303_02352_b200 as pb
+
+    starts = pb.uniform_partition(n, world)
+    return starts, int(starts[rank]), int(starts[rank + 1])
+
+
 def workload_name(args, world):
     nx, ny, nz, _ = problem_dims(args, world)
     base = f"poisson{args.stencil}" if args.problem == "poisson" else f"varcoef{args.stencil}L{args.levels}"
@@ -284,8 +292,7 @@ def bench_ours(args, rank, world, local_rank):
     rt = pb.Runtime(local_rank, rank, world, uid)
     nx, ny, nz, target = problem_dims(args, world)
     n = nx * ny * nz
-    starts = pb.uniform_partition(n, world)
-    b0, b1 = int(starts[rank]), int(starts[rank + 1])
+    starts, b0, b1 = slab(n, world, rank)
     m = b1 - b0
     L = pb.lib()
     nnz = L.pairamg_poisson_nnz(args.stencil, nx, ny, nz, b0, b1)
