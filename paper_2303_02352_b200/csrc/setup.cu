@@ -461,6 +461,104 @@ __global__ void __launch_bounds__(kGalBigThreads) k_galerkin_block(GalerkinArgs 
     }
 }
 
+// ---- coarse rows beyond the block kernel's shared-memory capacity ----
+// Contributions of each such row go to global memory in encounter order
+// (key = row << 40 | coarse column), a stable radix sort makes equal columns
+// contiguous without reordering them, and one thread per segment folds it in
+// the reference's order -- the same arithmetic as galerkin_team.
+constexpr int kHugeColBits = 40;
+
+__global__ void k_huge_len(GalerkinArgs a, const int64_t* __restrict__ rows, int64_t nh, int64_t* __restrict__ len) {
+    const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h > nh) return;
+    if (h == nh) {
+        len[nh] = 0;
+        return;
+    }
+    const int64_t c = rows[h];
+    int64_t m = 0;
+    for (int64_t t = a.rrp[c]; t < a.rrp[c + 1]; ++t) {
+        const int32_t i = a.rcol[t];
+        m += a.rp[i + 1] - a.rp[i];
+    }
+    len[h] = m;
+}
+
+__global__ void k_huge_fill(GalerkinArgs a, const int64_t* __restrict__ rows, int64_t nh, const int64_t* __restrict__ off,
+                            uint64_t* __restrict__ key, int64_t* __restrict__ pos, double* __restrict__ hv,
+                            double* __restrict__ hr, int32_t* __restrict__ ht) {
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int64_t c = rows[h];
+        int64_t m = off[h];
+        const int64_t rb = a.rrp[c], re = a.rrp[c + 1];
+        for (int64_t t = rb; t < re; ++t) {
+            const int32_t i = a.rcol[t];
+            const double rv = a.rval[t];
+            const int64_t b = a.rp[i], e = a.rp[i + 1];
+            for (int64_t u = threadIdx.x; u < e - b; u += blockDim.x) {
+                const int32_t j = a.col[b + u];
+                key[m + u] = (static_cast<uint64_t>(h) << kHugeColBits) | static_cast<uint64_t>(a.pc[j]);
+                pos[m + u] = m + u;
+                hv[m + u] = dmul(a.val[b + u], a.pv[j]);
+                hr[m + u] = rv;
+                ht[m + u] = static_cast<int32_t>(t - rb);
+            }
+            m += e - b;
+        }
+    }
+}
+
+__global__ void k_huge_heads(const uint64_t* __restrict__ key, int64_t M, int64_t* __restrict__ head) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < M) head[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// distinct columns of huge row h = segments starting in [off[h], off[h+1])
+__global__ void k_huge_count(const int64_t* __restrict__ rows, int64_t nh, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ segx, int64_t M, int64_t nseg, int64_t* __restrict__ cnt) {
+    const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h >= nh) return;
+    const int64_t a0 = off[h] < M ? segx[off[h]] : nseg;
+    const int64_t a1 = off[h + 1] < M ? segx[off[h + 1]] : nseg;
+    cnt[rows[h]] = a1 - a0;
+}
+
+__global__ void k_huge_fold(GalerkinArgs a, const int64_t* __restrict__ rows, const int64_t* __restrict__ off,
+                            const uint64_t* __restrict__ key, const int64_t* __restrict__ pos,
+                            const double* __restrict__ hv, const double* __restrict__ hr,
+                            const int32_t* __restrict__ ht, const int64_t* __restrict__ segx, int64_t M) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M || !(i == 0 || key[i] != key[i - 1])) return;
+    const int64_t h = static_cast<int64_t>(key[i] >> kHugeColBits);
+    const int64_t c = rows[h];
+    bool acc_set = false, ct_set = false;
+    double acc = 0.0, ct = 0.0, rt = 0.0;
+    int cur_t = -1;
+    for (int64_t j = i; j < M && key[j] == key[i]; ++j) {
+        const int64_t q = pos[j];
+        const int t2 = ht[q];
+        if (t2 != cur_t) {
+            if (ct_set) {
+                const double contrib = dmul(rt, ct);
+                acc = acc_set ? dadd(acc, contrib) : contrib;
+                acc_set = true;
+            }
+            ct_set = false;
+            cur_t = t2;
+            rt = hr[q];
+        }
+        ct = ct_set ? dadd(ct, hv[q]) : hv[q];
+        ct_set = true;
+    }
+    if (ct_set) {
+        const double contrib = dmul(rt, ct);
+        acc = acc_set ? dadd(acc, contrib) : contrib;
+    }
+    const int64_t o = a.orp[c] + (segx[i] - segx[off[h]]);
+    a.ocol[o] = static_cast<int64_t>(key[i] & ((uint64_t(1) << kHugeColBits) - 1));
+    a.oval[o] = acc;
+}
+
 __global__ void k_flag_big(const int64_t* __restrict__ cnt, int64_t nc, int64_t* __restrict__ flag) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c < nc) flag[c] = cnt[c] < 0 ? 1 : 0;
@@ -533,6 +631,7 @@ int64_t galerkin(const DevMatrix& A, const int64_t* pc, const double* pv, const 
         }
     }
     const size_t big_smem = kGalBigCap * (8 + 8 + 8 + 4);
+    int64_t nhuge = 0;
     if (nbig) {
         PB_CUDA(cudaFuncSetAttribute(k_galerkin_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(big_smem)));
@@ -547,8 +646,63 @@ int64_t galerkin(const DevMatrix& A, const int64_t* pc, const double* pv, const 
         cub_call([&](void* t, size_t& b) {
             return cub::DeviceReduce::Sum(t, b, flag.get(), num.get(), nc, s);
         }, s);
-        if (read_one(num.get(), s))
-            fail(PAIRAMG_INTERNAL, "galerkin: coarse row with more than 4096 contributions");
+        nhuge = read_one(num.get(), s);
+    }
+    // rows beyond kGalBigCap: global-memory contributions + stable radix sort
+    DBuf<int64_t> hrows, hoff, hpos, hsegx;
+    DBuf<uint64_t> hkey;
+    DBuf<double> hv, hr;
+    DBuf<int32_t> ht;
+    int64_t M = 0;
+    if (nhuge) {
+        DBuf<int64_t> flag(static_cast<size_t>(nc), s), num(1, s);
+        LAUNCH(k_flag_big, nc, cnt.get(), nc, flag.get());
+        hrows.alloc(static_cast<size_t>(nhuge), s);
+        thrust::counting_iterator<int64_t> it(0);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, it, flag.get(), hrows.get(), num.get(), nc, s);
+        }, s);
+        if (a.nc >= (int64_t(1) << (64 - kHugeColBits)) || nhuge >= (int64_t(1) << (64 - kHugeColBits)))
+            fail(PAIRAMG_INTERNAL, "galerkin: too many dense coarse rows");
+        hoff.alloc(static_cast<size_t>(nhuge + 1), s);
+        LAUNCH(k_huge_len, nhuge + 1, a, hrows.get(), nhuge, hoff.get());
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, hoff.get(), hoff.get(), nhuge + 1, s);
+        }, s);
+        M = read_one(hoff.get() + nhuge, s);
+        DBuf<uint64_t> key0(static_cast<size_t>(M), s);
+        DBuf<int64_t> pos0(static_cast<size_t>(M), s);
+        hv.alloc(static_cast<size_t>(M), s);
+        hr.alloc(static_cast<size_t>(M), s);
+        ht.alloc(static_cast<size_t>(M), s);
+        k_huge_fill<<<static_cast<int>(std::min<int64_t>(nhuge, 8 * kSmCount)), 256, 0, s>>>(
+            a, hrows.get(), nhuge, hoff.get(), key0.get(), pos0.get(), hv.get(), hr.get(), ht.get());
+        PB_CHECK_LAUNCH();
+        hkey.alloc(static_cast<size_t>(M), s);
+        hpos.alloc(static_cast<size_t>(M), s);
+        int hb = 0;
+        while ((int64_t(1) << hb) <= nhuge) ++hb;
+        const int end_bit = kHugeColBits + hb;
+        cub_call([&](void* t, size_t& b) {  // stable: equal keys keep encounter order
+            return cub::DeviceRadixSort::SortPairs(t, b, key0.get(), hkey.get(), pos0.get(), hpos.get(), M, 0,
+                                                   end_bit, s);
+        }, s);
+        hsegx.alloc(static_cast<size_t>(M), s);
+        LAUNCH(k_huge_heads, M, hkey.get(), M, hsegx.get());
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, hsegx.get(), hsegx.get(), M, s);
+        }, s);
+        int64_t nseg = 0;
+        {
+            int64_t last = 0;
+            uint64_t k1 = 0, k0 = 0;
+            PB_CUDA(cudaMemcpyAsync(&last, hsegx.get() + M - 1, 8, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaMemcpyAsync(&k1, hkey.get() + M - 1, 8, cudaMemcpyDeviceToHost, s));
+            if (M > 1) PB_CUDA(cudaMemcpyAsync(&k0, hkey.get() + M - 2, 8, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaStreamSynchronize(s));
+            nseg = last + ((M == 1 || k1 != k0) ? 1 : 0);
+        }
+        LAUNCH(k_huge_count, nhuge, hrows.get(), nhuge, hoff.get(), hsegx.get(), M, nseg, cnt.get());
     }
     orp.alloc(static_cast<size_t>(nc + 1), s);
     cub_call([&](void* t, size_t& b) {
@@ -566,6 +720,10 @@ int64_t galerkin(const DevMatrix& A, const int64_t* pc, const double* pv, const 
         k_galerkin_block<true><<<static_cast<int>(std::min<int64_t>(nbig, 4 * kSmCount)), kGalBigThreads,
                                  big_smem, s>>>(a, big.get(), nbig);
         PB_CHECK_LAUNCH();
+    }
+    if (M) {  // the huge rows' numeric pass (the warp / block kernels skipped them: overflow)
+        LAUNCH(k_huge_fold, M, a, hrows.get(), hoff.get(), hkey.get(), hpos.get(), hv.get(), hr.get(), ht.get(),
+               hsegx.get(), M);
     }
     return nnz;
 }

@@ -33,6 +33,14 @@ CASES = [
     dict(stencil=7, nx=64, ny=64, nz=64, nranks=1),   # configs[0] (SURVEY-pinned numbers)
 ]
 
+# BASELINE.json's single-GPU configs (python scripts/make_golden.py --big ->
+# tests/golden/hierarchies_big.json).  Slab-aligned, so the hierarchy is the
+# same at every power-of-two p; the reference runs at p = 8 host threads.
+BIG_CASES = [
+    dict(stencil=7, nx=256, ny=256, nz=256, nranks=8),   # configs[1]
+    dict(stencil=27, nx=192, ny=192, nz=192, nranks=8),  # configs[4], one GPU's 192^3
+]
+
 
 def digest(a) -> str:
     a = np.ascontiguousarray(a)
@@ -65,8 +73,9 @@ def hierarchy_record(o):
 
 
 def main():
+    big = "--big" in sys.argv
     out = []
-    for c in CASES:
+    for c in (BIG_CASES if big else CASES):
         nd = max(c["nx"], c["ny"], c["nz"]) if c["nz"] == c["nx"] else c["nx"]
         target = 40 * nd
         ref = oracle.Oracle("reference", coarse_size_target=target, **c).setup()
@@ -85,11 +94,19 @@ def main():
                                   "prolongator_digest": rec2["prolongator_digest"],
                                   "matching_digest": rec2["matching_digest"], "spmv_digest": rec2["spmv_digest"],
                                   "vcycle_digest": rec2["vcycle_digest"], "iterations": tot.solve()["iterations"]}
+        if big:  # the p = 8 hierarchy must be the p = 1 hierarchy (slab-aligned): check it
+            one = oracle.Oracle("reference", coarse_size_target=target, **{**c, "nranks": 1}).setup()
+            r1 = hierarchy_record(one)
+            rec["same_hierarchy_p1"] = all(rec[k] == r1[k] for k in ("sizes", "level_digest", "prolongator_digest",
+                                                                    "matching_digest", "spmv_digest",
+                                                                    "vcycle_digest"))
+            del one
         print(c, rec["levels"], rec["opc"], rec["iterations"], rec["relres"], "total_order_equal",
-              rec["total_order_equal"], flush=True)
+              rec["total_order_equal"], rec.get("same_hierarchy_p1"), flush=True)
         out.append(rec)
     os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
-    with open(os.path.join(ROOT, "tests", "golden", "hierarchies.json"), "w") as f:
+    name = "hierarchies_big.json" if big else "hierarchies.json"
+    with open(os.path.join(ROOT, "tests", "golden", name), "w") as f:
         json.dump({"generator": "scripts/make_golden.py (oracle/_ref = reference C++ compiled unmodified)",
                    "probe_vector": "sin(0.37 i) + 0.25 cos(1.3 i)", "cases": out}, f, indent=1)
 

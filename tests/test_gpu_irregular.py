@@ -133,3 +133,32 @@ def test_random_pattern_few_values(runtime, fmt):
     fmts = check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=20, s_exp=2, all_levels=True,
                       storage=fmt)
     assert fmts[0] == "coded", fmts
+
+
+def test_dense_coarse_rows(runtime):
+    """A coupling row that touches every unknown (arrow matrix): the coarse row
+    of its aggregate gathers more R*(A*P) contributions than the block
+    kernel's shared memory holds (> 4096), which takes the global-memory
+    stable-sort path of the Galerkin product -- still bitwise the oracle."""
+    n = 6000
+    rows = []
+    for i in range(n):
+        ent = {}
+        if i > 0:
+            ent[i - 1] = -1.0
+        if i < n - 1:
+            ent[i + 1] = -1.0
+        ent[i] = 2.5
+        rows.append(ent)
+    for j in range(2, n):  # row/column 0 coupled to everything
+        rows[0][j] = -1e-3
+        rows[j][0] = -1e-3
+        rows[j][j] += 1e-3
+    rows[0][0] += 1e-3 * (n - 2)
+    rp, ci, va = [0], [], []
+    for ent in rows:
+        for c in sorted(ent):
+            ci.append(c)
+            va.append(ent[c])
+        rp.append(len(ci))
+    check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=50, s_exp=3)
