@@ -7,7 +7,9 @@ breakdown, as the paper's protocol does.
 
 One process per GPU: with -P p > 1 the command re-launches itself under
 torch.distributed.run (p ranks on 127.0.0.1) unless it already runs as one of
-p ranks.  -n generates the 7/27-point Poisson operator on the device (z-box
+p ranks.  With --threads the p ranks are threads of this one process instead
+(the reference's spawn_ranks; LOCAL runtime, all on cuda:0 -- a multi-rank
+run on a single GPU).  -n generates the 7/27-point Poisson operator on the device (z-box
 nd x nd x (nd*p) with --zbox, else the nd^3 cube split by Partition::uniform);
 -m reads a MatrixMarket file and hands every rank its row block
 (read_matrix_market + distribute_matrix).  b = 1, u0 = 0, w0 = 1.
@@ -82,6 +84,7 @@ def main(argv=None) -> int:
     ap.add_argument("-s", dest="stencil", type=int, default=7, choices=(7, 27))
     ap.add_argument("--zbox", action="store_true", help="generator: nd x nd x (nd*p) (weak scaling)")
     ap.add_argument("-P", dest="ranks", type=int, default=1)
+    ap.add_argument("--threads", action="store_true", help="-P ranks as threads of this process on cuda:0")
     ap.add_argument("-p", dest="precflag", type=int, choices=(0, 1), default=None)
     ap.add_argument("-c", dest="config")
     ap.add_argument("--json", action="store_true")
@@ -99,6 +102,10 @@ def main(argv=None) -> int:
     if a.precflag is not None:
         cfg["precflag"] = a.precflag
 
+    if a.threads:
+        # every kernel loaded up front: ranks sharing a GPU (runtime.cu)
+        os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+        return run_threads(a, cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.ranks > 1 and world != a.ranks:
         if world != 1:
@@ -111,8 +118,17 @@ def main(argv=None) -> int:
     return run(a, cfg, world)
 
 
+def run_threads(a, cfg: dict) -> int:
+    import torch
+
+    import paper_2303_02352_b200 as pb
+
+    torch.cuda.set_device(0)
+    out = pb.spawn_ranks(a.ranks, lambda rt: run_rank(a, cfg, rt, a.ranks, rt.rank, 0, lambda: None))
+    return out[0]
+
+
 def run(a, cfg: dict, world: int) -> int:
-    import numpy as np
     import torch
 
     import paper_2303_02352_b200 as pb
@@ -120,7 +136,6 @@ def run(a, cfg: dict, world: int) -> int:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     uid = None
     if world > 1:
         import torch.distributed as dist
@@ -130,6 +145,29 @@ def run(a, cfg: dict, world: int) -> int:
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     rt = pb.Runtime(local, rank, world, uid)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    rc = run_rank(a, cfg, rt, world, rank, local, barrier)
+    rt.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return rc
+
+
+def run_rank(a, cfg: dict, rt, world: int, rank: int, local: int, barrier) -> int:
+    """One rank's generate / read, setup, solve and report (rank 0 prints)."""
+    import torch
+
+    import paper_2303_02352_b200 as pb
+
+    dev = torch.device("cuda", local)
     if a.nd is not None:
         nx = ny = a.nd
         nz = a.nd * world if a.zbox else a.nd
@@ -159,12 +197,6 @@ def run(a, cfg: dict, world: int) -> int:
     cycle = pb.CycleConfig(cfg.get("pre_sweeps", 4), cfg.get("post_sweeps", 4), cfg.get("coarsest_sweeps", 20),
                            cfg.get("relax_weight", 1.0))
     solve_cfg = pb.SolveConfig(cfg.get("rtol", 1e-6), cfg.get("max_iters", 1000), cfg.get("precflag", 1))
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
 
     s = pb.Solver(rt)
     barrier()
@@ -214,11 +246,6 @@ def run(a, cfg: dict, world: int) -> int:
             ti = report["titer_s"]
             print(f"tsolve       {st.t_solve_s:.4f} s   titer {ti * 1e3 if ti else float('nan'):.3f} ms")
     s.close()
-    rt.close()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
     return 0 if st.converged else 1
 
 

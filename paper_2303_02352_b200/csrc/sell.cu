@@ -1003,10 +1003,42 @@ bool sten_rpt2(const Sell& S, bool dots = false) {
 
 inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nblk; }
 
+// The 27-record main pattern as 9 pencils (c - 1, c, c + 1), centre record
+// L/2 the diagonal, contiguous rows: the k_stenp kernels apply (sell_sten.cuh).
+bool sten_pencils(const Sell& S) {
+    if (S.sten_L != 27 || !S.rows.empty() || !sten_center(S)) return false;
+    for (int k = 0; k < 9; ++k) {
+        const int c = S.sten_off[static_cast<size_t>(3 * k + 1)];
+        if (S.sten_off[static_cast<size_t>(3 * k)] != c - 1 || S.sten_off[static_cast<size_t>(3 * k + 2)] != c + 1)
+            return false;
+    }
+    return true;
+}
+
+// Launch arguments of the pencil kernels: 512-row blocks whose x loads
+// (rows wb - 1 .. wb + 64 of every warp, unclamped to nrows) stay in range.
+StenArgs stenp_args_of(const Sell& S, const StenArgs& a0) {
+    StenArgs a = a0;
+    const int64_t B = kPencilRows, nb = (S.nrows + B - 1) / B;
+    int64_t lo = 0, hi = nb;
+    while (lo < nb && S.row0 + B * lo + S.sten_offmin < 0) ++lo;
+    while (hi > lo && S.row0 + B * hi + S.sten_offmax - 1 > S.xlen - 1) --hi;
+    a.safe_lo = static_cast<int>(lo);
+    a.safe_hi = static_cast<int>(hi);
+    a.nblk = static_cast<int>(nb);
+    a.pf_blocks = 16 * kSmCount * 256 / kPencilRows;
+    return a;
+}
+
 // cap > 0: at most `cap` CTAs, grid-striding over the logical blocks.
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
+    if (!ROWS && cap == 0 && sten_pencils(S)) {
+        const StenArgs a = stenp_args_of(S, a0);
+        launch_k<2>(k_stenp<OP, 9>, a.nblk, 256, 0, s, a, p);
+        return;
+    }
     if (sten_rpt2(S)) {
         StenArgs a = sten_args_of(S, 512);
         a.x = a0.x;
@@ -1035,6 +1067,11 @@ void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
 template <bool ROWS>
 int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
+    if (!ROWS && cap == 0 && sten_pencils(S)) {  // 512-row blocks, as sten_rpt2's
+        const StenArgs a = stenp_args_of(S, a0);
+        launch_k<2>(k_stenp_dots<9>, a.nblk, 256, 0, s, a, p);
+        return a.nblk;
+    }
     if (sten_rpt2(S, true)) {
         StenArgs a = sten_args_of(S, 512);
         a.x = a0.x;

@@ -405,6 +405,152 @@ __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_con
 
 
 // ---------------------------------------------------------------------------
+// Pencil form of a contiguous row set whose main pattern is NP runs of three
+// records at (c - 1, c, c + 1) -- every level of the 27-point hierarchies
+// (NP = 9: the (j, k) neighbour pencils of a lexicographic grid).  A warp owns
+// 64 consecutive rows (lane -> rows wb + lane and wb + 32 + lane) and loads
+// only the pencil CENTRES x[row + c]; the i - 1 / i + 1 neighbours are the
+// adjacent rows' centres, taken by warp shuffles, and the two rows beyond the
+// warp's ends come from one extra load per pencil (lane 0: wb - 1, lane 31:
+// wb + 64).  27 gathers per row become 27 loads per 64 rows (+ shuffles): the
+// L1 wavefronts per row drop ~3x -- the 27-point sweeps were L1-bound.
+// Rows past nrows keep their true row index for the x loads (their centres
+// are a valid row's neighbours) and skip the store.  Row sums stay in record
+// order (left, centre, right of pencil 0, then pencil 1, ...): bitwise k_sten.
+constexpr int kPencilRows = 512;  // rows per 256-thread block
+
+template <int NP, bool EDGE>
+__device__ __forceinline__ void stenp_load(const StenArgs& a, const StenParam& p, int wb, int lane, double (&c0)[NP],
+                                           double (&c1)[NP], double (&e)[NP]) {
+    const int ra = a.row0 + wb + lane, re = a.row0 + wb + (lane < 16 ? -1 : 64);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const int o = p.off[3 * k + 1];
+        int i0 = ra + o, i1 = ra + 32 + o, ie = re + o;
+        if (EDGE) {
+            i0 = min(max(i0, 0), a.xlen - 1);
+            i1 = min(max(i1, 0), a.xlen - 1);
+            ie = min(max(ie, 0), a.xlen - 1);
+        }
+        c0[k] = a.x[i0];  // coherent loads: the kernel may start before x's producer completes (PDL)
+        c1[k] = a.x[i1];
+        e[k] = a.x[ie];
+    }
+}
+
+// Fold one row's records of pencil k in record order (masked records skipped).
+template <int NP>
+__device__ __forceinline__ void stenp_fold3(const StenParam& p, int k, double l, double c, double r, uint32_t m,
+                                            bool full, double& sum) {
+    const double v3[3] = {l, c, r};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int rec = 3 * k + j;
+        const bool diag = rec == (3 * NP) / 2;
+        if (!full && ((m >> rec) & 1u)) continue;
+        if (p.neg1 && !diag)
+            sum = dsub(sum, v3[j]);
+        else
+            sum = dadd(sum, dmul(p.val[rec], v3[j]));
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void stenp_sums(const StenParam& p, int lane, const double (&c0)[NP], const double (&c1)[NP],
+                                           const double (&e)[NP], uint32_t ma, uint32_t mb, double& sa, double& sb) {
+    const bool full = __all_sync(0xffffffffu, (ma | mb) == 0u);
+    const int dn = (lane + 31) & 31, up = (lane + 1) & 31;
+    sa = 0.0;
+    sb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const double l0 = __shfl_sync(0xffffffffu, c0[k], dn), l1 = __shfl_sync(0xffffffffu, c1[k], dn);
+        const double u0 = __shfl_sync(0xffffffffu, c0[k], up), u1 = __shfl_sync(0xffffffffu, c1[k], up);
+        const double left_a = lane ? l0 : e[k];
+        const double left_b = lane ? l1 : l0;  // lane 0: c0 of lane 31 = row wb + 31
+        const double right_a = lane < 31 ? u0 : u1;  // lane 31: c1 of lane 0 = row wb + 32
+        const double right_b = lane < 31 ? u1 : e[k];
+        stenp_fold3<NP>(p, k, left_a, c0[k], right_a, ma, full, sa);
+        stenp_fold3<NP>(p, k, left_b, c1[k], right_b, mb, full, sb);
+    }
+}
+
+template <int OP, int NP, bool EDGE>
+__device__ __forceinline__ void stenp_body(const StenArgs& a, const StenParam& p, int wb, int lane) {
+    const int last = a.nrows - 1;
+    const int ia = wb + lane, ib = ia + 32;
+    const int qa_row = a.row0 + min(ia, last), qb_row = a.row0 + min(ib, last);
+    const int qa = a.pid[qa_row], qb = a.pid[qb_row];
+    double ria = 0.0, rib = 0.0;
+    if (OP != kSpmv) {
+        ria = a.r[qa_row];
+        rib = a.r[qb_row];
+    }
+    double c0[NP], c1[NP], e[NP];
+    stenp_load<NP, EDGE>(a, p, wb, lane, c0, c1, e);
+    double sa, sb;
+    stenp_sums<NP>(p, lane, c0, c1, e, p.pmask[qa], p.pmask[qb], sa, sb);
+    if (ia <= last) sten_store<OP, 3 * NP>(a, p, a.row0 + ia, qa, ria, c0[NP / 2], sa);
+    if (ib <= last) sten_store<OP, 3 * NP>(a, p, a.row0 + ib, qb, rib, c1[NP / 2], sb);
+}
+
+template <int OP, int NP>
+__global__ void __launch_bounds__(256) k_stenp(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
+    const int blk = static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31;
+    const int wb = blk * kPencilRows + (static_cast<int>(threadIdx.x) >> 5) * 64;
+    sten_prefetch<OP, kPencilRows>(a, a.r, blk);
+    if (blk < a.safe_lo || blk >= a.safe_hi)
+        stenp_body<OP, NP, true>(a, p, wb, lane);
+    else
+        stenp_body<OP, NP, false>(a, p, wb, lane);
+}
+
+// v = A w + per-CTA partials of (w.r, w.v, w.q), pencil form.
+template <int NP, bool EDGE>
+__device__ __forceinline__ void stenp_dots_body(const StenArgs& a, const StenParam& p, int wb, int lane, double& sa,
+                                                double& sb, double& sg) {
+    const int last = a.nrows - 1;
+    const int ia = wb + lane, ib = ia + 32;
+    const int qa_row = a.row0 + min(ia, last), qb_row = a.row0 + min(ib, last);
+    const int qa = a.pid[qa_row], qb = a.pid[qb_row];
+    const double rra = a.r[qa_row], rrb = a.r[qb_row], qqa = a.q[qa_row], qqb = a.q[qb_row];
+    double c0[NP], c1[NP], e[NP];
+    stenp_load<NP, EDGE>(a, p, wb, lane, c0, c1, e);
+    double va, vb;
+    stenp_sums<NP>(p, lane, c0, c1, e, p.pmask[qa], p.pmask[qb], va, vb);
+    const double wa = c0[NP / 2], wbv = c1[NP / 2];
+    if (ia <= last) {
+        a.y[a.row0 + ia] = va;
+        sa = dadd(sa, dmul(wa, rra));
+        sb = dadd(sb, dmul(wa, va));
+        sg = dadd(sg, dmul(wa, qqa));
+    }
+    if (ib <= last) {
+        a.y[a.row0 + ib] = vb;
+        sa = dadd(sa, dmul(wbv, rrb));
+        sb = dadd(sb, dmul(wbv, vb));
+        sg = dadd(sg, dmul(wbv, qqb));
+    }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_stenp_dots(StenArgs a, const __grid_constant__ StenParam p) {
+    pdl_begin();
+    const int blk = static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31;
+    const int wb = blk * kPencilRows + (static_cast<int>(threadIdx.x) >> 5) * 64;
+    sten_prefetch<-1, kPencilRows>(a, a.r, blk);
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (blk < a.safe_lo || blk >= a.safe_hi)
+        stenp_dots_body<NP, true>(a, p, wb, lane, sa, sb, sg);
+    else
+        stenp_dots_body<NP, false>(a, p, wb, lane, sa, sb, sg);
+    dots_block_store(sa, sb, sg, a.partials);
+}
+
+// ---------------------------------------------------------------------------
 // The coarsest level's whole smoothing (zero start + nu-1 l1-Jacobi sweeps,
 // cycle.cpp:86-93) in ONE launch of one thread-block cluster: every CTA
 // owns R consecutive rows, keeps its slice of the iterate in shared memory
