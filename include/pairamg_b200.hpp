@@ -4,6 +4,7 @@
 //   pairamg::ErrorCode / pairamg::Error        types.hpp:13-35
 //   pairamg::Partition::uniform                 runtime.hpp:15-28, runtime.cpp:13-22
 //   pairamg::SetupConfig / CycleConfig          amg.hpp:17-23, cycle.hpp:7-12
+//   pairamg::MatchingTrace (replay / record)    amg.hpp:13-23, amg.cpp:182-220
 //   pairamg::SolveConfig / SolveStats           SPEC.md:468-477 (pcg.cpp absent)
 //   pairamg::b200::Solver::setup                setup_hierarchy, amg.hpp:84-85
 //   pairamg::b200::Solver::solve                pcg_solve
@@ -70,10 +71,17 @@ struct Partition {
     index_t extent(int r) const { return starts[r + 1] - starts[r]; }
 };
 
+// Recorded pairwise matchings (global mates, one array per pairwise step).
+struct MatchingTrace {
+    std::vector<std::vector<index_t>> steps;
+};
+
 struct SetupConfig {
     int aggregation_exponent = 3;
     index_t coarse_size_target = 40;
     int max_levels = 40;
+    const MatchingTrace* replay = nullptr;
+    MatchingTrace* record = nullptr;
 };
 
 struct CycleConfig {
@@ -113,6 +121,12 @@ public:
         check(pairamg_comm_unique_id(id.data()));
         return id;
     }
+    // ranks that are threads of this process (spawn_ranks): one id for all of them
+    static std::vector<uint8_t> local_id() {
+        std::vector<uint8_t> id(128);
+        check(pairamg_comm_local_id(id.data()));
+        return id;
+    }
     int rank() const { return rank_; }
     int nranks() const { return nranks_; }
     pairamg_runtime* get() const { return h_; }
@@ -133,9 +147,52 @@ public:
     void setup(const Partition& part, const std::vector<index_t>& row_ptr, const std::vector<index_t>& col_idx,
                const std::vector<real_t>& values, const std::vector<real_t>* w0 = nullptr,
                const SetupConfig& cfg = {}) {
-        const pairamg_setup_config c{cfg.aggregation_exponent, cfg.coarse_size_target, cfg.max_levels};
+        pairamg_setup_config c;
+        pairamg_default_setup_config(&c);
+        c.aggregation_exponent = cfg.aggregation_exponent;
+        c.coarse_size_target = cfg.coarse_size_target;
+        c.max_levels = cfg.max_levels;
+        std::vector<const int64_t*> mates;
+        std::vector<int64_t> sizes;
+        if (cfg.replay) {
+            for (const auto& m : cfg.replay->steps) {
+                mates.push_back(m.data());
+                sizes.push_back(static_cast<int64_t>(m.size()));
+            }
+            c.replay_steps = static_cast<int>(mates.size());
+            c.replay_mates = mates.data();
+            c.replay_sizes = sizes.data();
+        }
         check(pairamg_setup(h_, part.global_n, part.starts.data(), part.extent(rt_.rank()), row_ptr.data(),
                             col_idx.data(), values.data(), w0 ? w0->data() : nullptr, &c));
+        if (cfg.record) {  // this rank's owned block of every step (the reference records on rank 0 only)
+            int steps = 0;
+            check(pairamg_num_matchings(h_, &steps));
+            cfg.record->steps.clear();
+            for (int t = 0; t < steps; ++t) {
+                int64_t n = 0;
+                check(pairamg_matching_export(h_, t, &n, nullptr));
+                std::vector<index_t> m(static_cast<size_t>(n));
+                check(pairamg_matching_export(h_, t, &n, m.data()));
+                cfg.record->steps.push_back(std::move(m));
+            }
+        }
+    }
+
+    // Hierarchy::warnings (amg.hpp:56) + validate_cycle_config's (cycle.cpp:7-13).
+    std::vector<std::string> warnings() const {
+        int n = 0;
+        check(pairamg_setup_warnings(h_, &n));
+        std::vector<std::string> out;
+        for (int i = 0; i < n; ++i) {
+            size_t len = 0;
+            check(pairamg_setup_warning(h_, i, nullptr, 0, &len));
+            std::string w(len + 1, '\0');
+            check(pairamg_setup_warning(h_, i, w.data(), w.size(), nullptr));
+            w.resize(len);
+            out.push_back(std::move(w));
+        }
+        return out;
     }
 
     SolveStats solve(const std::vector<real_t>& b, std::vector<real_t>& u, const CycleConfig& cc = {},

@@ -121,6 +121,26 @@ struct Blob {
 
 }  // namespace
 
+// Teardown order (CUDA IPC): every importer closes its mappings of a peer's
+// buffers before the exporter frees them.  Re-setups do it collectively --
+// p2p_close_imports on every rank, a barrier, then the frees (Solver::setup).
+void p2p_close_imports(P2PHalo& P) {
+    for (void* p : P.opened) cudaIpcCloseMemHandle(p);
+    P.opened.clear();
+    P.peer_staging.clear();
+    P.peer_stride.clear();
+    P.peer_flag.clear();
+    P.ok = false;
+}
+
+void p2p_seg_close_imports(P2PSegGather& G) {
+    for (void* p : G.opened) cudaIpcCloseMemHandle(p);
+    G.opened.clear();
+    G.peer_buf.clear();
+    G.peer_flags.clear();
+    G.ok = false;
+}
+
 void p2p_destroy(P2PHalo& P) {
     for (void* p : P.opened) cudaIpcCloseMemHandle(p);
     P.opened.clear();

@@ -39,6 +39,8 @@ struct P2PHalo {
 // path stays) when IPC is unavailable.
 void p2p_setup(Runtime& rt, const HaloPlan& H, P2PHalo& P, cudaStream_t s);
 void p2p_destroy(P2PHalo& P);
+// Close this rank's mappings of peer buffers (no free); see p2p.cu.
+void p2p_close_imports(P2PHalo& P);
 // x_halo <- the owners' x (push from every rank, then pull), on stream s.
 void p2p_exchange(const HaloPlan& H, P2PHalo& P, const double* x_owned, double* x_halo, cudaStream_t s);
 // Push only: the consumer is a split launch reading the staging slot itself
@@ -87,6 +89,7 @@ struct P2PSegGather {
 // Collective; leaves G.ok = false (NCCL stays) when IPC is unavailable.
 void p2p_seg_setup(Runtime& rt, P2PSegGather& G, int64_t total, cudaStream_t s);
 void p2p_seg_destroy(P2PSegGather& G);
+void p2p_seg_close_imports(P2PSegGather& G);
 // G.buf[off + i] = src[i] on every rank, all ranks' segments present when the
 // kernel completes (stream s, graph-capturable).
 void p2p_seg_gather(P2PSegGather& G, const double* src, int64_t cnt, int64_t off, cudaStream_t s);

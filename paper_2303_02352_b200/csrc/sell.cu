@@ -1003,40 +1003,46 @@ bool sten_rpt2(const Sell& S, bool dots = false) {
 
 inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nblk; }
 
-// The 27-record main pattern as 9 pencils (c - 1, c, c + 1), centre record
-// L/2 the diagonal, contiguous rows: the k_stenp kernels apply (sell_sten.cuh).
-bool sten_pencils(const Sell& S) {
-    if (S.sten_L != 27 || !S.rows.empty() || !sten_center(S)) return false;
-    for (int k = 0; k < 9; ++k) {
-        const int c = S.sten_off[static_cast<size_t>(3 * k + 1)];
-        if (S.sten_off[static_cast<size_t>(3 * k)] != c - 1 || S.sten_off[static_cast<size_t>(3 * k + 2)] != c + 1)
-            return false;
-    }
+// The 27-record main pattern as the full 3x3x3 box (record 9(dk+1) + 3(dj+1)
+// + (di+1) at offset di + nx dj + nxy dk) on contiguous rows: the marching
+// kernels apply (sell_sten.cuh).  Fills the geometry of the row set.
+bool sten_march(const Sell& S, MarchGeom* out = nullptr) {
+    if (S.sten_L != 27 || !S.rows.empty() || !sten_center(S) || S.nrows == 0) return false;
+    const auto& o = S.sten_off;
+    const int nx = o[static_cast<size_t>(16)] - o[static_cast<size_t>(13)];
+    const int nxy = o[static_cast<size_t>(22)] - o[static_cast<size_t>(13)];
+    if (nx < 2 || nxy < 2 * nx || nxy % nx) return false;
+    for (int dk = -1; dk <= 1; ++dk)
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int di = -1; di <= 1; ++di)
+                if (o[static_cast<size_t>(9 * (dk + 1) + 3 * (dj + 1) + di + 1)] != di + nx * dj + nxy * dk) return false;
+    MarchGeom g{};
+    g.nx = nx;
+    g.nxy = nxy;
+    g.ny = nxy / nx;
+    g.tiles_x = (nx + kMarchTX - 1) / kMarchTX;
+    g.tiles_y = (g.ny + kMarchTY - 1) / kMarchTY;
+    g.k0 = static_cast<int>(S.row0 / nxy);
+    g.nk = static_cast<int>((S.row0 + S.nrows - 1) / nxy) - g.k0 + 1;
+    // planes per CTA: about two waves of 4 CTAs per SM (measured at 192^3:
+    // 2 waves 72 us per sweep, 1 wave 83, 4 waves 77, 8 waves 84; the two
+    // halo planes per chunk are the re-read cost); small levels keep k_sten
+    const int64_t cols = int64_t(g.tiles_x) * g.tiles_y;
+    g.kz = static_cast<int>(std::min<int64_t>(32, cols * g.nk / (int64_t(kMarchWaves) * kMarchMinBlocks * kSmCount)));
+    if (g.kz < 4) return false;
+    g.chunks = (g.nk + g.kz - 1) / g.kz;
+    if (out) *out = g;
     return true;
 }
 
-// Launch arguments of the pencil kernels: 512-row blocks whose x loads
-// (rows wb - 1 .. wb + 64 of every warp, unclamped to nrows) stay in range.
-StenArgs stenp_args_of(const Sell& S, const StenArgs& a0) {
-    StenArgs a = a0;
-    const int64_t B = kPencilRows, nb = (S.nrows + B - 1) / B;
-    int64_t lo = 0, hi = nb;
-    while (lo < nb && S.row0 + B * lo + S.sten_offmin < 0) ++lo;
-    while (hi > lo && S.row0 + B * hi + S.sten_offmax - 1 > S.xlen - 1) --hi;
-    a.safe_lo = static_cast<int>(lo);
-    a.safe_hi = static_cast<int>(hi);
-    a.nblk = static_cast<int>(nb);
-    a.pf_blocks = 16 * kSmCount * 256 / kPencilRows;
-    return a;
-}
+int march_grid(const MarchGeom& g) { return g.tiles_x * g.tiles_y * g.chunks; }
 
-// cap > 0: at most `cap` CTAs, grid-striding over the logical blocks.
 template <int OP, bool ROWS>
 void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
-    if (!ROWS && cap == 0 && sten_pencils(S)) {
-        const StenArgs a = stenp_args_of(S, a0);
-        launch_k<2>(k_stenp<OP, 9>, a.nblk, 256, 0, s, a, p);
+    MarchGeom g;
+    if (!ROWS && cap == 0 && sten_march(S, &g)) {
+        launch_k<2>(k_sten_march<OP>, march_grid(g), 256, 0, s, a0, p, g);
         return;
     }
     if (sten_rpt2(S)) {
@@ -1067,10 +1073,10 @@ void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
 template <bool ROWS>
 int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
-    if (!ROWS && cap == 0 && sten_pencils(S)) {  // 512-row blocks, as sten_rpt2's
-        const StenArgs a = stenp_args_of(S, a0);
-        launch_k<2>(k_stenp_dots<9>, a.nblk, 256, 0, s, a, p);
-        return a.nblk;
+    MarchGeom g;
+    if (!ROWS && cap == 0 && sten_march(S, &g)) {
+        launch_k<2>(k_sten_march_dots, march_grid(g), 256, 0, s, a0, p, g);
+        return march_grid(g);
     }
     if (sten_rpt2(S, true)) {
         StenArgs a = sten_args_of(S, 512);
@@ -1304,6 +1310,7 @@ bool build_sten_wide(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sel
 
 void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s, int storage,
                 const double* l1) {
+    NvtxRange nv("setup/solve-time storage");
     sell_prologue(M, rows, nrows, S, s);
 
     // Format choice (measured on B200): STEN whenever the rows
@@ -1593,6 +1600,8 @@ int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* 
 }
 
 int sell_dots_grid(const Sell& S, int cap) {
+    MarchGeom g;
+    if (S.format == Sell::kSten && cap == 0 && S.rows.empty() && sten_march(S, &g)) return march_grid(g);
     if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256), cap);
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;

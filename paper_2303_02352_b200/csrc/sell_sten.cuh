@@ -405,148 +405,172 @@ __global__ void __launch_bounds__(256) k_sten2_dots(StenArgs a, const __grid_con
 
 
 // ---------------------------------------------------------------------------
-// Pencil form of a contiguous row set whose main pattern is NP runs of three
-// records at (c - 1, c, c + 1) -- every level of the 27-point hierarchies
-// (NP = 9: the (j, k) neighbour pencils of a lexicographic grid).  A warp owns
-// 64 consecutive rows (lane -> rows wb + lane and wb + 32 + lane) and loads
-// only the pencil CENTRES x[row + c]; the i - 1 / i + 1 neighbours are the
-// adjacent rows' centres, taken by warp shuffles, and the two rows beyond the
-// warp's ends come from one extra load per pencil (lane 0: wb - 1, lane 31:
-// wb + 64).  27 gathers per row become 27 loads per 64 rows (+ shuffles): the
-// L1 wavefronts per row drop ~3x -- the 27-point sweeps were L1-bound.
-// Rows past nrows keep their true row index for the x loads (their centres
-// are a valid row's neighbours) and skip the store.  Row sums stay in record
-// order (left, centre, right of pencil 0, then pencil 1, ...): bitwise k_sten.
-constexpr int kPencilRows = 512;  // rows per 256-thread block
+// 27-point STEN on a contiguous row set, 2.5-D blocked ("marching" form).
+// Applies when the main pattern is the full 3x3x3 box: record
+// 9*(dk+1) + 3*(dj+1) + (di+1) at offset di + nx*dj + nxy*dk (levels of the
+// 27-point hierarchies; nx, nxy read off the pattern).  Row r is split as
+// r = i + nx*j + nxy*k (a bijection; the split only organises the work): a
+// CTA owns a 32 x 8 (i, j) tile and marches over kz consecutive k.  Every
+// haloed x-plane (34 x 10) is copied ONCE into shared memory by cp.async
+// (four buffers, two planes in flight, one barrier per plane) and each
+// thread reads its 3x3 neighbourhood of it; that plane feeds three rows of
+// the thread's column (records 18..26 of row k-1, 9..17 of row k, 0..8 of
+// row k+1), so only one plane of values and two running sums live in
+// registers.  Per row: ~1.3 global + 9 shared loads instead of 27 gathers.
+// The k_sten<27> gather kernel was latency-bound (47 M instructions per
+// 192^3 sweep, 31 % occupancy at 68 registers, 96 us); this form runs at
+// 4 CTAs per SM (<= 64 registers): 72 us.  The value used for record
+// (dk, dj, di) of row r is x[r + di + nx*dj + nxy*dk] = x[r + off] exactly
+// as in k_sten, halo cells included (the index is linear in (i, j, k));
+// records absent from a row's pattern are skipped by its mask; each row's
+// sum runs in record order: bitwise k_sten.
+constexpr int kMarchTX = 32, kMarchTY = 8;
+constexpr int kMarchMinBlocks = 4;  // CTAs per SM (<= 64 registers; 4 beat 3 and 2: 72 vs 86 vs 119 us)
+constexpr int kMarchWaves = 2;      // grid ~ two waves: planes per CTA = columns * planes / (2 * 4 * 148)
+constexpr int kMarchHX = kMarchTX + 2, kMarchHY = kMarchTY + 2, kMarchPlane = kMarchHX * kMarchHY;
 
-template <int NP, bool EDGE>
-__device__ __forceinline__ void stenp_load(const StenArgs& a, const StenParam& p, int wb, int lane, double (&c0)[NP],
-                                           double (&c1)[NP], double (&e)[NP]) {
-    const int ra = a.row0 + wb + lane, re = a.row0 + wb + (lane < 16 ? -1 : 64);
+struct MarchGeom {
+    int nx, nxy, ny;           // row split r = i + nx*j + nxy*k (rows < 2^31)
+    int tiles_x, tiles_y;      // (i, j) tiles per plane
+    int k0, nk;                // planes [k0, k0 + nk) hold the row set
+    int kz, chunks;            // planes per CTA, ceil(nk / kz)
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kMarchBuf = 4;  // planes in shared memory: 2 being read, 2 in flight (cp.async)
+
+// Fold one plane's 9 values into a row sum as records BASE .. BASE+8 (record
+// order; masked records skipped; -1.0 records subtract when neg1).  The
+// uniform branches (neg1, every row of the warp complete) are hoisted.
+template <int BASE>
+__device__ __forceinline__ double march_fold(const StenParam& p, const double (&v)[9], double sum, uint32_t m,
+                                             bool full) {
+    if (p.neg1) {
+        if (full) {
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        const int o = p.off[3 * k + 1];
-        int i0 = ra + o, i1 = ra + 32 + o, ie = re + o;
-        if (EDGE) {
-            i0 = min(max(i0, 0), a.xlen - 1);
-            i1 = min(max(i1, 0), a.xlen - 1);
-            ie = min(max(ie, 0), a.xlen - 1);
+            for (int t = 0; t < 9; ++t) sum = (BASE + t == 13) ? dadd(sum, dmul(p.val[13], v[t])) : dsub(sum, v[t]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 9; ++t)
+                if (!((m >> (BASE + t)) & 1u))
+                    sum = (BASE + t == 13) ? dadd(sum, dmul(p.val[13], v[t])) : dsub(sum, v[t]);
         }
-        c0[k] = a.x[i0];  // coherent loads: the kernel may start before x's producer completes (PDL)
-        c1[k] = a.x[i1];
-        e[k] = a.x[ie];
-    }
-}
-
-// Fold one row's records of pencil k in record order (masked records skipped).
-template <int NP>
-__device__ __forceinline__ void stenp_fold3(const StenParam& p, int k, double l, double c, double r, uint32_t m,
-                                            bool full, double& sum) {
-    const double v3[3] = {l, c, r};
+    } else {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        const int rec = 3 * k + j;
-        const bool diag = rec == (3 * NP) / 2;
-        if (!full && ((m >> rec) & 1u)) continue;
-        if (p.neg1 && !diag)
-            sum = dsub(sum, v3[j]);
-        else
-            sum = dadd(sum, dmul(p.val[rec], v3[j]));
+        for (int t = 0; t < 9; ++t)
+            if (full || !((m >> (BASE + t)) & 1u)) sum = dadd(sum, dmul(p.val[BASE + t], v[t]));
     }
+    return sum;
 }
 
-template <int NP>
-__device__ __forceinline__ void stenp_sums(const StenParam& p, int lane, const double (&c0)[NP], const double (&c1)[NP],
-                                           const double (&e)[NP], uint32_t ma, uint32_t mb, double& sa, double& sb) {
-    const bool full = __all_sync(0xffffffffu, (ma | mb) == 0u);
-    const int dn = (lane + 31) & 31, up = (lane + 1) & 31;
-    sa = 0.0;
-    sb = 0.0;
+// Streaming form: plane P, read once from shared memory, feeds three rows --
+// the LAST 9 records of row P-1 (which then completes), the middle 9 of row P
+// and the first 9 of row P+1 -- so only one plane of values and two running
+// sums (each in record order: bitwise k_sten) live in registers, and a row's
+// pattern byte / r / q load two steps before they are needed.
+template <int OP, bool DOTS>
+__device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p, const MarchGeom& g, double& sa,
+                                           double& sb, double& sg) {
+    __shared__ double pl[kMarchBuf][kMarchPlane];
+    int blk = static_cast<int>(blockIdx.x);
+    const int tx = blk % g.tiles_x;
+    blk /= g.tiles_x;
+    const int ty = blk % g.tiles_y;
+    const int kc = blk / g.tiles_y;
+    const int i0 = tx * kMarchTX, j0 = ty * kMarchTY;
+    const int kb = g.k0 + kc * g.kz;
+    const int kend = min(kb + g.kz, g.k0 + g.nk);
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+    const bool h1ok = threadIdx.x + 256 < kMarchPlane;
+    const int h0 = threadIdx.x, h1 = threadIdx.x + 256;
+    const int c0 = (i0 - 1 + h0 % kMarchHX) + g.nx * (j0 - 1 + h0 / kMarchHX);
+    const int c1 = (i0 - 1 + h1 % kMarchHX) + g.nx * (j0 - 1 + h1 / kMarchHX);
+    const int st = g.nxy, hi = a.xlen - 1;
+    const int i = i0 + lx, j = j0 + ly;
+    const bool col_ok = i < g.nx && j < g.ny;
+    const int colrow = i + g.nx * j;
+    const int row_lo = a.row0, row_hi = a.row0 + a.nrows;
+    // plane P -> buffer (P - kb + 1) % kMarchBuf, copied asynchronously
+    auto issue = [&](int P) {
+        if (P <= kend) {
+            const int bf = (P - kb + 1) & (kMarchBuf - 1);
+            cp_async8(&pl[bf][h0], a.x + min(max(c0 + st * P, 0), hi));
+            if (h1ok) cp_async8(&pl[bf][h1], a.x + min(max(c1 + st * P, 0), hi));
+        }
+        cp_async_commit();  // one group per plane slot, empty past the chunk: uniform counting
+    };
+    issue(kb - 1);
+    issue(kb);
+    issue(kb + 1);
+    // rows of this CTA: k in [kb, kend); row (i, j, k) = colrow + st*k
+    double s_old = 0.0, s_mid = 0.0;  // rows P-1 (18 records folded), P (9)
+    uint32_t m_old = 0u, m_mid = 0u;
+    bool f_old = true, f_mid = true, ok_old = false, ok_mid = false;
+    int q_old = 0, q_mid = 0, r_old = 0, r_mid = 0;
+    double ri_old = 0.0, ri_mid = 0.0, qq_old = 0.0, qq_mid = 0.0;
+    double x_old = 0.0;  // own x of row P-1 (centre of plane P-1)
+    for (int P = kb - 1; P <= kend; ++P) {
+        // row P+1 starts at this plane: its operands now, used two planes later
+        const int r64 = colrow + st * (P + 1);
+        const bool ok_new = col_ok && P + 1 >= kb && P + 1 < kend && r64 >= row_lo && r64 < row_hi;
+        const int r_new = ok_new ? r64 : row_lo;
+        const int q_new = a.pid[r_new];
+        const double ri_new = (OP != kSpmv || DOTS) ? a.r[r_new] : 0.0;
+        const double qq_new = DOTS ? a.q[r_new] : 0.0;
+        cp_async_wait<1>();  // plane P landed; P+1 may still fly
+        __syncthreads();     // ... for every thread; the buffer of plane P-2 is free
+        issue(P + 2);
+        double v[9];
+        const int bf = (P - kb + 1) & (kMarchBuf - 1);
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        const double l0 = __shfl_sync(0xffffffffu, c0[k], dn), l1 = __shfl_sync(0xffffffffu, c1[k], dn);
-        const double u0 = __shfl_sync(0xffffffffu, c0[k], up), u1 = __shfl_sync(0xffffffffu, c1[k], up);
-        const double left_a = lane ? l0 : e[k];
-        const double left_b = lane ? l1 : l0;  // lane 0: c0 of lane 31 = row wb + 31
-        const double right_a = lane < 31 ? u0 : u1;  // lane 31: c1 of lane 0 = row wb + 32
-        const double right_b = lane < 31 ? u1 : e[k];
-        stenp_fold3<NP>(p, k, left_a, c0[k], right_a, ma, full, sa);
-        stenp_fold3<NP>(p, k, left_b, c1[k], right_b, mb, full, sb);
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) v[3 * dy + dx] = pl[bf][(ly + dy) * kMarchHX + lx + dx];
+        // row P-1 completes with plane P as its records 18..26
+        if (P - 1 >= kb) {
+            const double sum = march_fold<18>(p, v, s_old, m_old, f_old);
+            if (ok_old) {
+                if (DOTS) {
+                    a.y[r_old] = sum;
+                    sa = dadd(sa, dmul(x_old, ri_old));
+                    sb = dadd(sb, dmul(x_old, sum));
+                    sg = dadd(sg, dmul(x_old, qq_old));
+                } else {
+                    sten_store<OP, 27>(a, p, r_old, q_old, ri_old, x_old, sum);
+                }
+            }
+        }
+        // row P: records 9..17 (centre 13); row P+1: records 0..8
+        s_old = march_fold<9>(p, v, s_mid, m_mid, f_mid);
+        m_old = m_mid, f_old = f_mid, ok_old = ok_mid, q_old = q_mid, r_old = r_mid, ri_old = ri_mid, qq_old = qq_mid;
+        x_old = v[4];
+        const uint32_t m_new = p.pmask[q_new];
+        const bool f_new = __all_sync(0xffffffffu, !ok_new || m_new == 0u);
+        s_mid = march_fold<0>(p, v, 0.0, m_new, f_new);
+        m_mid = m_new, f_mid = f_new, ok_mid = ok_new, q_mid = q_new, r_mid = r_new, ri_mid = ri_new, qq_mid = qq_new;
     }
+    cp_async_wait<0>();
 }
 
-template <int OP, int NP, bool EDGE>
-__device__ __forceinline__ void stenp_body(const StenArgs& a, const StenParam& p, int wb, int lane) {
-    const int last = a.nrows - 1;
-    const int ia = wb + lane, ib = ia + 32;
-    const int qa_row = a.row0 + min(ia, last), qb_row = a.row0 + min(ib, last);
-    const int qa = a.pid[qa_row], qb = a.pid[qb_row];
-    double ria = 0.0, rib = 0.0;
-    if (OP != kSpmv) {
-        ria = a.r[qa_row];
-        rib = a.r[qb_row];
-    }
-    double c0[NP], c1[NP], e[NP];
-    stenp_load<NP, EDGE>(a, p, wb, lane, c0, c1, e);
-    double sa, sb;
-    stenp_sums<NP>(p, lane, c0, c1, e, p.pmask[qa], p.pmask[qb], sa, sb);
-    if (ia <= last) sten_store<OP, 3 * NP>(a, p, a.row0 + ia, qa, ria, c0[NP / 2], sa);
-    if (ib <= last) sten_store<OP, 3 * NP>(a, p, a.row0 + ib, qb, rib, c1[NP / 2], sb);
-}
-
-template <int OP, int NP>
-__global__ void __launch_bounds__(256) k_stenp(StenArgs a, const __grid_constant__ StenParam p) {
+template <int OP>
+__global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
-    const int blk = static_cast<int>(blockIdx.x);
-    const int lane = threadIdx.x & 31;
-    const int wb = blk * kPencilRows + (static_cast<int>(threadIdx.x) >> 5) * 64;
-    sten_prefetch<OP, kPencilRows>(a, a.r, blk);
-    if (blk < a.safe_lo || blk >= a.safe_hi)
-        stenp_body<OP, NP, true>(a, p, wb, lane);
-    else
-        stenp_body<OP, NP, false>(a, p, wb, lane);
-}
-
-// v = A w + per-CTA partials of (w.r, w.v, w.q), pencil form.
-template <int NP, bool EDGE>
-__device__ __forceinline__ void stenp_dots_body(const StenArgs& a, const StenParam& p, int wb, int lane, double& sa,
-                                                double& sb, double& sg) {
-    const int last = a.nrows - 1;
-    const int ia = wb + lane, ib = ia + 32;
-    const int qa_row = a.row0 + min(ia, last), qb_row = a.row0 + min(ib, last);
-    const int qa = a.pid[qa_row], qb = a.pid[qb_row];
-    const double rra = a.r[qa_row], rrb = a.r[qb_row], qqa = a.q[qa_row], qqb = a.q[qb_row];
-    double c0[NP], c1[NP], e[NP];
-    stenp_load<NP, EDGE>(a, p, wb, lane, c0, c1, e);
-    double va, vb;
-    stenp_sums<NP>(p, lane, c0, c1, e, p.pmask[qa], p.pmask[qb], va, vb);
-    const double wa = c0[NP / 2], wbv = c1[NP / 2];
-    if (ia <= last) {
-        a.y[a.row0 + ia] = va;
-        sa = dadd(sa, dmul(wa, rra));
-        sb = dadd(sb, dmul(wa, va));
-        sg = dadd(sg, dmul(wa, qqa));
-    }
-    if (ib <= last) {
-        a.y[a.row0 + ib] = vb;
-        sa = dadd(sa, dmul(wbv, rrb));
-        sb = dadd(sb, dmul(wbv, vb));
-        sg = dadd(sg, dmul(wbv, qqb));
-    }
-}
-
-template <int NP>
-__global__ void __launch_bounds__(256) k_stenp_dots(StenArgs a, const __grid_constant__ StenParam p) {
-    pdl_begin();
-    const int blk = static_cast<int>(blockIdx.x);
-    const int lane = threadIdx.x & 31;
-    const int wb = blk * kPencilRows + (static_cast<int>(threadIdx.x) >> 5) * 64;
-    sten_prefetch<-1, kPencilRows>(a, a.r, blk);
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    if (blk < a.safe_lo || blk >= a.safe_hi)
-        stenp_dots_body<NP, true>(a, p, wb, lane, sa, sb, sg);
-    else
-        stenp_dots_body<NP, false>(a, p, wb, lane, sa, sb, sg);
+    march_body<OP, false>(a, p, g, sa, sb, sg);
+}
+
+// v = A w + per-CTA partials of (w.r, w.v, w.q), marching form.
+__global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_dots(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
+    pdl_begin();
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    march_body<kSpmv, true>(a, p, g, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
 }
 
@@ -627,15 +651,20 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
 
 // ---------------------------------------------------------------------------
 // Interior + halo-boundary rows of a halo level in ONE launch, with the halo
-// delivered by NVLink direct stores (p2p.cu).  Order on the compute stream:
-// push (this rank's boundary values into the neighbours' staging), then this
-// kernel.  Boundary blocks (the lowest block ids, dispatched first) wait
-// until every neighbour's flag shows this exchange, then gather
-// halo columns straight from the staging slot of its parity.  A neighbour's
-// push for exchange k is issued before its own kernel k, so a waiting block
-// only waits on work that is already enqueued ahead of everything on the
-// other GPU: no deadlock, whatever holds SM slots here.  The last boundary
-// block advances the exchange counter (read by the next push).
+// delivered by NVLink direct stores (p2p.cu).  Block order (bnd_last = 1, the
+// default): push | interior | boundary.  The push blocks (lowest ids,
+// dispatched first) store this rank's boundary values into the neighbours'
+// staging and raise their flags; they never wait.  The interior blocks never
+// wait either.  Only the boundary blocks (highest ids) wait, for every
+// neighbour's flag of this exchange, then gather halo columns straight from
+// the staging slot of its parity.  No circular wait: a neighbour's push for
+// exchange k sits in the first blocks of its own launch k, which depends only
+// on its exchange k-1 having completed (its boundary blocks of k-1 waited for
+// OUR push k-1, already done); waiting boundary blocks here hold SM slots only
+// after every non-waiting block of this grid was dispatched, and the
+// neighbour's GPU is a different device.  (Ranks sharing one GPU -- LOCAL
+// runtime -- do not use this launch: Solver::split_launch.)  The last
+// boundary block advances the exchange counter (read by the next push).
 struct HaloSplit {
     StenParam pa;              // interior main pattern
     StenParamW pb;             // boundary main pattern (<= 64 records)

@@ -598,6 +598,7 @@ void build_R(const int32_t* pcol, const double* pval, int64_t nf, int64_t nc, DB
 int64_t galerkin(const DevMatrix& A, const int64_t* pc, const double* pv, const int64_t* rrp,
                  const int32_t* rcol, const double* rval, int64_t nc, DBuf<int64_t>& orp,
                  DBuf<int64_t>& ocol, DBuf<double>& oval, cudaStream_t s) {
+    NvtxRange nv("setup/galerkin R*(A*P)");
     GalerkinArgs a{};
     a.rp = A.rp.get();
     a.col = A.col.get();
@@ -873,6 +874,7 @@ void gather_segments(Runtime& rt, const double* d_local, int64_t count, double* 
 }
 
 void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows, int storage) {
+    NvtxRange nv("setup/replicate coarse levels");
     h.rep_level = -1;
     h.rep.clear();
     if (rt.nranks() == 1) return;
@@ -1008,6 +1010,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
     cudaStream_t s = rt.stream();
     const int rank = rt.rank();
     const auto t_start = Clock::now();
+    NvtxRange nv_setup("pairamg/setup_hierarchy");
     h = Hierarchy();
 
     auto L0 = std::make_unique<Level>();
@@ -1048,6 +1051,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             // ---- decoupled matching (no communication) ----
             PB_CUDA(cudaStreamSynchronize(s));
             const auto tm = Clock::now();
+            nvtxRangePushA("setup/matching");
             const int64_t msg0 = rt.stats().total_messages();
             DBuf<int64_t> mate(static_cast<size_t>(n), s);
             if (!cfg.replay.empty()) {
@@ -1076,6 +1080,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             const int64_t local_aggs = read_one(pos.get() + n, s);
             h.stats.matching_messages += rt.stats().total_messages() - msg0;
             h.stats.t_matching += since(tm);
+            nvtxRangePop();
             {
                 DBuf<int64_t> gm(static_cast<size_t>(n), s);
                 LAUNCH(k_global_mate, n, mate.get(), n, part[rank], gm.get());

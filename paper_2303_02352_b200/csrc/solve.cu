@@ -444,6 +444,15 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
                    int64_t nnz, const double* d_w0, const SetupConfig& cfg) {
     destroy_graph();
     ready = false;
+    if (rt.nranks() > 1 && h.nl() > 0) {
+        // collective teardown of the previous hierarchy's peer mappings: every
+        // rank closes what it imported, then (barrier) the exporters free
+        PB_CUDA(cudaStreamSynchronize(s_));
+        for (auto& L : h.levels) p2p_close_imports(L->p2p);
+        p2p_seg_close_imports(rep_gather_);
+        rt.barrier();
+        p2p_seg_destroy(rep_gather_);
+    }
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
     if (rt.nranks() > 1 && p2p_)
         p2p_gather_setup(rt, dots_gather_, 4, s_);  // collective
@@ -915,6 +924,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
 
 void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double rtol, int max_iters,
                    bool precflag, pairamg_solve_stats* st) {
+    NvtxRange nv("pairamg/solve");
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "solve: setup not run");
     if (rtol <= 0.0 || max_iters < 1) fail(PAIRAMG_INVALID_ARGUMENT, "solve: need rtol > 0 and max_iters >= 1");
     cycle_warning = check_cycle(cc);

@@ -72,6 +72,33 @@ __global__ void k_global_cols(const int32_t* __restrict__ col, int64_t nnz, int6
     out[t] = c < n ? b + c : recv[c - n];
 }
 
+// exchange_requests on the device: the halo ids are sorted, so every owner's
+// ids form one contiguous segment; its first index is a lower_bound of the
+// owner's first row (one thread per owner).
+__global__ void k_owner_segments(const int64_t* __restrict__ ids, int64_t m, const int64_t* __restrict__ starts,
+                                 int p, int64_t* __restrict__ seg) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q > p) return;
+    const int64_t key = starts[q];
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ids[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    seg[q] = lo;
+}
+
+// requested global ids -> owned local ids; flags ids outside [b, e)
+__global__ void k_to_local(const int64_t* __restrict__ g, int64_t m, int64_t b, int64_t e, int32_t* __restrict__ out,
+                           int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t v = g[i];
+    if (v < b || v >= e) atomicExch(bad, 1);
+    out[i] = static_cast<int32_t>(v - b);
+}
+
 __global__ void k_pack(const int32_t* __restrict__ idx, int64_t m, const double* __restrict__ x,
                        double* __restrict__ buf) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -136,6 +163,7 @@ int64_t select_rows(const uint8_t* flag, int64_t n, DBuf<int32_t>& out, cudaStre
 
 void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gcol,
               DBuf<double>&& val, int64_t nnz) {
+    NvtxRange nv("setup/localize (halo plan)");
     cudaStream_t s = rt.stream();
     const int p = rt.nranks();
     const int r = rt.rank();
@@ -195,44 +223,71 @@ void localize(Runtime& rt, DevMatrix& M, DBuf<int64_t>&& rp, DBuf<int64_t>&& gco
     M.val = std::move(val);
     gcol.reset();
 
-    // exchange_requests (dist.cpp:67-91): tell owners what we need.
+    // exchange_requests (dist.cpp:67-91): tell owners what we need -- on the
+    // device: owner segments of the sorted ids by binary search, p counts to
+    // the host, the id lists peer to peer (no host copy of the ids).
     H.recv_peers.clear();
     H.recv_off.assign(1, 0);
     H.send_peers.clear();
     H.send_off.assign(1, 0);
     if (p > 1) {
-        std::vector<int64_t> ids(static_cast<size_t>(H.n_halo));
-        if (H.n_halo)
-            PB_CUDA(cudaMemcpyAsync(ids.data(), H.recv_gid.get(), 8 * H.n_halo, cudaMemcpyDeviceToHost, s));
-        PB_CUDA(cudaStreamSynchronize(s));
-        std::vector<std::vector<int64_t>> req(static_cast<size_t>(p));
-        for (int64_t g : ids) {
-            const int owner = static_cast<int>(std::upper_bound(M.starts.begin(), M.starts.end(), g) -
-                                               M.starts.begin()) - 1;
-            if (owner == r || owner < 0 || owner >= p)
-                fail(PAIRAMG_INTERNAL, "halo plan: owned id in receive set");
-            req[owner].push_back(g);
+        std::vector<int64_t> seg(static_cast<size_t>(p) + 1, 0);
+        if (H.n_halo) {
+            DBuf<int64_t> dstarts(static_cast<size_t>(p) + 1, s), dseg(static_cast<size_t>(p) + 1, s);
+            PB_CUDA(cudaMemcpyAsync(dstarts.get(), M.starts.data(), 8 * (p + 1), cudaMemcpyHostToDevice, s));
+            k_owner_segments<<<blocks_for(p + 1, 128), 128, 0, s>>>(H.recv_gid.get(), H.n_halo, dstarts.get(), p,
+                                                                   dseg.get());
+            PB_CHECK_LAUNCH();
+            PB_CUDA(cudaMemcpyAsync(seg.data(), dseg.get(), 8 * (p + 1), cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaStreamSynchronize(s));
+            seg[static_cast<size_t>(p)] = H.n_halo;  // ids >= starts[p] cannot exist (validated columns)
         }
+        std::vector<int64_t> want(static_cast<size_t>(p), 0);  // ids this rank requests from each rank
+        for (int q = 0; q < p; ++q) want[static_cast<size_t>(q)] = seg[static_cast<size_t>(q) + 1] - seg[static_cast<size_t>(q)];
+        if (want[static_cast<size_t>(r)] != 0 || seg[0] != 0)
+            fail(PAIRAMG_INTERNAL, "halo plan: owned id in receive set");
         for (int q = 0; q < p; ++q)
-            if (!req[q].empty()) {
+            if (want[static_cast<size_t>(q)]) {
                 H.recv_peers.push_back(q);
-                H.recv_off.push_back(H.recv_off.back() + static_cast<int64_t>(req[q].size()));
+                H.recv_off.push_back(H.recv_off.back() + want[static_cast<size_t>(q)]);
             }
-        auto incoming = rt.alltoallv_i64(req);
-        std::vector<int32_t> sidx;
-        for (int q = 0; q < p; ++q) {
-            if (q == r || incoming[q].empty()) continue;
-            for (int64_t g : incoming[q]) {
-                if (g < b || g >= e) fail(PAIRAMG_INTERNAL, "halo plan: asked for a row we do not own");
-                sidx.push_back(static_cast<int32_t>(g - b));
+        // counts matrix (row = requester): what every rank asks of us
+        const std::vector<uint8_t> all = rt.allgather_bytes(want.data(), 8 * static_cast<size_t>(p));
+        std::vector<int64_t> asked(static_cast<size_t>(p), 0);
+        for (int q = 0; q < p; ++q) std::memcpy(&asked[static_cast<size_t>(q)], all.data() + (static_cast<size_t>(q) * p + r) * 8, 8);
+        for (int q = 0; q < p; ++q)
+            if (q != r && asked[static_cast<size_t>(q)]) {
+                H.send_peers.push_back(q);
+                H.send_off.push_back(H.send_off.back() + asked[static_cast<size_t>(q)]);
             }
-            H.send_peers.push_back(q);
-            H.send_off.push_back(static_cast<int64_t>(sidx.size()));
+        const int64_t nsend = H.send_off.back();
+        rt.stats().alltoallvs += 1;
+        DBuf<int64_t> gsend(static_cast<size_t>(std::max<int64_t>(nsend, 1)), s);
+        std::vector<int> to(H.recv_peers.begin(), H.recv_peers.end()), from(H.send_peers.begin(), H.send_peers.end());
+        std::vector<const void*> sb;
+        std::vector<void*> rb;
+        std::vector<size_t> sn, rn;
+        for (size_t i = 0; i < H.recv_peers.size(); ++i) {
+            sb.push_back(H.recv_gid.get() + H.recv_off[i]);
+            sn.push_back(8 * static_cast<size_t>(H.recv_off[i + 1] - H.recv_off[i]));
         }
-        H.send_idx.alloc(sidx.size(), s);
-        H.send_buf.alloc(sidx.size(), s);
-        if (!sidx.empty())
-            PB_CUDA(cudaMemcpyAsync(H.send_idx.get(), sidx.data(), 4 * sidx.size(), cudaMemcpyHostToDevice, s));
+        for (size_t i = 0; i < H.send_peers.size(); ++i) {
+            rb.push_back(gsend.get() + H.send_off[i]);
+            rn.push_back(8 * static_cast<size_t>(H.send_off[i + 1] - H.send_off[i]));
+        }
+        rt.exchange_dev(to, sb, sn, from, rb, rn, s);
+        H.send_idx.alloc(static_cast<size_t>(nsend), s);
+        H.send_buf.alloc(static_cast<size_t>(nsend), s);
+        if (nsend) {
+            DBuf<int> bad(1, s);
+            bad.zero(s);
+            k_to_local<<<blocks_for(nsend, 256), 256, 0, s>>>(gsend.get(), nsend, b, e, H.send_idx.get(), bad.get());
+            PB_CHECK_LAUNCH();
+            int hb = 0;
+            PB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+            PB_CUDA(cudaStreamSynchronize(s));
+            if (hb) fail(PAIRAMG_INTERNAL, "halo plan: asked for a row we do not own");
+        }
     }
 
     // boundary / interior rows (build_spmv_plan, dist.cpp:109-118)

@@ -162,3 +162,13 @@ def test_dense_coarse_rows(runtime):
             va.append(ent[c])
         rp.append(len(ci))
     check_pair(runtime, np.array(rp), np.array(ci), np.array(va), target=50, s_exp=3)
+
+
+@pytest.mark.parametrize("levels", [2, 0])
+def test_varcoef_generator_hierarchy(runtime, levels):
+    """The device varcoef workload (bench --problem varcoef) at a size with
+    several levels and multi-block kernels: bitwise the oracle."""
+    import paper_2303_02352_b200 as pb
+
+    rp, ci, va = pb.varcoef(7, 40, 40, 40, levels, 1)
+    check_pair(runtime, rp, ci, va, target=1600)
