@@ -379,6 +379,8 @@ def bench_ours(args, rank, world, local_rank):
     s.solve(b, u)
     s.set_kernel_timing(False)
     kt = [s.kernel_timing(k) for k in range(4)]
+    # per-level V-cycle time per iteration (class 4 + k: entry to restriction + return to exit)
+    level_us = [1e3 * s.kernel_timing(4 + k)["ms"] / max(1, it) for k in range(min(s.num_levels, 16))]
     peak, peak_src = measured_peaks()
     li0 = s.level_info(0)
     fmt0 = s.level_storage(0)
@@ -452,6 +454,7 @@ def bench_ours(args, rank, world, local_rank):
         "iterations": it, "final_relres": st.final_relres, "ms_per_iter": t_solve * 1e3 / it,
         "setup_s": min(setup_times), "setup_breakdown": {k: sstats[k] for k in ("t_matching", "t_spmm", "t_spmm_comm")},
         "levels": sstats["levels"], "opc": sstats["opc"],
+        "vcycle_level_us_per_iter": level_us,
         "spmv_gbs": spmv_gbs, "spmv_frac_hbm": spmv_gbs / peak if spmv_gbs else None,
         "roofline": {"bound": "hbm", "kernel": f"level-0 l1-Jacobi sweep, {sweep_kernel}", "storage": fmt0,
                      "bytes_model": "algorithmic bytes of the stored format: pattern/code/column+value bytes + x, r, "

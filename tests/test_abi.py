@@ -104,3 +104,56 @@ def test_no_load_ahead_of_grid_dependency_wait(lib):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "check_pdl_sass.py")], capture_output=True,
                        text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _splitmix_coef(c, seed, levels):
+    import numpy as np
+
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * (c.astype(np.uint64) + np.uint64(1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    if levels > 0:
+        return 1.0 + (z % np.uint64(levels)).astype(np.float64)
+    return 0.5 + (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def test_host_varcoef_generator(lib):
+    """pairamg_varcoef_host = its definition (include/pairamg_b200.h): Poisson
+    sparsity, couplings -(k_i + k_j)/2, diagonal = sum over the stencil
+    directions (k_i across the boundary), symmetric, diagonally dominant."""
+    import numpy as np
+
+    import paper_2303_02352_b200 as pb
+
+    for st, dims, levels in ((7, (5, 4, 6), 2), (7, (6, 5, 4), 0), (27, (4, 5, 3), 3)):
+        nx, ny, nz = dims
+        n = nx * ny * nz
+        rp, ci, va = pb.varcoef(st, nx, ny, nz, levels, 7)
+        prp, pci, _ = pb.poisson(st, nx, ny, nz)
+        np.testing.assert_array_equal(rp, prp)
+        np.testing.assert_array_equal(ci, pci)
+        k = _splitmix_coef(np.arange(n), 7, levels)
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        off = ci != rows
+        np.testing.assert_array_equal(va[off], -((k[rows[off]] + k[ci[off]]) * 0.5))
+        A = np.zeros((n, n))
+        A[rows, ci] = va
+        np.testing.assert_array_equal(A, A.T)
+        d = np.diag(A)
+        assert np.all(d >= np.abs(A - np.diag(d)).sum(axis=1) - 1e-12)
+        # diagonal: every direction's (k_i + k_j)/2, or k_i across the boundary, summed in direction order
+        for r in (0, n // 2, n - 1):
+            i, j, kk = r % nx, (r // nx) % ny, r // (nx * ny)
+            s = 0.0
+            for dk in (-1, 0, 1):
+                for dj in (-1, 0, 1):
+                    for di in (-1, 0, 1):
+                        man = (di != 0) + (dj != 0) + (dk != 0)
+                        if man == 0 or (st == 7 and man > 1):
+                            continue
+                        ii, jj, k2 = i + di, j + dj, kk + dk
+                        inside = 0 <= ii < nx and 0 <= jj < ny and 0 <= k2 < nz
+                        s = s + ((k[r] + k[ii + nx * (jj + ny * k2)]) * 0.5 if inside else k[r])
+            assert A[r, r] == s
