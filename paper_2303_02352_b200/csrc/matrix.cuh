@@ -168,6 +168,9 @@ struct HaloSrc {
 // Interior (contiguous STEN) + boundary (STEN) rows in one launch; the
 // boundary blocks wait for the neighbours' pushes of this exchange.
 bool sell_split_ok(const Sell& interior, const Sell& boundary);
+// The row set runs the 27-point marching kernels (sell_sten.cuh): contiguous
+// rows, full 3x3x3 main pattern, large enough for two waves of 4 CTAs/SM.
+bool sell_march_ok(const Sell& S);
 // STEN with a main pattern of up to 64 records (split-launch boundary rows
 // only); false (S unusable) when the rows do not nest into one.
 bool build_sten_wide(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S, cudaStream_t s,

@@ -1481,6 +1481,8 @@ bool sell_coarse_solve(const Sell& S, const double* rhs, double* x, int nu, doub
     return true;
 }
 
+bool sell_march_ok(const Sell& S) { return S.format == Sell::kSten && sten_march(S); }
+
 bool sell_split_ok(const Sell& I, const Sell& B) {
     return I.format == Sell::kSten && B.format == Sell::kSten && I.rows.empty() && I.nrows > 0 && B.nrows > 0;
 }

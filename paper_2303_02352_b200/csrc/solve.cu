@@ -593,9 +593,15 @@ void Solver::exchange(Level& L, const double* x, cudaStream_t st) {
 // One launch for interior + boundary rows whose boundary blocks wait for the
 // neighbours' pushes.  Not when ranks share a GPU (LOCAL runtime): a grid
 // whose last blocks wait on a peer's kernel could hold every SM slot.
+// Interior rows that run the 27-point marching kernels take the
+// exchange-on-the-communication-stream schedule instead: the marching
+// kernel (72 us at 192^3) beats the split launch's interior gathers.
 bool Solver::split_launch(const Level& L) const {
-    return L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) && !rt.shared_device();
+    return L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) && !rt.shared_device() &&
+           !sell_march_ok(L.sell_int);
 }
+
+int Solver::interior_cap(const Level& L) const { return sell_march_ok(L.sell_int) ? 0 : halo_grid_; }
 
 void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
     begin_time(kc);
@@ -638,7 +644,7 @@ void Solver::apply_on(Level& L, const SellOpArgs& o, int kc) {
         // boundary kernels (else they only run once every interior CTA has
         // been dispatched; measured: halo done at 91 us of an 89 us interior)
         SellOpArgs oi = o;
-        oi.max_grid = halo_grid_;
+        oi.max_grid = interior_cap(L);
         sell_apply(L.sell_int, oi, s_);
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         launches_ += 1;
@@ -872,7 +878,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
                                           max_blocks_, hs, s_);
         launches_ += hs.fused ? 1 : 2;
     } else if (L0.A.halo.n_halo > 0) {  // boundary rows behind the halo, on the comm stream
-        const int g1 = sell_dots_grid(L0.sell_int, halo_grid_);
+        const int g1 = sell_dots_grid(L0.sell_int, interior_cap(L0));
         PB_CUDA(cudaEventRecord(ev_fork_, s_));
         PB_CUDA(cudaStreamWaitEvent(rt.comm_stream(), ev_fork_, 0));
         exchange(L0, w, rt.comm_stream());
@@ -880,7 +886,7 @@ void Solver::iteration_enqueue(const CycleConfig& cc, bool precflag) {
                                       max_blocks_ - g1, rt.comm_stream());
         PB_CUDA(cudaEventRecord(ev_join_, rt.comm_stream()));
         const int g1b = sell_spmv_dots(L0.sell_int, w, v_.get(), r_.get(), q_.get(), partials_.get(), g1, s_,
-                                       halo_grid_);
+                                       interior_cap(L0));
         if (g1b != g1) fail(PAIRAMG_INTERNAL, "spmv+dots: interior partial count changed");
         PB_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         dots_grid_ = g1 + g2;

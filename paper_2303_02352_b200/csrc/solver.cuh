@@ -83,6 +83,7 @@ private:
     void apply_on(Level& L, const SellOpArgs& o, int kclass);
     void exchange(Level& L, const double* x, cudaStream_t st);
     bool split_launch(const Level& L) const;
+    int interior_cap(const Level& L) const;  // CTA cap of the interior launch next to a halo exchange
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
     void iteration_enqueue(const CycleConfig& cc, bool precflag);
