@@ -9,6 +9,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 
 #include <cuda.h>
 #include <unistd.h>
@@ -119,6 +120,35 @@ const std::vector<const void*>& Runtime::hub_gather(const void* mine) {
 
 void Runtime::hub_release() { hub_->wait_all(rank_); }
 
+void Runtime::wait(cudaStream_t s) {
+    if (!comm_) {
+        PB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    static const int timeout_s = env_int("PAIRAMG_NCCL_TIMEOUT_S", 600);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) PB_CUDA(q);
+        ncclResult_t ae = ncclSuccess;
+        PB_NCCL(ncclCommGetAsyncError(comm_, &ae));
+        if (ae != ncclSuccess && ae != ncclInProgress) {
+            ncclCommAbort(comm_);
+            comm_ = nullptr;
+            fail(PAIRAMG_INTERNAL, "rank " + std::to_string(rank_) + ": NCCL asynchronous error " +
+                                       ncclGetErrorString(ae) + " (a peer rank failed?)");
+        }
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(timeout_s)) {
+            ncclCommAbort(comm_);
+            comm_ = nullptr;
+            fail(PAIRAMG_DEADLOCK, "rank " + std::to_string(rank_) + ": collective did not complete in " +
+                                       std::to_string(timeout_s) + " s");
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
 void Runtime::barrier() {
     if (nranks_ == 1) return;
     if (hub_) {
@@ -196,7 +226,7 @@ void Runtime::warmup() {
     PB_NCCL(ncclGroupEnd());
     PB_NCCL(ncclAllGather(buf.get(), buf.get() + 2 * nranks_, 1, ncclDouble, comm_, stream_));
     PB_NCCL(ncclAllReduce(buf.get(), buf.get() + 3 * nranks_, 1, ncclDouble, ncclSum, comm_, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
 }
 
 Runtime::~Runtime() {
@@ -223,7 +253,7 @@ std::vector<int64_t> Runtime::allgather_i64(int64_t x) {
     PB_CUDA(cudaMemcpyAsync(d.get() + nranks_, &x, 8, cudaMemcpyHostToDevice, stream_));
     PB_NCCL(ncclAllGather(d.get() + nranks_, d.get(), 1, ncclInt64, comm_, stream_));
     PB_CUDA(cudaMemcpyAsync(out.data(), d.get(), 8 * nranks_, cudaMemcpyDeviceToHost, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
     return out;
 }
 
@@ -244,7 +274,7 @@ std::vector<uint8_t> Runtime::allgather_bytes(const void* data, size_t n) {
     PB_CUDA(cudaMemcpyAsync(d.get() + nranks_ * n, data, n, cudaMemcpyHostToDevice, stream_));
     PB_NCCL(ncclAllGather(d.get() + nranks_ * n, d.get(), n, ncclUint8, comm_, stream_));
     PB_CUDA(cudaMemcpyAsync(out.data(), d.get(), static_cast<size_t>(nranks_) * n, cudaMemcpyDeviceToHost, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
     return out;
 }
 
@@ -288,7 +318,7 @@ std::vector<std::vector<int64_t>> Runtime::alltoallv_i64(
     PB_NCCL(ncclAllGather(dc.get() + p * p, dc.get(), p, ncclInt64, comm_, stream_));
     std::vector<int64_t> counts(static_cast<size_t>(p) * p);
     PB_CUDA(cudaMemcpyAsync(counts.data(), dc.get(), 8 * p * p, cudaMemcpyDeviceToHost, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
     int64_t send_total = 0, recv_total = 0;
     for (int d = 0; d < p; ++d) {
         if (d == rank_) continue;
@@ -322,7 +352,7 @@ std::vector<std::vector<int64_t>> Runtime::alltoallv_i64(
     std::vector<int64_t> flat(static_cast<size_t>(recv_total));
     if (recv_total)
         PB_CUDA(cudaMemcpyAsync(flat.data(), rbuf.get(), 8 * recv_total, cudaMemcpyDeviceToHost, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
     ro = 0;
     for (int s = 0; s < p; ++s) {
         if (s == rank_) continue;
@@ -345,23 +375,23 @@ void Runtime::allgather_f64(const double* send, double* recv, size_t count, cuda
 void Runtime::allgather_dev(const void* send, void* recv, size_t bytes) {
     if (nranks_ == 1) {
         if (bytes) PB_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, stream_));
-        PB_CUDA(cudaStreamSynchronize(stream_));
+        wait(stream_);
         return;
     }
     stats_.allgathers += 1;
     if (hub_) {
-        PB_CUDA(cudaStreamSynchronize(stream_));
+        wait(stream_);
         const auto& p = hub_gather(send);
         for (int r = 0; r < nranks_; ++r)
             if (bytes)
                 PB_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + r * bytes, p[static_cast<size_t>(r)], bytes,
                                         cudaMemcpyDefault, stream_));
-        PB_CUDA(cudaStreamSynchronize(stream_));
+        wait(stream_);
         hub_release();
         return;
     }
     PB_NCCL(ncclAllGather(send, recv, bytes, ncclChar, comm_, stream_));
-    PB_CUDA(cudaStreamSynchronize(stream_));
+    wait(stream_);
 }
 
 namespace {

@@ -98,6 +98,12 @@ public:
                       const std::vector<size_t>& send_bytes, const std::vector<int>& recv_from,
                       const std::vector<void*>& recvs, const std::vector<size_t>& recv_bytes, cudaStream_t s);
     void barrier();
+    // Synchronise stream s, polling NCCL's asynchronous error state and a
+    // deadlock timeout (PAIRAMG_NCCL_TIMEOUT_S, default 600 s) while waiting,
+    // as the reference's timed receive does (runtime.cpp:184-205): a peer
+    // failure or a hang becomes PAIRAMG_INTERNAL / PAIRAMG_DEADLOCK instead of
+    // blocking forever.  A plain cudaStreamSynchronize for one rank.
+    void wait(cudaStream_t s);
 
     // Device-level: gather `count` doubles from every rank into recv
     // (nranks*count), enqueued on stream s (graph-capturable; NCCL only).

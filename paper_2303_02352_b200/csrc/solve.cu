@@ -1041,7 +1041,7 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
                 PB_CUDA(cudaGraphLaunch(graph_, s_));
                 launches_ += per_iter_launches_;
                 PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
-                PB_CUDA(cudaStreamSynchronize(s_));
+                rt.wait(s_);  // NCCL error / deadlock polling while the iteration runs
                 collect_times();
                 if (h_state_->status)
                     fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(h_state_->it));
