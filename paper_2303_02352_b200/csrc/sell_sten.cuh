@@ -430,6 +430,7 @@ constexpr int kMarchWaves = 2;      // grid ~ two waves: planes per CTA = column
 constexpr int kMarchHX = kMarchTX + 2, kMarchHY = kMarchTY + 2, kMarchPlane = kMarchHX * kMarchHY;
 
 struct MarchGeom {
+    int st;                    // 27 or 7 points
     int nx, nxy, ny;           // row split r = i + nx*j + nxy*k (rows < 2^31)
     int tiles_x, tiles_y;      // (i, j) tiles per plane
     int k0, nk;                // planes [k0, k0 + nk) hold the row set
@@ -446,36 +447,90 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 constexpr int kMarchBuf = 4;  // planes in shared memory: 2 being read, 2 in flight (cp.async)
 
-// Fold one plane's 9 values into a row sum as records BASE .. BASE+8 (record
-// order; masked records skipped; -1.0 records subtract when neg1).  The
-// uniform branches (neg1, every row of the warp complete) are hoisted.
-template <int BASE>
-__device__ __forceinline__ double march_fold(const StenParam& p, const double (&v)[9], double sum, uint32_t m,
-                                             bool full) {
+// Fold N values into a row sum as records BASE .. BASE+N-1 (record order;
+// masked records skipped; records other than the diagonal DIAG subtract
+// when neg1).  The uniform branches (neg1, every row of the warp complete)
+// are hoisted out of the record loop.
+template <int BASE, int N, int DIAG>
+__device__ __forceinline__ double march_fold(const StenParam& p, const double* v, double sum, uint32_t m, bool full) {
     if (p.neg1) {
         if (full) {
 #pragma unroll
-            for (int t = 0; t < 9; ++t) sum = (BASE + t == 13) ? dadd(sum, dmul(p.val[13], v[t])) : dsub(sum, v[t]);
+            for (int t = 0; t < N; ++t) sum = (BASE + t == DIAG) ? dadd(sum, dmul(p.val[DIAG], v[t])) : dsub(sum, v[t]);
         } else {
 #pragma unroll
-            for (int t = 0; t < 9; ++t)
+            for (int t = 0; t < N; ++t)
                 if (!((m >> (BASE + t)) & 1u))
-                    sum = (BASE + t == 13) ? dadd(sum, dmul(p.val[13], v[t])) : dsub(sum, v[t]);
+                    sum = (BASE + t == DIAG) ? dadd(sum, dmul(p.val[DIAG], v[t])) : dsub(sum, v[t]);
         }
     } else {
 #pragma unroll
-        for (int t = 0; t < 9; ++t)
+        for (int t = 0; t < N; ++t)
             if (full || !((m >> (BASE + t)) & 1u)) sum = dadd(sum, dmul(p.val[BASE + t], v[t]));
     }
     return sum;
 }
 
-// Streaming form: plane P, read once from shared memory, feeds three rows --
-// the LAST 9 records of row P-1 (which then completes), the middle 9 of row P
-// and the first 9 of row P+1 -- so only one plane of values and two running
-// sums (each in record order: bitwise k_sten) live in registers, and a row's
-// pattern byte / r / q load two steps before they are needed.
-template <int OP, bool DOTS>
+// What one plane contributes to the three rows of a column, per stencil.
+// 27 points: the 3x3 neighbourhood (9 shared loads) is records 0-8 of the
+// row above, 9-17 (diagonal 13) of the row in the plane, 18-26 of the row
+// below.  7 points: the centre is record 0 of the row above and record 6 of
+// the row below; the cross (j-1, i-1, centre, i+1, j+1) is records 1-5
+// (diagonal 3) of the row in the plane (5 shared loads).
+template <int ST>
+struct MarchPlane;
+
+template <>
+struct MarchPlane<27> {
+    static constexpr int kL = 27;
+    double v[9];
+    __device__ __forceinline__ void load(const double* buf, int lx, int ly) {
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) v[3 * dy + dx] = buf[(ly + dy) * kMarchHX + lx + dx];
+    }
+    __device__ __forceinline__ double centre() const { return v[4]; }
+    __device__ __forceinline__ double first(const StenParam& p, uint32_t m, bool f) const {
+        return march_fold<0, 9, 13>(p, v, 0.0, m, f);
+    }
+    __device__ __forceinline__ double mid(const StenParam& p, double s, uint32_t m, bool f) const {
+        return march_fold<9, 9, 13>(p, v, s, m, f);
+    }
+    __device__ __forceinline__ double last(const StenParam& p, double s, uint32_t m, bool f) const {
+        return march_fold<18, 9, 13>(p, v, s, m, f);
+    }
+};
+
+template <>
+struct MarchPlane<7> {
+    static constexpr int kL = 7;
+    double c5[5];  // j-1, i-1, centre, i+1, j+1 (record order of the row in the plane)
+    __device__ __forceinline__ void load(const double* buf, int lx, int ly) {
+        c5[0] = buf[ly * kMarchHX + lx + 1];
+        c5[1] = buf[(ly + 1) * kMarchHX + lx];
+        c5[2] = buf[(ly + 1) * kMarchHX + lx + 1];
+        c5[3] = buf[(ly + 1) * kMarchHX + lx + 2];
+        c5[4] = buf[(ly + 2) * kMarchHX + lx + 1];
+    }
+    __device__ __forceinline__ double centre() const { return c5[2]; }
+    __device__ __forceinline__ double first(const StenParam& p, uint32_t m, bool f) const {
+        return march_fold<0, 1, 3>(p, &c5[2], 0.0, m, f);
+    }
+    __device__ __forceinline__ double mid(const StenParam& p, double s, uint32_t m, bool f) const {
+        return march_fold<1, 5, 3>(p, c5, s, m, f);
+    }
+    __device__ __forceinline__ double last(const StenParam& p, double s, uint32_t m, bool f) const {
+        return march_fold<6, 1, 3>(p, &c5[2], s, m, f);
+    }
+};
+
+// Streaming form: plane P, read once from shared memory, feeds three rows of
+// the thread's column -- the last records of row P-1 (which then completes),
+// the middle records of row P and the first of row P+1 -- so one plane of
+// values and two running sums (each in record order: bitwise k_sten) live in
+// registers, and a row's pattern byte / r / q load two planes before use.
+template <int ST, int OP, bool DOTS>
 __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p, const MarchGeom& g, double& sa,
                                            double& sb, double& sg) {
     __shared__ double pl[kMarchBuf][kMarchPlane];
@@ -510,7 +565,7 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
     issue(kb);
     issue(kb + 1);
     // rows of this CTA: k in [kb, kend); row (i, j, k) = colrow + st*k
-    double s_old = 0.0, s_mid = 0.0;  // rows P-1 (18 records folded), P (9)
+    double s_old = 0.0, s_mid = 0.0;  // rows P-1 and P, their records before plane P folded
     uint32_t m_old = 0u, m_mid = 0u;
     bool f_old = true, f_mid = true, ok_old = false, ok_mid = false;
     int q_old = 0, q_mid = 0, r_old = 0, r_mid = 0;
@@ -527,15 +582,10 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
         cp_async_wait<1>();  // plane P landed; P+1 may still fly
         __syncthreads();     // ... for every thread; the buffer of plane P-2 is free
         issue(P + 2);
-        double v[9];
-        const int bf = (P - kb + 1) & (kMarchBuf - 1);
-#pragma unroll
-        for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx) v[3 * dy + dx] = pl[bf][(ly + dy) * kMarchHX + lx + dx];
-        // row P-1 completes with plane P as its records 18..26
-        if (P - 1 >= kb) {
-            const double sum = march_fold<18>(p, v, s_old, m_old, f_old);
+        MarchPlane<ST> v;
+        v.load(pl[(P - kb + 1) & (kMarchBuf - 1)], lx, ly);
+        if (P - 1 >= kb) {  // row P-1 completes
+            const double sum = v.last(p, s_old, m_old, f_old);
             if (ok_old) {
                 if (DOTS) {
                     a.y[r_old] = sum;
@@ -543,34 +593,34 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
                     sb = dadd(sb, dmul(x_old, sum));
                     sg = dadd(sg, dmul(x_old, qq_old));
                 } else {
-                    sten_store<OP, 27>(a, p, r_old, q_old, ri_old, x_old, sum);
+                    sten_store<OP, ST>(a, p, r_old, q_old, ri_old, x_old, sum);
                 }
             }
         }
-        // row P: records 9..17 (centre 13); row P+1: records 0..8
-        s_old = march_fold<9>(p, v, s_mid, m_mid, f_mid);
+        s_old = v.mid(p, s_mid, m_mid, f_mid);  // row P
         m_old = m_mid, f_old = f_mid, ok_old = ok_mid, q_old = q_mid, r_old = r_mid, ri_old = ri_mid, qq_old = qq_mid;
-        x_old = v[4];
+        x_old = v.centre();
         const uint32_t m_new = p.pmask[q_new];
         const bool f_new = __all_sync(0xffffffffu, !ok_new || m_new == 0u);
-        s_mid = march_fold<0>(p, v, 0.0, m_new, f_new);
+        s_mid = v.first(p, m_new, f_new);  // row P+1
         m_mid = m_new, f_mid = f_new, ok_mid = ok_new, q_mid = q_new, r_mid = r_new, ri_mid = ri_new, qq_mid = qq_new;
     }
     cp_async_wait<0>();
 }
 
-template <int OP>
+template <int ST, int OP>
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<OP, false>(a, p, g, sa, sb, sg);
+    march_body<ST, OP, false>(a, p, g, sa, sb, sg);
 }
 
 // v = A w + per-CTA partials of (w.r, w.v, w.q), marching form.
+template <int ST>
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_dots(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<kSpmv, true>(a, p, g, sa, sb, sg);
+    march_body<ST, kSpmv, true>(a, p, g, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
 }
 
