@@ -186,3 +186,33 @@ def test_local_ranks_marching_interior_with_halos():
         assert np.array_equal(bits(got), bits(one[key])), key
     assert two[0]["iters"] == one["iters"]
     np.testing.assert_allclose(two[0]["hist"], one["hist"], rtol=1e-8)
+
+
+def test_local_ranks_585_iterations_match_reference():
+    """configs[3] (7-point 585^3, 200 M unknowns) at p = 4 and 8 ranks sharing one
+    B200: the reference's own iteration counts at those partitions
+    (tests/golden/ref_counts.json: 88 and 94, measured by oracle/_ref on the
+    GPU box's host) within +-1.  Odd grid: the total-order matching differs from
+    the reference's on coarse steps, so this is the north star's +-1 criterion
+    on the real config, not a bitwise one."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(0)
+    if free < 150e9:
+        pytest.skip("needs ~150 GB of free device memory")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "ref_counts.json")) as f:
+        ref = {r["p"]: r["iterations"] for r in json.load(f)["runs"] if r.get("grid") == [585, 585, 585]}
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "run_local_big.py"), "585", "4", "8"],
+                       capture_output=True, text=True, timeout=1500, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for p in (4, 8):
+        g = got[str(p)]
+        assert g["relres"] < 1e-6 and g["reductions_per_iter"] == 1
+        assert abs(g["iterations"] - ref[p]) <= 1, (p, g["iterations"], ref[p])
