@@ -219,10 +219,12 @@ def bench_reference(args, world):
     t0 = time.time()
     o.setup()
     setup_s = time.time() - t0
-    k = args.ref_sample_iters
-    o.set_solve(1e-6, k)
+    o.set_solve(1e-6, 1)
     r = o.solve()
     ms_iter0 = 1e3 * r["t_solve"] / max(r["iterations"], 1)
+    # iterations per step: up to --ref-sample-iters, a step of at most ~3 s
+    k = max(1, min(args.ref_sample_iters, int(3000.0 / max(ms_iter0, 1e-3))))
+    o.set_solve(1e-6, k)
     iters_full, full_s, full_rel = None, None, None
     if ms_iter0 * 1e-3 * 60 < args.ref_full_budget_s:
         o.set_solve(1e-6, 1000)
