@@ -1007,32 +1007,15 @@ inline int capped(int nblk, int cap) { return cap > 0 ? std::min(nblk, cap) : nb
 // + (di+1) at offset di + nx dj + nxy dk) on contiguous rows: the marching
 // kernels apply (sell_sten.cuh).  Fills the geometry of the row set.
 bool sten_march(const Sell& S, MarchGeom* out = nullptr) {
-    static const int which = env_int("PAIRAMG_MARCH", 27);  // A/B: 34 = 7- and 27-point (7-point form under measurement)
-    if ((S.sten_L != 27 && S.sten_L != 7) || !S.rows.empty() || !sten_center(S) || S.nrows == 0) return false;
-    if (!(which == 34 || which == S.sten_L)) return false;
+    if (S.sten_L != 27 || !S.rows.empty() || !sten_center(S) || S.nrows == 0) return false;
     const auto& o = S.sten_off;
-    int nx = 0, nxy = 0;
-    if (S.sten_L == 27) {
-        nx = o[16] - o[13];
-        nxy = o[22] - o[13];
-    } else {
-        nx = o[5] - o[3];
-        nxy = o[6] - o[3];
-    }
+    const int nx = o[16] - o[13], nxy = o[22] - o[13];
     if (nx < 2 || nxy < 2 * nx || nxy % nx) return false;
-    if (S.sten_L == 27) {
-        for (int dk = -1; dk <= 1; ++dk)
-            for (int dj = -1; dj <= 1; ++dj)
-                for (int di = -1; di <= 1; ++di)
-                    if (o[static_cast<size_t>(9 * (dk + 1) + 3 * (dj + 1) + di + 1)] != di + nx * dj + nxy * dk)
-                        return false;
-    } else {
-        const int want[7] = {-nxy, -nx, -1, 0, 1, nx, nxy};
-        for (int k = 0; k < 7; ++k)
-            if (o[static_cast<size_t>(k)] != want[k]) return false;
-    }
+    for (int dk = -1; dk <= 1; ++dk)
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int di = -1; di <= 1; ++di)
+                if (o[static_cast<size_t>(9 * (dk + 1) + 3 * (dj + 1) + di + 1)] != di + nx * dj + nxy * dk) return false;
     MarchGeom g{};
-    g.st = S.sten_L;
     g.nx = nx;
     g.nxy = nxy;
     g.ny = nxy / nx;
@@ -1058,7 +1041,7 @@ void launch_sten(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s) {
     const StenParam p = sten_param(S);
     MarchGeom g;
     if (!ROWS && cap == 0 && sten_march(S, &g)) {
-        launch_k<2>(g.st == 27 ? k_sten_march<27, OP> : k_sten_march<7, OP>, march_grid(g), 256, 0, s, a0, p, g);
+        launch_k<2>(k_sten_march<OP>, march_grid(g), 256, 0, s, a0, p, g);
         return;
     }
     if (sten_rpt2(S)) {
@@ -1091,7 +1074,7 @@ int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s)
     const StenParam p = sten_param(S);
     MarchGeom g;
     if (!ROWS && cap == 0 && sten_march(S, &g)) {
-        launch_k<2>(g.st == 27 ? k_sten_march_dots<27> : k_sten_march_dots<7>, march_grid(g), 256, 0, s, a0, p, g);
+        launch_k<2>(k_sten_march_dots, march_grid(g), 256, 0, s, a0, p, g);
         return march_grid(g);
     }
     if (sten_rpt2(S, true)) {
@@ -1353,9 +1336,11 @@ void build_sell(const DevMatrix& M, const int32_t* rows, int64_t nrows, Sell& S,
                 reset_pat(S);
             }
             if (want_pat && try_pattern(M, rows, S, l1, s)) return;
-            if (try_dict(M, rows, S, l1, s)) return;
             if (!want_pat && try_pattern(M, rows, S, l1, s)) return;
+            // CODED before DICT: with per-entry values DICT's lookups diverge
+            // (varcoef 256^3 level-0 sweep: CODED 202 us, DICT 258 us)
             if (try_coded(M, rows, S, s)) return;
+            if (try_dict(M, rows, S, l1, s)) return;
         } else if (storage == Sell::kSten) {
             if (maxlen <= kStenMax && try_pattern(M, rows, S, l1, s)) {
                 if (try_sten(S)) return;

@@ -430,7 +430,6 @@ constexpr int kMarchWaves = 2;      // grid ~ two waves: planes per CTA = column
 constexpr int kMarchHX = kMarchTX + 2, kMarchHY = kMarchTY + 2, kMarchPlane = kMarchHX * kMarchHY;
 
 struct MarchGeom {
-    int st;                    // 27 or 7 points
     int nx, nxy, ny;           // row split r = i + nx*j + nxy*k (rows < 2^31)
     int tiles_x, tiles_y;      // (i, j) tiles per plane
     int k0, nk;                // planes [k0, k0 + nk) hold the row set
@@ -471,18 +470,9 @@ __device__ __forceinline__ double march_fold(const StenParam& p, const double* v
     return sum;
 }
 
-// What one plane contributes to the three rows of a column, per stencil.
-// 27 points: the 3x3 neighbourhood (9 shared loads) is records 0-8 of the
-// row above, 9-17 (diagonal 13) of the row in the plane, 18-26 of the row
-// below.  7 points: the centre is record 0 of the row above and record 6 of
-// the row below; the cross (j-1, i-1, centre, i+1, j+1) is records 1-5
-// (diagonal 3) of the row in the plane (5 shared loads).
-template <int ST>
-struct MarchPlane;
-
-template <>
-struct MarchPlane<27> {
-    static constexpr int kL = 27;
+// The 3x3 neighbourhood of a plane (9 shared loads): records 0-8 of the row
+// above, 9-17 (diagonal 13) of the row in the plane, 18-26 of the row below.
+struct MarchPlane {
     double v[9];
     __device__ __forceinline__ void load(const double* buf, int lx, int ly) {
 #pragma unroll
@@ -502,35 +492,12 @@ struct MarchPlane<27> {
     }
 };
 
-template <>
-struct MarchPlane<7> {
-    static constexpr int kL = 7;
-    double c5[5];  // j-1, i-1, centre, i+1, j+1 (record order of the row in the plane)
-    __device__ __forceinline__ void load(const double* buf, int lx, int ly) {
-        c5[0] = buf[ly * kMarchHX + lx + 1];
-        c5[1] = buf[(ly + 1) * kMarchHX + lx];
-        c5[2] = buf[(ly + 1) * kMarchHX + lx + 1];
-        c5[3] = buf[(ly + 1) * kMarchHX + lx + 2];
-        c5[4] = buf[(ly + 2) * kMarchHX + lx + 1];
-    }
-    __device__ __forceinline__ double centre() const { return c5[2]; }
-    __device__ __forceinline__ double first(const StenParam& p, uint32_t m, bool f) const {
-        return march_fold<0, 1, 3>(p, &c5[2], 0.0, m, f);
-    }
-    __device__ __forceinline__ double mid(const StenParam& p, double s, uint32_t m, bool f) const {
-        return march_fold<1, 5, 3>(p, c5, s, m, f);
-    }
-    __device__ __forceinline__ double last(const StenParam& p, double s, uint32_t m, bool f) const {
-        return march_fold<6, 1, 3>(p, &c5[2], s, m, f);
-    }
-};
-
 // Streaming form: plane P, read once from shared memory, feeds three rows of
 // the thread's column -- the last records of row P-1 (which then completes),
 // the middle records of row P and the first of row P+1 -- so one plane of
 // values and two running sums (each in record order: bitwise k_sten) live in
 // registers, and a row's pattern byte / r / q load two planes before use.
-template <int ST, int OP, bool DOTS>
+template <int OP, bool DOTS>
 __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p, const MarchGeom& g, double& sa,
                                            double& sb, double& sg) {
     __shared__ double pl[kMarchBuf][kMarchPlane];
@@ -582,7 +549,7 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
         cp_async_wait<1>();  // plane P landed; P+1 may still fly
         __syncthreads();     // ... for every thread; the buffer of plane P-2 is free
         issue(P + 2);
-        MarchPlane<ST> v;
+        MarchPlane v;
         v.load(pl[(P - kb + 1) & (kMarchBuf - 1)], lx, ly);
         if (P - 1 >= kb) {  // row P-1 completes
             const double sum = v.last(p, s_old, m_old, f_old);
@@ -593,7 +560,7 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
                     sb = dadd(sb, dmul(x_old, sum));
                     sg = dadd(sg, dmul(x_old, qq_old));
                 } else {
-                    sten_store<OP, ST>(a, p, r_old, q_old, ri_old, x_old, sum);
+                    sten_store<OP, 27>(a, p, r_old, q_old, ri_old, x_old, sum);
                 }
             }
         }
@@ -608,19 +575,18 @@ __device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p
     cp_async_wait<0>();
 }
 
-template <int ST, int OP>
+template <int OP>
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<ST, OP, false>(a, p, g, sa, sb, sg);
+    march_body<OP, false>(a, p, g, sa, sb, sg);
 }
 
 // v = A w + per-CTA partials of (w.r, w.v, w.q), marching form.
-template <int ST>
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_dots(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<ST, kSpmv, true>(a, p, g, sa, sb, sg);
+    march_body<kSpmv, true>(a, p, g, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
 }
 

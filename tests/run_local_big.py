@@ -36,8 +36,9 @@ def main():
             pb._check(L.pairamg_poisson_device(rt.h, 7, nd, nd, nd, b0, b1, pb._ptr(rp), pb._ptr(ci), pb._ptr(va)))
             s = pb.Solver(rt)
             s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, 40 * nd, 40))
+            # no torch.cuda.empty_cache() here: cudaFree synchronises the device,
+            # and a peer rank may already spin on this rank's first halo push
             del rp, ci, va
-            torch.cuda.empty_cache()
             b = torch.ones(b1 - b0, dtype=torch.float64, device="cuda")
             u = torch.zeros(b1 - b0, dtype=torch.float64, device="cuda")
             st = s.solve(b, u)
