@@ -454,6 +454,16 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
         p2p_seg_destroy(rep_gather_);
     }
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
+    if (rt.shared_device()) {
+        // ranks sharing a GPU: hand the setup temporaries back now, while
+        // every rank is still inside this collective call -- later, a
+        // device-synchronising release (a caller's allocator under memory
+        // pressure) could wait on a peer's spinning halo exchange
+        PB_CUDA(cudaStreamSynchronize(s_));
+        cudaMemPool_t pool;
+        PB_CUDA(cudaDeviceGetDefaultMemPool(&pool, rt.device()));
+        PB_CUDA(cudaMemPoolTrimTo(pool, 0));
+    }
     if (rt.nranks() > 1 && p2p_)
         p2p_gather_setup(rt, dots_gather_, 4, s_);  // collective
     if (rt.nranks() > 1 && p2p_) {  // collective: every rank, every distributed level

@@ -34,13 +34,14 @@ def main():
             ci = torch.empty(nnz, dtype=torch.int64, device="cuda")
             va = torch.empty(nnz, dtype=torch.float64, device="cuda")
             pb._check(L.pairamg_poisson_device(rt.h, 7, nd, nd, nd, b0, b1, pb._ptr(rp), pb._ptr(ci), pb._ptr(va)))
-            s = pb.Solver(rt)
-            s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, 40 * nd, 40))
-            # no torch.cuda.empty_cache() here: cudaFree synchronises the device,
-            # and a peer rank may already spin on this rank's first halo push
-            del rp, ci, va
+            # every torch allocation BEFORE the setup: once a peer rank spins on
+            # this rank's first halo push, a device-synchronising call here (torch's
+            # allocator releasing cached blocks under memory pressure -> cudaFree)
+            # would wait for that spin
             b = torch.ones(b1 - b0, dtype=torch.float64, device="cuda")
             u = torch.zeros(b1 - b0, dtype=torch.float64, device="cuda")
+            s = pb.Solver(rt)
+            s.setup(n, starts, rp, ci, va, cfg=pb.SetupConfig(3, 40 * nd, 40))
             st = s.solve(b, u)
             res = {"iterations": st.iterations, "relres": st.final_relres, "levels": s.level_sizes(),
                    "reductions_per_iter": st.reductions_per_iter, "t_solve_s": st.t_solve_s}
