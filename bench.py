@@ -386,7 +386,10 @@ def bench_ours(args, rank, world, local_rank):
     peak, peak_src = measured_peaks()
     li0 = s.level_info(0)
     fmt0 = s.level_storage(0)
-    sweep_kernel = {"sten": "k_sten<kJacobi> (STEN: one pattern byte per row, uniform offsets/values)",
+    sweep_kernel = {"sten": ("k_sten_march<kJacobi> (27-point STEN, 2.5-D tiles: each x-plane once into shared "
+                             "memory by cp.async, streaming row sums)" if args.stencil == 27 else
+                             "k_sten2<kJacobi> (STEN: one pattern byte per row, uniform offsets/values, two rows "
+                             "per thread)"),
                     "pat": "k_pat<kJacobi> (PAT: one pattern byte per row)",
                     "dict": "k_sell<kJacobi> (DICT: one code byte per entry)",
                     "coded": "k_sell<kJacobi> (CODED SELL-32: one 32-bit column-delta/value-code word per entry)",
