@@ -1028,6 +1028,10 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             graph_cc_ = cc;
             graph_prec_ = precflag;
             graph_timing_ = timing;
+            // ranks sharing a GPU: nobody launches a graph whose halo waits
+            // spin while a peer is still instantiating its own (instantiation
+            // may synchronise the device)
+            if (rt.shared_device()) rt.barrier();
         }
         const bool device_loop = loop_ok && !timing && rt.nranks() == 1 && env_flag("PAIRAMG_GRAPH_LOOP", true);
         if (device_loop) {
