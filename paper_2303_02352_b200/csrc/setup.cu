@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 
 #include "amg.cuh"
@@ -29,6 +30,12 @@ using ull = unsigned long long;
 using Clock = std::chrono::steady_clock;
 
 double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+// PAIRAMG_VERBOSE: per-phase setup times on stderr (development aid)
+void trace(const Runtime& rt, const char* what, double secs) {
+    static const bool on = env_flag("PAIRAMG_VERBOSE", false);
+    if (on) std::fprintf(stderr, "rank %d setup %-28s %.4f s\n", rt.rank(), what, secs);
+}
 
 template <typename F>
 void cub_call(F&& f, cudaStream_t s) {
@@ -786,6 +793,7 @@ void extend_p_join(Runtime& rt, PExt& x, SetupStats& st) {
         halo_exchange_pair(rt, A.halo, pc.get(), pc.get() + A.n, pv.get(), pv.get() + A.n, s);
         PB_CUDA(cudaStreamSynchronize(s));
         st.t_spmm_comm += since(t0);
+        trace(rt, "P halo exchange", since(t0));
     }
 }
 
@@ -1019,6 +1027,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         const auto tc = Clock::now();
         localize(rt, L0->A, std::move(rp), std::move(gcol), std::move(val), nnz);
         h.stats.t_spmm_comm += since(tc);
+        trace(rt, "localize level 0", since(tc));
     }
     L0->w.alloc(static_cast<size_t>(L0->A.n), s);
     if (d_w0) {
@@ -1154,6 +1163,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
                 const auto tc = Clock::now();
                 localize(rt, *An, std::move(orp), std::move(ocol), std::move(oval), onnz);
                 h.stats.t_spmm_comm += since(tc);
+                trace(rt, "localize pairwise", since(tc));
                 A_pair_own = std::move(An);
                 A_pair = A_pair_own.get();
             }
@@ -1191,6 +1201,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
             const auto tc = Clock::now();
             localize(rt, Lc->A, std::move(orp), std::move(ocol), std::move(oval), onnz);
             h.stats.t_spmm_comm += since(tc);
+            trace(rt, "localize composed", since(tc));
         }
         A_pair_own.reset();
         Lc->w = std::move(w_pair);
@@ -1239,6 +1250,7 @@ void setup_hierarchy(Runtime& rt, Hierarchy& h, std::vector<int64_t> starts, DBu
         const auto tc = Clock::now();
         replicate_coarse_levels(rt, h, cfg.replicate_rows, cfg.storage);
         h.stats.t_spmm_comm += since(tc);
+        trace(rt, "replicate coarse levels", since(tc));
     }
     PB_CUDA(cudaStreamSynchronize(s));
     h.stats.t_total = since(t_start);
