@@ -14,7 +14,7 @@ timeout 400 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench7.json
 PAIRAMG_GRAPH_LOOP=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file gpurun_out/${TAG}_launches.csv python scripts/profile_solve.py --iters 2 > gpurun_out/${TAG}_ncu_l.log 2>&1 || exit 2
 PAIRAMG_GRAPH_LOOP=0 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k 'regex:k_sten2|k_update|k_restrict_c|k_prolong_c4' --launch-count 14 -o gpurun_out/${TAG}_full7 -f \
+    -k 'regex:k_sten2|k_update|k_restrict_c|k_prolong_c4' --launch-count 10 -o gpurun_out/${TAG}_full7 -f \
     python scripts/profile_solve.py --iters 2 > gpurun_out/${TAG}_ncu_f7.log 2>&1 || exit 3
 PAIRAMG_GRAPH_LOOP=0 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -k 'regex:k_sten_march' --launch-count 6 -o gpurun_out/${TAG}_full27 -f \
@@ -22,4 +22,10 @@ PAIRAMG_GRAPH_LOOP=0 timeout 900 ncu --set full --clock-control none --import-so
 PAIRAMG_GRAPH_LOOP=0 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -k 'regex:k_sell' --launch-count 4 -o gpurun_out/${TAG}_fullplain -f \
     python scripts/profile_solve.py --problem varcoef --levels 0 --format plain --iters 1 > gpurun_out/${TAG}_ncu_fp.log 2>&1 || exit 5
+# raw-page CSV exports here; the reports themselves exceed gpurun's 64 MiB copy-back
+for r in gpurun_out/${TAG}_full7 gpurun_out/${TAG}_full27 gpurun_out/${TAG}_fullplain; do
+  ncu -i $r.ncu-rep --page raw --csv > ${r}_raw.csv 2>/dev/null
+  ncu -i $r.ncu-rep --page details --csv > ${r}_details.csv 2>/dev/null
+  rm -f $r.ncu-rep
+done
 echo profile_round ok
