@@ -449,7 +449,9 @@ def bench_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return None
-    traffic = ncu_traffic("l1_jacobi_sweep_L0", workload_name(args, world), world)
+    key = "l1_jacobi_sweep_L0" + ("_27pt" if args.stencil == 27 else "") + \
+        ("_" + fmt0 if args.problem != "poisson" else "")
+    traffic = ncu_traffic(key, workload_name(args, world), world)
     return {
         "metric": METRIC, "value": t_solve, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_solve * 1e3, "higher_is_better": False,
