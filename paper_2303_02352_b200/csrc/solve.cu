@@ -29,15 +29,29 @@ __global__ void k_zero_start(const double* r, const double* d,
 }
 
 // restrict_to_coarse (cycle.cpp:64-75): rc_c = 0.0 + sum R_ci res_i, fine ascending
+// The coarse level's zero-start sweep x1 = (omega*rc)/d (cycle.cpp:49-53),
+// formed by the restriction that produced rc (one launch and one pass over
+// rc and d fewer per level and V-cycle; the same operations, bitwise).
+struct RestrictZs {
+    double* x = nullptr;  // null: no fused zero start
+    const double* d = nullptr;
+    double omega = 1.0;
+};
+
+__device__ __forceinline__ void restrict_store(double* rc, int64_t c, double s, const RestrictZs& z) {
+    rc[c] = s;
+    if (z.x) z.x[c] = ddiv(dmul(z.omega, s), z.d[c]);
+}
+
 __global__ void k_restrict(const int64_t* rrp, const int32_t* rcol,
                            const double* rval, const double* res,
-                           double* rc, int64_t nc) {
+                           double* rc, int64_t nc, RestrictZs z) {
     pdl_begin();
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     double s = 0.0;
     for (int64_t t = rrp[c]; t < rrp[c + 1]; ++t) s = dadd(s, dmul(rval[t], res[rcol[t]]));
-    rc[c] = s;
+    restrict_store(rc, c, s, z);
 }
 
 // prolongate_add (cycle.cpp:77-84): x_i = x_i + p_i * e_agg(i)
@@ -56,13 +70,13 @@ struct CodeTab {
 
 __global__ void k_restrict_c(const int64_t* rrp, const int32_t* rcol,
                              const uint8_t* rcode, const __grid_constant__ CodeTab t,
-                             const double* res, double* rc, int64_t nc) {
+                             const double* res, double* rc, int64_t nc, RestrictZs z) {
     pdl_begin();
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     double s = 0.0;
     for (int64_t k = rrp[c]; k < rrp[c + 1]; ++k) s = dadd(s, dmul(t.v[rcode[k]], res[rcol[k]]));
-    rc[c] = s;
+    restrict_store(rc, c, s, z);
 }
 
 __global__ void k_prolong_c(const int32_t* pcol, const uint8_t* pcode,
@@ -454,16 +468,7 @@ void Solver::setup(std::vector<int64_t> starts, DBuf<int64_t>&& rp, DBuf<int64_t
         p2p_seg_destroy(rep_gather_);
     }
     setup_hierarchy(rt, h, std::move(starts), std::move(rp), std::move(col), std::move(val), nnz, d_w0, cfg);
-    if (rt.shared_device()) {
-        // ranks sharing a GPU: hand the setup temporaries back now, while
-        // every rank is still inside this collective call -- later, a
-        // device-synchronising release (a caller's allocator under memory
-        // pressure) could wait on a peer's spinning halo exchange
-        PB_CUDA(cudaStreamSynchronize(s_));
-        cudaMemPool_t pool;
-        PB_CUDA(cudaDeviceGetDefaultMemPool(&pool, rt.device()));
-        PB_CUDA(cudaMemPoolTrimTo(pool, 0));
-    }
+
     if (rt.nranks() > 1 && p2p_)
         p2p_gather_setup(rt, dots_gather_, 4, s_);  // collective
     if (rt.nranks() > 1 && p2p_) {  // collective: every rank, every distributed level
@@ -689,6 +694,9 @@ void Solver::smooth(int k, bool zero_start, int nu, const double* rhs, double*& 
     if (zero_start && k == 0 && zs_pending_) {  // x1 already formed by the previous update / the solve prologue
         zs_pending_ = false;
         sweep = 1;
+    } else if (zero_start && k == zs_level_) {  // x1 formed by the restriction into this level
+        zs_level_ = -1;
+        sweep = 1;
     } else if (zero_start) {
         begin_time(-1);
         if (n) launch_k<4>(k_zero_start, blocks_for(n, 256), 256, 0, s_, rhs, L.l1.get(), xc, n, omega);
@@ -734,12 +742,19 @@ void Solver::vcycle_enqueue(int k, const double* rhs, double*& out, const CycleC
     const bool gather = h.rep_level >= 0 && k + 1 == h.rep_level;
     Level& T = gather ? *h.levels[k + 1] : lvl(k + 1);
     Level& C = lvl(k + 1);
+    RestrictZs zs;
+    if (!gather && k + 1 < h.nl() - 1 && cc.pre_sweeps >= 1) {  // level k+1 starts with a zero-start sweep
+        zs.x = C.x.get();
+        zs.d = C.l1.get();
+        zs.omega = cc.relax_weight;
+        zs_level_ = k + 1;
+    }
     if (T.A.n && !T.rcode.empty())
         launch_k<4>(k_restrict_c, blocks_for(T.A.n, 256), 256, 0, s_, T.rrp.get(), T.rcol.get(), T.rcode.get(),
-                                                             code_tab(T.rtab), L.res.get(), T.rhs.get(), T.A.n);
+                                                             code_tab(T.rtab), L.res.get(), T.rhs.get(), T.A.n, zs);
     else if (T.A.n)
         launch_k<4>(k_restrict, blocks_for(T.A.n, 256), 256, 0, s_, T.rrp.get(), T.rcol.get(), T.rval.get(), L.res.get(),
-                                                           T.rhs.get(), T.A.n);
+                                                           T.rhs.get(), T.A.n, zs);
     PB_CHECK_LAUNCH();
     launches_ += 1;
     const double* crhs = C.rhs.get();
@@ -944,6 +959,11 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "solve: setup not run");
     if (rtol <= 0.0 || max_iters < 1) fail(PAIRAMG_INVALID_ARGUMENT, "solve: need rtol > 0 and max_iters >= 1");
     cycle_warning = check_cycle(cc);
+    if (rt.nranks() > 1 && hist_.size() < static_cast<size_t>(max_iters) + 1) {
+        destroy_graph();  // the multi-rank iteration graph writes the history (k_fcg_scalars4)
+        hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
+    }
+    shared_gpu_fence();
     Level& L0 = *h.levels[0];
     for (auto& kt : ktime) kt = KernelClassTiming{};
     // Algorithmic bytes per level-0 launch of the stored format (matrix
@@ -1010,7 +1030,6 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             destroy_graph();
             cap_rtol_ = rtol;
             cap_maxit_ = max_iters;
-            if (mr) hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
             tcount_.fill(0);
             cudaGraph_t g;
             const int64_t l0 = launches_;
@@ -1111,9 +1130,18 @@ std::vector<std::string> Solver::warnings() const {
     return w;
 }
 
+// Ranks sharing one GPU (LOCAL runtime): every rank has made this call's
+// allocations (the C ABI's staging buffers, pool growth -- which may
+// synchronise the device) before any rank enqueues a kernel that spins on a
+// peer's halo flag.  Collective, like the call itself.
+void Solver::shared_gpu_fence() {
+    if (rt.shared_device()) rt.barrier();
+}
+
 void Solver::vcycle(const double* d_r, double* d_x, const CycleConfig& cc) {
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "vcycle: setup not run");
     cycle_warning = check_cycle(cc);
+    shared_gpu_fence();
     if (n_) PB_CUDA(cudaMemcpyAsync(r_.get(), d_r, 8 * n_, cudaMemcpyDeviceToDevice, s_));
     double* out = nullptr;
     const bool t = timing;
@@ -1130,6 +1158,7 @@ void Solver::vcycle(const double* d_r, double* d_x, const CycleConfig& cc) {
 void Solver::spmv(int level, const double* d_x, double* d_y) {
     if (!ready) fail(PAIRAMG_CONTRACT_VIOLATION, "spmv: setup not run");
     if (level < 0 || level >= h.nl()) fail(PAIRAMG_INVALID_ARGUMENT, "spmv: level out of range");
+    shared_gpu_fence();
     Level& L = *h.levels[level];
     if (L.A.n) PB_CUDA(cudaMemcpyAsync(L.xt.get(), d_x, 8 * L.A.n, cudaMemcpyDeviceToDevice, s_));
     const bool t = timing;

@@ -83,6 +83,7 @@ private:
     void apply_on(Level& L, const SellOpArgs& o, int kclass);
     void exchange(Level& L, const double* x, cudaStream_t st);
     bool split_launch(const Level& L) const;
+    void shared_gpu_fence();
     int interior_cap(const Level& L) const;  // CTA cap of the interior launch next to a halo exchange
     Level& lvl(int k);  // replicated copy for k >= h.rep_level, else the distributed level
     void vcycle_enqueue(int k, const double* rhs, double*& out, const CycleConfig& cc);
@@ -90,6 +91,7 @@ private:
     bool zs_fused(const CycleConfig& cc, bool precflag);
     ZeroStart zero_start_args(const CycleConfig& cc);
     bool zs_pending_ = false;  // level-0 x1 of the next V-cycle is already formed
+    int zs_level_ = -1;        // coarse level whose x1 the last restriction formed
     void reduce_dots_enqueue(bool fused_norm);
     void reduce_norm_enqueue(bool init_rr0);
     void ensure_vectors();
