@@ -228,7 +228,8 @@ def spawn_ranks(nranks: int, program, devices=None, timeout: float = 900.0):
     unless ``devices`` lists one per rank).  Returns the per-rank results in
     rank order; the first rank failure is re-raised as "rank r: ..." like the
     reference (runtime.cpp:139-151).  Ranks sharing a GPU need
-    CUDA_MODULE_LOADING=EAGER in the environment before CUDA is initialised,
+    CUDA_MODULE_LOADING=EAGER and CUDA_DEVICE_MAX_CONNECTIONS >= 2 * ranks
+    (e.g. 32) in the environment before CUDA is initialised,
     and ``program`` must not make device-synchronising CUDA calls
     (cudaFree / torch.cuda.empty_cache, cudaDeviceSynchronize) between
     library calls: a peer rank's halo wait may be running on the same GPU."""

@@ -105,6 +105,7 @@ def main(argv=None) -> int:
     if a.threads:
         # every kernel loaded up front: ranks sharing a GPU (runtime.cu)
         os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
         return run_threads(a, cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.ranks > 1 and world != a.ranks:

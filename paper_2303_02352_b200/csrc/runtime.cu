@@ -193,6 +193,22 @@ Runtime::Runtime(int device, int rank, int nranks, const uint8_t* id)
                     }
                 }
             }
+            // every rank on this GPU drives two streams; CUDA maps streams onto
+            // CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8), and two
+            // streams sharing a queue serialise -- a rank's spinning halo wait
+            // queued ahead of a peer's push would then never finish
+            int on_dev = 0;
+            for (int64_t d : devs) on_dev += d == device ? 1 : 0;
+            const char* mc = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+            const int conns = mc && *mc ? std::atoi(mc) : 8;
+            if (shared_device_ && 2 * on_dev > conns) {
+                hub_->abort("too few hardware queues for the ranks sharing a GPU");
+                fail(PAIRAMG_INVALID_ARGUMENT,
+                     "runtime: " + std::to_string(on_dev) + " ranks on one GPU need CUDA_DEVICE_MAX_CONNECTIONS >= " +
+                         std::to_string(2 * on_dev) + " (set before the process initialises CUDA; max 32): two "
+                         "streams per rank, and streams sharing a hardware queue serialise a peer's halo push "
+                         "behind a rank's wait");
+            }
             if (shared_device_ && lazy_module_loading()) {
                 hub_->abort("lazy module loading with ranks sharing a GPU");
                 fail(PAIRAMG_INVALID_ARGUMENT,

@@ -7,6 +7,8 @@ import pytest
 # tests/test_local_ranks.py); that needs every kernel loaded up front -- set
 # before anything initialises CUDA in this process (runtime.cu explains why).
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# ... and enough hardware work queues for two streams per rank (up to 16 ranks)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
