@@ -1090,7 +1090,7 @@ int launch_sten_dots(const Sell& S, const StenArgs& a0, int cap, cudaStream_t s)
             launch_k<2>(gs ? k_sten2_dots<ROWS, 7, true> : k_sten2_dots<ROWS, 7, false>, grid, 256, 0, s, a, p);
         else
             launch_k<2>(gs ? k_sten2_dots<ROWS, 27, true> : k_sten2_dots<ROWS, 27, false>, grid, 256, 0, s, a, p);
-        return grid;
+        return gs ? grid : 8 * grid;  // partial triples: per warp unless grid-striding
     }
     const StenArgs& a = a0;
     const int grid = capped(a.nblk, cap);
@@ -1605,7 +1605,11 @@ int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* 
 int sell_dots_grid(const Sell& S, int cap) {
     MarchGeom g;
     if (S.format == Sell::kSten && cap == 0 && S.rows.empty() && sten_march(S, &g)) return march_grid(g);
-    if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, sten_rpt2(S, true) ? 512 : 256), cap);
+    if (S.format == Sell::kSten && sten_rpt2(S, true)) {  // k_sten2_dots: per-warp partials unless capped
+        const int nb = blocks_for(S.nrows, 512), grid = capped(nb, cap);
+        return grid < nb ? grid : 8 * grid;
+    }
+    if (S.format == Sell::kSten) return capped(blocks_for(S.nrows, 256), cap);
     if (S.format != Sell::kPat) return blocks_for(S.nslices, kWarps);  // one warp per slice
     const int64_t want = (S.nrows + kThreads - 1) / kThreads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(kSmCount) * 8)));
