@@ -159,6 +159,7 @@ def config_dict(args, world):
         "workload": workload_name(args, world),
         "unknowns": nx * ny * nz, "stencil": args.stencil, "problem": args.problem,
         "storage": args.format, "coarse_size_target": target, "aggregation_exponent": 3,
+        "replicate_rows": args.replicate_rows if world > 1 else None,
         "sweeps": "4/4/20 l1-Jacobi", "rtol": 1e-6, "parallelism": part,
         "step": "one full FCG solve to rtol (hierarchy prebuilt)",
         "l2": "working set larger than L2 (no flush): every level-0 vector is 8*unknowns bytes (134 MB at 256^3 "
@@ -313,7 +314,7 @@ def bench_ours(args, rank, world, local_rank):
         pb._check(L.pairamg_varcoef_device(rt.h, args.stencil, nx, ny, nz, args.levels, args.seed, b0, b1,
                                            pb._ptr(rp), pb._ptr(ci), pb._ptr(va)))
     s = pb.Solver(rt)
-    cfg = pb.SetupConfig(3, target, 40, storage=args.format)
+    cfg = pb.SetupConfig(3, target, 40, storage=args.format, replicate_rows=args.replicate_rows)
 
     def barrier():
         if world > 1:
@@ -514,6 +515,8 @@ def main():
     ap.add_argument("--levels", type=int, default=2, help="varcoef: distinct cell coefficients (0 = continuous)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--format", default="auto", choices=["auto", "sten", "pat", "dict", "coded", "plain"])
+    ap.add_argument("--replicate-rows", type=int, default=2500000,
+                    help="N > 1: coarse levels with at most this many global rows are replicated on every rank")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-pipeline", dest="pipeline", action="store_false")
     ap.add_argument("--ref-sample-iters", type=int, default=3)
