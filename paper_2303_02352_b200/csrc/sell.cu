@@ -1494,6 +1494,8 @@ struct SplitPlan {
     HaloSplit h;
     int la;
     bool r2;
+    bool march;  // interior blocks are marching tiles (k_sten_march_split)
+    MarchGeom g;
     int grid;
 };
 
@@ -1501,13 +1503,14 @@ constexpr int kMaxPush = 2 * kSmCount;  // push blocks of 2048 values (8 per thr
 
 SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs) {
     SplitPlan P{};
+    P.march = sten_march(I, &P.g);
     P.la = (I.sten_L == 7 || I.sten_L == 27) && sten_center(I) ? I.sten_L : 0;
-    P.r2 = P.la != 0 && sten_rpt2(I, dots);
+    P.r2 = !P.march && P.la != 0 && sten_rpt2(I, dots);
     P.a = sten_args_of(I, P.r2 ? 512 : 256);
     P.h.pa = sten_param(I);
     P.h.pb = sten_param_w(B);
     P.h.b = sten_args_of(B);
-    P.h.nblk_a = P.a.nblk;
+    P.h.nblk_a = P.march ? march_grid(P.g) : P.a.nblk;
     P.h.nblk_b = P.h.b.nblk;
     P.grid = P.h.nblk_a + P.h.nblk_b;
     if (hs) {
@@ -1547,7 +1550,8 @@ void sell_apply_split(const Sell& I, const Sell& B, const SellOpArgs& o, const H
     }
     const bool br = !B.rows.empty();
 #define PB_SPLIT2(OP, BR)                                                                                 \
-    if (P.la == 7 && P.r2) launch_k<2>(k_sten_split<OP, 7, true, BR>, P.grid, 256, 0, s, P.a, P.h);        \
+    if (P.march) launch_k<2>(k_sten_march_split<OP, BR>, P.grid, 256, 0, s, P.a, P.h, P.g);              \
+    else if (P.la == 7 && P.r2) launch_k<2>(k_sten_split<OP, 7, true, BR>, P.grid, 256, 0, s, P.a, P.h);        \
     else if (P.la == 7) launch_k<2>(k_sten_split<OP, 7, false, BR>, P.grid, 256, 0, s, P.a, P.h);         \
     else if (P.la == 27 && P.r2) launch_k<2>(k_sten_split<OP, 27, true, BR>, P.grid, 256, 0, s, P.a, P.h);  \
     else if (P.la == 27) launch_k<2>(k_sten_split<OP, 27, false, BR>, P.grid, 256, 0, s, P.a, P.h);       \
@@ -1589,7 +1593,12 @@ int sell_spmv_dots_split(const Sell& I, const Sell& B, const double* w, double* 
         else
             launch_k<2>(kf, P.grid, 256, 0, s, P.a, P.h);
     };
-    if (P.la == 7 && P.r2)
+    if (P.march) {
+        if (br)
+            launch_k<2>(k_sten_march_split_dots<true>, P.grid, 256, 0, s, P.a, P.h, P.g);
+        else
+            launch_k<2>(k_sten_march_split_dots<false>, P.grid, 256, 0, s, P.a, P.h, P.g);
+    } else if (P.la == 7 && P.r2)
         go(k_sten_split_dots<7, true, true>, k_sten_split_dots<7, true, false>);
     else if (P.la == 7)
         go(k_sten_split_dots<7, false, true>, k_sten_split_dots<7, false, false>);

@@ -516,10 +516,9 @@ struct MarchPlane {
 // values and two running sums (each in record order: bitwise k_sten) live in
 // registers, and a row's pattern byte / r / q load two planes before use.
 template <int OP, bool DOTS>
-__device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p, const MarchGeom& g, double& sa,
-                                           double& sb, double& sg) {
+__device__ __forceinline__ void march_body(const StenArgs& a, const StenParam& p, const MarchGeom& g, int blk,
+                                           double& sa, double& sb, double& sg) {
     __shared__ double pl[kMarchBuf][kMarchPlane];
-    int blk = static_cast<int>(blockIdx.x);
     const int tx = blk % g.tiles_x;
     blk /= g.tiles_x;
     const int ty = blk % g.tiles_y;
@@ -597,14 +596,14 @@ template <int OP>
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<OP, false>(a, p, g, sa, sb, sg);
+    march_body<OP, false>(a, p, g, static_cast<int>(blockIdx.x), sa, sb, sg);
 }
 
 // v = A w + per-CTA partials of (w.r, w.v, w.q), marching form.
 __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_dots(StenArgs a, const __grid_constant__ StenParam p, MarchGeom g) {
     pdl_begin();
     double sa = 0.0, sb = 0.0, sg = 0.0;
-    march_body<kSpmv, true>(a, p, g, sa, sb, sg);
+    march_body<kSpmv, true>(a, p, g, static_cast<int>(blockIdx.x), sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
 }
 
@@ -780,7 +779,7 @@ __device__ __forceinline__ void halo_done_p2p(const HaloSplit& h) {
 // cost the interior a fifth of its warps.
 template <int OP, int LLA, bool R2, bool BROWS>
 __global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
-    pdl_wait_only();  // no early dependents: the boundary blocks wait on another GPU
+    pdl_wait_only();  // no early dependents (measured: an early trigger gains nothing here)
     // push blocks first; then (bnd_last) the interior rows, whose pass covers
     // the neighbours' pushes, and the boundary rows last, when their halo has
     // arrived -- boundary blocks dispatched early would hold SM slots while
@@ -842,6 +841,55 @@ __global__ void __launch_bounds__(256, LLA == 7 ? 5 : 2) k_sten_split_dots(StenA
     StenArgs b = h.b;
     b.hsrc = halo_wait_p2p(h);
     sten1_dots_block<BROWS, 0, true>(b, h.pb, bb, sa, sb, sg);
+    dots_block_store(sa, sb, sg, a.partials);
+    halo_done_p2p(h);
+}
+
+// The split launch with marching interior blocks (27-point levels whose
+// interior is a contiguous plane range, sten_march): push | marching tiles |
+// boundary rows, so a halo level keeps the 72-us marching sweep and still
+// needs no communication stream, pull kernel or cross-stream join.  The
+// boundary rows stay on the generic per-row path (their halo records read
+// the staging buffer).  Same 4-CTA/SM bound as k_sten_march.
+template <int OP, bool BROWS>
+__global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_split(StenArgs a, const __grid_constant__ HaloSplit h,
+                                                                            MarchGeom g) {
+    pdl_wait_only();
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (static_cast<int>(blockIdx.x) < h.npush) {
+        halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
+        return;
+    }
+    const int rel = static_cast<int>(blockIdx.x) - h.npush;
+    if (rel < h.nblk_a) {
+        march_body<OP, false>(a, h.pa, g, rel, sa, sb, sg);
+        return;
+    }
+    StenArgs b = h.b;
+    b.hsrc = halo_wait_p2p(h);
+    sten1_block<OP, BROWS, 0, true>(b, h.pb, rel - h.nblk_a);
+    halo_done_p2p(h);
+}
+
+template <bool BROWS>
+__global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_split_dots(StenArgs a, const __grid_constant__ HaloSplit h,
+                                                                                 MarchGeom g) {
+    pdl_wait_only();
+    double sa = 0.0, sb = 0.0, sg = 0.0;
+    if (static_cast<int>(blockIdx.x) < h.npush) {
+        halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
+        dots_block_store(sa, sb, sg, a.partials);
+        return;
+    }
+    const int rel = static_cast<int>(blockIdx.x) - h.npush;
+    if (rel < h.nblk_a) {
+        march_body<kSpmv, true>(a, h.pa, g, rel, sa, sb, sg);
+        dots_block_store(sa, sb, sg, a.partials);
+        return;
+    }
+    StenArgs b = h.b;
+    b.hsrc = halo_wait_p2p(h);
+    sten1_dots_block<BROWS, 0, true>(b, h.pb, rel - h.nblk_a, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
     halo_done_p2p(h);
 }

@@ -33,3 +33,17 @@ def test_distributed_parity(world, overlap):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("MP_PARITY_OK") == 5, out[-4000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_marching_split_launch(world):
+    """27-point 192 x 192 x 384: level 0's halo sweeps run the split launch with
+    marching interior blocks (tests/mp_march.py); bitwise equal to one rank."""
+    if gpu_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + world),
+           os.path.join(ROOT, "tests", "mp_march.py")]
+    r = subprocess.run(["timeout", "-k", "10", "400", *cmd], capture_output=True, text=True, timeout=500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MP_MARCH_OK" in out, out[-4000:]
