@@ -104,7 +104,8 @@ typedef struct pairamg_setup_config {
     int storage;             /* pairamg_storage; default PAIRAMG_STORAGE_AUTO.  A forced
                                 format falls back to PLAIN on rows it cannot encode. */
     int64_t replicate_rows;  /* nranks > 1: coarse levels with <= this many global rows
-                                are also held in full on every rank (default 2500000; 0 = off) */
+                                are also held in full on every rank (default 2500000; 0 = off);
+                                the first such level must also have <= 8 x this many nonzeros */
     int setup_overlap;       /* nranks > 1: P's halo exchange on the communication stream
                                 while R, w_next and the composed P are built (default 0:
                                 measured no gain) */

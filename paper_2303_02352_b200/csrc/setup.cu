@@ -887,9 +887,15 @@ void replicate_coarse_levels(Runtime& rt, Hierarchy& h, int64_t max_rows, int st
     h.rep.clear();
     if (rt.nranks() == 1) return;
     cudaStream_t s = rt.stream();
+    // replicate from the first level small in rows AND in nonzeros: a
+    // replicated level costs every rank the whole level's sweep, a
+    // distributed one a halo exchange per launch (measured at N = 2: the
+    // 27-point level 1, 1.8 M rows / 47 M nonzeros, ran 2.3x slower
+    // replicated than distributed; 7-point levels of <= 1 M rows, ~7 M
+    // nonzeros, are faster replicated)
     int kr = -1;
     for (int k = 1; k < h.nl(); ++k)
-        if (h.levels[k]->A.n_global <= max_rows) {
+        if (h.levels[k]->A.n_global <= max_rows && h.level_nnz[static_cast<size_t>(k)] <= 8 * max_rows) {
             kr = k;
             break;
         }

@@ -87,7 +87,9 @@ for e in ev:
             cut = i
             break
     nm = nm[:cut]
-    per[nm].append(float(e["dur"]))
+    g = e.get("args", {}).get("grid")
+    e["short"] = nm + (f" grid={g[0]}" if g else "")
+    per[e["short"]].append(float(e["dur"]))
 busy, end, gaps = 0.0, None, []
 for e in ev:  # union of kernel intervals (streams may overlap)
     t0, t1 = float(e["ts"]), float(e["ts"]) + float(e["dur"])
@@ -105,7 +107,9 @@ out = {"rank": rank, "world": world, "stencil": a.stencil, "nd": a.nd, "iteratio
        "gaps_over_2us": sum(1 for g in gaps if g > 2.0), "gap_hist_us": {k: sum(1 for g in gaps if lo <= g < hi)
                                                                    for k, (lo, hi) in {"<1": (0, 1), "1-2": (1, 2), "2-5": (2, 5), "5-10": (5, 10), ">=10": (10, 1e18)}.items()},
        "kernels": {k: {"count": len(v), "mean_us": sum(v) / len(v), "total_us": sum(v)}
-                   for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]))}}
+                   for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]))},
+       # the raw timeline (CUPTI host-clock timestamps: comparable across the ranks of one box)
+       "timeline": [[e["short"], float(e["ts"]), float(e["dur"])] for e in ev]}
 with open(f"gpurun_out/trace/{a.tag}_r{rank}.json", "w") as f:
     json.dump(out, f, indent=1)
 if rank == 0:
