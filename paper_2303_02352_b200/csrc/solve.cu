@@ -343,6 +343,14 @@ __global__ void __launch_bounds__(kRedThreads) k_rr_local(const double* partials
 
 // Device-side stopping test of the graph loop (same operations as the host
 // loop: rel = sqrt(rr)/sqrt(rr0); stop on rel < rtol, max_iters or breakdown).
+// Multi-rank loop: k_fcg_scalars4 (same allgathered sums in the same order on
+// every rank, so every rank stops after the same iteration) already decided.
+__global__ void k_loop_ctl_mr(const FcgState* st, cudaGraphConditionalHandle h) {
+    pdl_begin();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    cudaGraphSetConditional(h, (st->stop || st->status) ? 0u : 1u);
+}
+
 __global__ void k_loop_ctl(const FcgState* st, double rtol, int max_iters, double* hist,
                            cudaGraphConditionalHandle h) {
     pdl_begin();
@@ -419,6 +427,21 @@ void Solver::destroy_graph() {
     loop_graph_ = nullptr;
 }
 
+// The multi-rank iteration can loop on the device when nothing in it needs
+// the host: the dot allgather, every halo exchange and the replicated-level
+// gather are P2P kernels (no NCCL call), and the ranks own their GPUs (LOCAL
+// ranks sharing one keep the per-iteration launches).
+bool Solver::mr_device_loop_ok() const {
+    if (rt.shared_device() || !dots_gather_.ok) return false;
+    if (h.rep_level >= 0 && !rep_gather_.ok) return false;
+    const int nd = h.rep_level >= 0 ? h.rep_level : h.nl();
+    for (int k = 0; k < nd; ++k) {
+        const Level& L = *h.levels[static_cast<size_t>(k)];
+        if (L.A.halo.has_traffic() && !L.p2p.ok) return false;
+    }
+    return true;
+}
+
 void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol, int max_iters) {
     if (loop_graph_ && loop_cc_.pre_sweeps == cc.pre_sweeps && loop_cc_.post_sweeps == cc.post_sweeps &&
         loop_cc_.coarsest_sweeps == cc.coarsest_sweeps && loop_cc_.relax_weight == cc.relax_weight &&
@@ -426,7 +449,8 @@ void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol
         return;
     if (loop_graph_) cudaGraphExecDestroy(loop_graph_);
     loop_graph_ = nullptr;
-    hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
+    // (multi-rank: preallocated by solve(); the per-iteration graph writes it too)
+    if (hist_.size() < static_cast<size_t>(max_iters) + 1) hist_.alloc(static_cast<size_t>(max_iters) + 1, s_);
     cudaGraph_t g;
     PB_CUDA(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle handle;
@@ -442,7 +466,10 @@ void Solver::ensure_loop_graph(const CycleConfig& cc, bool precflag, double rtol
     const int64_t l0 = launches_;
     PB_CUDA(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     iteration_enqueue(cc, precflag);
-    launch_k(k_loop_ctl, 1, 32, 0, s_, state_.get(), rtol, max_iters, hist_.get(), handle);
+    if (rt.nranks() > 1)
+        launch_k(k_loop_ctl_mr, 1, 32, 0, s_, state_.get(), handle);
+    else
+        launch_k(k_loop_ctl, 1, 32, 0, s_, state_.get(), rtol, max_iters, hist_.get(), handle);
     PB_CHECK_LAUNCH();
     PB_CUDA(cudaStreamEndCapture(s_, &body));
     launches_ = l0;
@@ -1053,16 +1080,21 @@ void Solver::solve(const double* d_b, double* d_u, const CycleConfig& cc, double
             // may synchronise the device)
             if (rt.shared_device()) rt.barrier();
         }
-        const bool device_loop = loop_ok && !timing && rt.nranks() == 1 && env_flag("PAIRAMG_GRAPH_LOOP", true);
+        const bool device_loop = loop_ok && !timing && (!mr || mr_device_loop_ok()) &&
+                                 env_flag("PAIRAMG_GRAPH_LOOP", true);
         if (device_loop) {
             // the whole iteration loop as ONE graph launch: a conditional WHILE
             // node re-runs the captured iteration until k_loop_ctl clears it
+            // (multi-rank: every exchange in it is a P2P kernel, no host step)
             ensure_loop_graph(cc, precflag, rtol, max_iters);
             PB_CUDA(cudaGraphLaunch(loop_graph_, s_));
             PB_CUDA(cudaMemcpyAsync(h_state_, state_.get(), sizeof(FcgState), cudaMemcpyDeviceToHost, s_));
-            PB_CUDA(cudaStreamSynchronize(s_));
+            if (mr)
+                rt.wait(s_);  // NCCL error / deadlock polling while the loop runs
+            else
+                PB_CUDA(cudaStreamSynchronize(s_));
             it = h_state_->it;
-            launches_ += (per_iter_launches_ + 1) * it;
+            launches_ += (per_iter_launches_ + 1) * (mr ? it + 1 : it);
             if (h_state_->status) fail(PAIRAMG_BREAKDOWN, "fcg: breakdown at iteration " + std::to_string(it));
             std::vector<double> dh(static_cast<size_t>(it) + 1);
             PB_CUDA(cudaMemcpy(dh.data(), hist_.get(), 8 * (it + 1), cudaMemcpyDeviceToHost));

@@ -66,6 +66,7 @@ public:
     bool ready = false;
     bool timing = false;
     bool overlap = true;  // halo exchange overlapped with interior rows (else exchange, then all rows)
+    bool mr_device_loop_ok() const;
     bool loop_ok = true;  // single-rank solves run as one graph with a device-side stopping test
     bool p2p_ = true;         // NVLink direct-store exchanges (else NCCL)
     int halo_grid_ = 0;       // CTA cap of interior kernels on halo levels (0 = uncapped)
