@@ -684,18 +684,21 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_solve(StenArgs a, con
 
 // ---------------------------------------------------------------------------
 // Interior + halo-boundary rows of a halo level in ONE launch, with the halo
-// delivered by NVLink direct stores (p2p.cu).  Block order (bnd_last = 1, the
-// default): push | interior | boundary.  The push blocks (lowest ids,
-// dispatched first) store this rank's boundary values into the neighbours'
-// staging and raise their flags; they never wait.  The interior blocks never
-// wait either.  Only the boundary blocks (highest ids) wait, for every
+// delivered by NVLink direct stores (p2p.cu).  Block order: push |
+// interior[0, bnd_at) | boundary | interior[bnd_at, nblk_a), bnd_at = two
+// resident waves before the end of the interior.  The push blocks (lowest
+// ids, dispatched first) store this rank's boundary values into the
+// neighbours' staging and raise their flags; they never wait.  The interior
+// blocks never wait either.  Only the boundary blocks wait, for every
 // neighbour's flag of this exchange, then gather halo columns straight from
-// the staging slot of its parity.  No circular wait: a neighbour's push for
-// exchange k sits in the first blocks of its own launch k, which depends only
-// on its exchange k-1 having completed (its boundary blocks of k-1 waited for
-// OUR push k-1, already done); waiting boundary blocks here hold SM slots only
-// after every non-waiting block of this grid was dispatched, and the
-// neighbour's GPU is a different device.  (Ranks sharing one GPU -- LOCAL
+// the staging slot of its parity; dispatched late in the grid their halo has
+// normally arrived, and the last interior waves overlap them instead of a
+// serial boundary tail.  No circular wait: a neighbour's push for exchange k
+// sits in the first blocks of its own launch k, which depends only on its
+// exchange k-1 having completed (its boundary blocks of k-1 waited for OUR
+// push k-1, already done); the blocks of this grid that a waiting boundary
+// block could delay never wait themselves, and the neighbour's GPU is a
+// different device.  (Ranks sharing one GPU -- LOCAL
 // runtime -- do not use this launch: Solver::split_launch.)  The last
 // boundary block advances the exchange counter (read by the next push).
 struct HaloSplit {
@@ -713,7 +716,8 @@ struct HaloSplit {
     // the neighbours' staging, then [npush, npush + nblk_b) are the boundary
     // rows and the rest the interior
     int npush, npeers;
-    int bnd_last;              // block order push | interior | boundary (else push | boundary | interior)
+    int bnd_at;                // interior blocks before the boundary blocks (block order
+                               // push | interior[0, bnd_at) | boundary | interior[bnd_at, nblk_a))
     int64_t off[9];
     double* dst[8];
     int64_t stride[8];
@@ -744,6 +748,17 @@ __device__ __forceinline__ void halo_push_block(const HaloSplit& h, const double
         for (int p = 0; p < h.npeers; ++p)
             asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(h.pflag[p]), "l"(e + 1) : "memory");
     }
+}
+
+// Block rel (past the push blocks) -> boundary block index, or -1 with the
+// interior block index in blk.
+__device__ __forceinline__ int split_bnd_index(const HaloSplit& h, int rel, int& blk) {
+    blk = rel;
+    if (rel < h.bnd_at) return -1;
+    const int bb = rel - h.bnd_at;
+    if (bb < h.nblk_b) return bb;
+    blk = rel - h.nblk_b;
+    return -1;
 }
 
 __device__ __forceinline__ const double* halo_wait_p2p(const HaloSplit& h) {
@@ -780,18 +795,17 @@ __device__ __forceinline__ void halo_done_p2p(const HaloSplit& h) {
 template <int OP, int LLA, bool R2, bool BROWS>
 __global__ void __launch_bounds__(256, LLA == 7 ? 5 : 1) k_sten_split(StenArgs a, const __grid_constant__ HaloSplit h) {
     pdl_wait_only();  // no early dependents (measured: an early trigger gains nothing here)
-    // push blocks first; then (bnd_last) the interior rows, whose pass covers
-    // the neighbours' pushes, and the boundary rows last, when their halo has
-    // arrived -- boundary blocks dispatched early would hold SM slots while
+    // push blocks first; then most of the interior rows, whose pass covers
+    // the neighbours' pushes, and the boundary rows once their halo has
+    // arrived -- boundary blocks dispatched first would hold SM slots while
     // they wait (measured +25-30 us per level-0 sweep at 4 GPUs)
     if (static_cast<int>(blockIdx.x) < h.npush) {
         halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
         return;
     }
-    const int rel = static_cast<int>(blockIdx.x) - h.npush;
-    const int bb = h.bnd_last ? rel - h.nblk_a : rel;
-    const int blk = h.bnd_last ? rel : rel - h.nblk_b;
-    if (h.bnd_last ? bb < 0 : blk >= 0) {
+    int blk;
+    const int bb = split_bnd_index(h, static_cast<int>(blockIdx.x) - h.npush, blk);
+    if (bb < 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
             const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
@@ -820,10 +834,9 @@ __global__ void __launch_bounds__(256, LLA == 7 ? 5 : 2) k_sten_split_dots(StenA
         dots_block_store(sa, sb, sg, a.partials);
         return;
     }
-    const int rel = static_cast<int>(blockIdx.x) - h.npush;  // then interior / boundary as k_sten_split
-    const int bb = h.bnd_last ? rel - h.nblk_a : rel;
-    const int blk = h.bnd_last ? rel : rel - h.nblk_b;
-    if (h.bnd_last ? bb < 0 : blk >= 0) {
+    int blk;  // then interior / boundary as k_sten_split
+    const int bb = split_bnd_index(h, static_cast<int>(blockIdx.x) - h.npush, blk);
+    if (bb < 0) {
         if constexpr (R2) {
             const int ia = blk * 512 + static_cast<int>(threadIdx.x);
             const bool edge = blk < a.safe_lo || blk >= a.safe_hi;
@@ -860,14 +873,15 @@ __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_split(StenA
         halo_push_block(h, a.x, static_cast<int>(blockIdx.x));
         return;
     }
-    const int rel = static_cast<int>(blockIdx.x) - h.npush;
-    if (rel < h.nblk_a) {
-        march_body<OP, false>(a, h.pa, g, rel, sa, sb, sg);
+    int blk;
+    const int bb = split_bnd_index(h, static_cast<int>(blockIdx.x) - h.npush, blk);
+    if (bb < 0) {
+        march_body<OP, false>(a, h.pa, g, blk, sa, sb, sg);
         return;
     }
     StenArgs b = h.b;
     b.hsrc = halo_wait_p2p(h);
-    sten1_block<OP, BROWS, 0, true>(b, h.pb, rel - h.nblk_a);
+    sten1_block<OP, BROWS, 0, true>(b, h.pb, bb);
     halo_done_p2p(h);
 }
 
@@ -881,15 +895,16 @@ __global__ void __launch_bounds__(256, kMarchMinBlocks) k_sten_march_split_dots(
         dots_block_store(sa, sb, sg, a.partials);
         return;
     }
-    const int rel = static_cast<int>(blockIdx.x) - h.npush;
-    if (rel < h.nblk_a) {
-        march_body<kSpmv, true>(a, h.pa, g, rel, sa, sb, sg);
+    int blk;
+    const int bb = split_bnd_index(h, static_cast<int>(blockIdx.x) - h.npush, blk);
+    if (bb < 0) {
+        march_body<kSpmv, true>(a, h.pa, g, blk, sa, sb, sg);
         dots_block_store(sa, sb, sg, a.partials);
         return;
     }
     StenArgs b = h.b;
     b.hsrc = halo_wait_p2p(h);
-    sten1_dots_block<BROWS, 0, true>(b, h.pb, rel - h.nblk_a, sa, sb, sg);
+    sten1_dots_block<BROWS, 0, true>(b, h.pb, bb, sa, sb, sg);
     dots_block_store(sa, sb, sg, a.partials);
     halo_done_p2p(h);
 }
