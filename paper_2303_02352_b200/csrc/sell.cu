@@ -1538,11 +1538,10 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
     // the end of the interior -- their halo has long arrived at level 0 (the
     // neighbours push at their launch start) and they no longer form a
     // serial tail after the last interior wave (7-point N = 2: 72.3 -> 71.5
-    // ms; PAIRAMG_BND_TAIL waves, 0 = boundary last).  Marching interiors
-    // keep the boundary last (two waves early: 42.6 -> 46.6 ms, 27-point).
-    static const int tail_waves = env_int("PAIRAMG_BND_TAIL", 2);
+    // ms).  Marching interiors keep the boundary last (two waves early:
+    // 42.6 -> 46.6 ms, 27-point).
     const int resident = kSmCount * (P.la == 7 ? 5 : 2);
-    P.h.bnd_at = P.march ? P.h.nblk_a : std::max(0, P.h.nblk_a - tail_waves * resident);
+    P.h.bnd_at = P.march ? P.h.nblk_a : std::max(0, P.h.nblk_a - 2 * resident);
     P.grid = P.h.npush + P.h.nblk_a + P.h.nblk_b;
     return P;
 }

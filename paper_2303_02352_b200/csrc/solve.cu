@@ -636,12 +636,10 @@ void Solver::exchange(Level& L, const double* x, cudaStream_t st) {
 // neighbours' pushes.  Not when ranks share a GPU (LOCAL runtime): a grid
 // whose last blocks wait on a peer's kernel could hold every SM slot.
 // Interior rows that run the 27-point marching kernels keep them inside the
-// split launch (k_sten_march_split); PAIRAMG_MARCH_SPLIT=0 puts those levels
-// back on the exchange-on-the-communication-stream schedule.
+// split launch (k_sten_march_split; the level-0 sweep at N = 2: 74 us vs
+// 81.9 with the exchange on the communication stream).
 bool Solver::split_launch(const Level& L) const {
-    static const bool march_split = env_flag("PAIRAMG_MARCH_SPLIT", true);
-    return L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) && !rt.shared_device() &&
-           (march_split || !sell_march_ok(L.sell_int));
+    return L.p2p.ok && L.A.halo.n_halo > 0 && sell_split_ok(L.sell_int, L.split_bnd()) && !rt.shared_device();
 }
 
 int Solver::interior_cap(const Level& L) const { return sell_march_ok(L.sell_int) ? 0 : halo_grid_; }

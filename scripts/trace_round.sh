@@ -8,6 +8,5 @@ for st in 7 27; do
   PAIRAMG_GRAPH_LOOP=0 timeout 300 python scripts/trace_solve.py --stencil $st --nd $nd --tag n1_$st 2>&1 | tail -1
   timeout 300 $TR scripts/trace_solve.py --stencil $st --nd $nd --tag n2_$st 2>&1 | grep -v "^\*\|OMP" | tail -1
 done
-PAIRAMG_MARCH_SPLIT=0 timeout 300 $TR scripts/trace_solve.py --stencil 27 --nd 192 --tag n2_27_nomsplit 2>&1 | tail -1
 timeout 300 $TR scripts/trace_solve.py --stencil 27 --nd 192 --replicate-rows 1000000 --tag n2_27_rep1m 2>&1 | tail -1
 echo trace done
