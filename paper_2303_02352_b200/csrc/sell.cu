@@ -1499,7 +1499,13 @@ struct SplitPlan {
     int grid;
 };
 
-constexpr int kMaxPush = 2 * kSmCount;  // push blocks of 2048 values (8 per thread)
+// Push blocks: kPushVals values each (2 per thread: the push is on the
+// neighbour's critical path -- the 2.1 M-row level 1 at N = 2 runs its V-cycle
+// share in 181 vs 199 us/iter with 512 vs 2048 per block), at most kMaxPush
+// (more push blocks at level 0 took SM slots from the interior: 7-point
+// level 0 807-836 vs 800 us/iter uncapped).
+constexpr int kPushVals = 512;
+constexpr int kMaxPush = 32;
 
 SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs) {
     SplitPlan P{};
@@ -1523,7 +1529,8 @@ SplitPlan split_plan(const Sell& I, const Sell& B, bool dots, const HaloSrc* hs)
         P.h.b.nown = static_cast<int>(I.xlen - hs->nhalo);
         if (hs->fused) {  // push blocks ahead of the boundary blocks
             const int64_t nsend = hs->off[hs->npeers];
-            P.h.npush = static_cast<int>(std::min<int64_t>(kMaxPush, std::max<int64_t>(1, (nsend + 2047) / 2048)));
+            P.h.npush = static_cast<int>(
+                std::min<int64_t>(kMaxPush, std::max<int64_t>(1, (nsend + kPushVals - 1) / kPushVals)));
             P.h.npeers = hs->npeers;
             for (int i = 0; i <= hs->npeers; ++i) P.h.off[i] = hs->off[i];
             for (int i = 0; i < hs->npeers; ++i) {
