@@ -741,12 +741,19 @@ __device__ __forceinline__ void halo_push_block(const HaloSplit& h, const double
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&h.ctr[5], 1ull) == static_cast<unsigned long long>(h.npush) - 1) {
-        h.ctr[5] = 0;
-        h.ctr[4] = e + 1;
-        __threadfence_system();
-        for (int p = 0; p < h.npeers; ++p)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(h.pflag[p]), "l"(e + 1) : "memory");
+    // every push block's stores are system-visible (its fence) before its
+    // count; the last block's acq_rel count therefore follows all of them,
+    // and its flag store needs no second system fence (~3 us of the level-1
+    // launch's critical path under the interior's HBM load)
+    if (threadIdx.x == 0) {
+        unsigned long long prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(h.ctr + 5) : "memory");
+        if (prev == static_cast<unsigned long long>(h.npush) - 1) {
+            h.ctr[5] = 0;
+            h.ctr[4] = e + 1;
+            for (int p = 0; p < h.npeers; ++p)
+                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.pflag[p]), "l"(e + 1) : "memory");
+        }
     }
 }
 
