@@ -31,6 +31,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p) {
+    unsigned long long prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(p) : "memory");
+    return prev;
+}
 
 // Every rank pushes its boundary values into each neighbour's staging slot of
 // parity (exchange count & 1); the last CTA raises the neighbours' flags.
@@ -46,11 +54,13 @@ __global__ void __launch_bounds__(256) k_p2p_push(const double* x, const int32_t
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&ctr[5], 1ull) == gridDim.x - 1) {
+    // every block's stores are system-visible (its fence) before its count;
+    // the last block's acq_rel count follows all of them, so its flag
+    // stores need no second system fence (as halo_push_block)
+    if (threadIdx.x == 0 && atom_add_acq_rel(&ctr[5]) == gridDim.x - 1) {
         ctr[5] = 0;
         ctr[4] = e + 1;
-        __threadfence_system();
-        for (int p = 0; p < pa.npeers; ++p) st_release_sys(pa.flag[p], e + 1);
+        for (int p = 0; p < pa.npeers; ++p) st_relaxed_sys(pa.flag[p], e + 1);
     }
 }
 
@@ -411,10 +421,10 @@ __global__ void __launch_bounds__(256) k_seg_gather(const double* src, int64_t c
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1ull) == gridDim.x - 1) {
+    if (threadIdx.x == 0 && atom_add_acq_rel(&ctr[1]) == gridDim.x - 1) {  // see k_p2p_push
         ctr[1] = 0;
         for (int r = 0; r < a.nranks; ++r)
-            if (r != a.rank) st_release_sys(a.flag[r] + a.rank, e + 1);
+            if (r != a.rank) st_relaxed_sys(a.flag[r] + a.rank, e + 1);
         for (int r = 0; r < a.nranks; ++r) {
             if (r == a.rank) continue;
             long long spins = 0;
